@@ -1,0 +1,143 @@
+/*
+ * coverblip_b200.h -- C ABI of libcoverblip_b200.so, the B200 (sm_100a) hot path
+ * of the CoverBLIP exact-projection IPG reconstruction (arXiv 1810.01967).
+ *
+ * All array arguments are DEVICE pointers (CUDA global memory) unless named
+ * *_host; `stream` is a cudaStream_t (NULL = legacy default stream).  Complex
+ * arrays are interleaved (re, im): complex64 = float2, complex128 = double2,
+ * row-major, voxel-major (row v = voxel v), exactly the numpy layouts of the
+ * reference.  Every function returns 0 on success; 1 = bad argument (the
+ * Python shim raises ValueError), 2 = CUDA error, 3 = unsupported shape,
+ * 4 = cuFFT error.  cbb_last_error() returns the last message (thread-local).
+ *
+ * Functions are re-entrant: no global mutable state besides per-plan objects
+ * owned by the caller (reference SURVEY 8b "Threading").
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/coverblip):
+ *   cbb_project_cone_exact  <- projection.py:45-67  project_cone_exact(Z, dictionary)
+ *                              (+ projection.py:38-42 _gammas_for, :64 write-back)
+ *   cbb_project_step        <- solver.py:128-130   proj = project_fn(X - mu*G); dX; ||dX||^2
+ *   cbb_dict_prepare        <- projection.py:26-29 _atoms_of (device copy of .atoms /
+ *                              .atoms_compressed, done once per dictionary)
+ *   cbb_op_*                <- forward_model.py:123-167 ForwardOperator.apply/adjoint
+ *                              (cartesian_dft) and dictionary.py:116-122 compress/decompress
+ *   cbb_residual, cbb_norm2_c64, cbb_scaled_residual_norm2
+ *                           <- solver.py:130,135,180-190 (np.linalg.norm(.)**2 reductions)
+ *   cbb_argmax_select       <- projection.py:62 np.argmax across atom shards (multi-GPU)
+ */
+#ifndef COVERBLIP_B200_H_
+#define COVERBLIP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define CBB_ABI_VERSION 1
+
+/* Device view of a prepared dictionary (filled by cbb_dict_prepare). */
+typedef struct cbb_dict_view {
+  int64_t d;          /* number of atoms */
+  int32_t s;          /* complex dimension of an atom (L, or s when compressed) */
+  int32_t s_pad;      /* FFMA register width */
+  int32_t kpad;       /* tensor-core K (32 or 64) */
+  int32_t n_btiles;   /* ceil(d / 128) */
+  const void* atoms64;   /* d x s complex128 */
+  const void* atoms32;   /* d x 2*s_pad fp32 planar */
+  const void* atoms_tc;  /* bf16 UMMA tiles */
+  const float* bounds;   /* certified error bounds */
+} cbb_dict_view;
+
+/* Projection algorithms. */
+enum { CBB_ALGO_AUTO = 0, CBB_ALGO_TCGEN05 = 1, CBB_ALGO_FFMA = 2, CBB_ALGO_EXHAUSTIVE = 3 };
+
+int cbb_abi_version(void);
+const char* cbb_last_error(void);
+int cbb_device_sm_count(int* out);
+
+/* ---- dictionary (projection.py:26-29) ---- */
+size_t cbb_dict_storage_bytes(int64_t d, int32_t s);
+int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s, void* storage,
+                     cbb_dict_view* view_out, void* stream);
+
+/* ---- exact cone projection (projection.py:45-67) ---- */
+size_t cbb_project_workspace_bytes(int64_t n, int32_t s);
+/* z: n x s complex (c128 if z_c128 else c64).  Outputs (any may be NULL):
+ * idx_out int64 (idx_int64=1) or int32, gamma_out fp64, proj_out c128 (proj_c128=1) or c64. */
+int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
+                           void* idx_out, int32_t idx_int64, double* gamma_out, void* proj_out,
+                           int32_t proj_c128, void* workspace, size_t workspace_bytes,
+                           int32_t algo, void* stream);
+/* One IPG trial (solver.py:128-130): Z = X - mu*G (c64, written to z_out), project,
+ * X' = proj (c64), dX = X' - X (c64), nd_out[0] = ||dX||^2 (fp64, deterministic). */
+int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64_t n,
+                     const cbb_dict_view* dict, int32_t* idx_out, double* gamma_out,
+                     void* xnext_out, void* dx_out, double* nd_out, void* workspace,
+                     size_t workspace_bytes, int32_t algo, void* stream);
+/* Number of voxels that needed the exhaustive fp64 rescan in the last call (synchronises). */
+int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count_host,
+                               void* stream);
+/* Bring-up / test hook: prologue only (bf16 voxel tiles + windows in the workspace). */
+int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
+                         void* workspace, size_t workspace_bytes, void* stream);
+/* Bring-up / test hook: raw tcgen05 bf16 scores of voxel tile a_tile x atom tile b_tile
+ * (128 x 128 fp32, row = voxel) from the workspace voxel tiles. */
+int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_tile,
+                        int32_t b_tile, float* out, void* stream);
+
+/* ---- Cartesian operator (forward_model.py:123-167) + subspace maps (dictionary.py:116-122) ---- */
+typedef struct cbb_op cbb_op;
+/* spatial dims (ndim 2 or 3), L frames, m samples per frame, pattern (L x m int32 device). */
+int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const int32_t* pattern,
+                  cbb_op** out);
+int cbb_op_destroy(cbb_op* op);
+size_t cbb_op_workspace_bytes(const cbb_op* op);
+/* Y = A X.  X: n x L complex64 voxel-major (reference layout); Y: L x m complex64
+ * FRAME-major (Y_fm[t][i] = Y_ref[i][t]; the Python shim transposes at the boundary). */
+int cbb_op_apply(cbb_op* op, const void* X, void* Y, void* workspace, void* stream);
+/* X = A^H Y. */
+int cbb_op_adjoint(cbb_op* op, const void* Y, void* X, void* workspace, void* stream);
+/* Compressed chain: Y = A(Xc V^H) with Xc n x s c64, V L x s c64 (basis), Y frame-major. */
+int cbb_op_apply_compressed(cbb_op* op, const void* Xc, const void* V, int32_t s, void* Y,
+                            void* workspace, void* stream);
+/* ||A(Xc V^H)||^2 only (apply_diff norm, solver.py:135) -> norm_out[0] fp64. */
+int cbb_op_apply_norm2_compressed(cbb_op* op, const void* Xc, const void* V, int32_t s,
+                                  double* norm_out, void* workspace, void* stream);
+/* Gc = (A^H R) V for a frame-major residual R (L x m, already weighted). */
+int cbb_op_adjoint_compressed(cbb_op* op, const void* R, const void* V, int32_t s, void* Gc,
+                              void* workspace, void* stream);
+
+/* ---- small fused vector kernels ---- */
+/* R = a - b (complex64, count elements); optional fp64 ||R||^2 (weights w fp32 or NULL). */
+int cbb_residual(const void* a, const void* b, int64_t count, const float* w, void* R,
+                 double* norm_out, void* workspace, void* stream);
+/* out = ||alpha*a - b||^2 (complex64, count elements, fp64 deterministic). */
+int cbb_scaled_residual_norm2(const void* a, double alpha, const void* b, int64_t count,
+                              const float* w, double* norm_out, void* workspace, void* stream);
+/* out = ||a||^2 (complex64). */
+int cbb_norm2_c64(const void* a, int64_t count, double* norm_out, void* workspace, void* stream);
+/* a *= alpha (complex64, in place). */
+int cbb_scale_c64(void* a, double alpha, int64_t count, void* stream);
+size_t cbb_reduce_workspace_bytes(void);
+
+/* ---- multi-GPU atom sharding: exact (max score, lowest index) combine ---- */
+/* After an all-reduce MAX of the per-rank best fp64 scores (gmax), each rank emits
+ * cand[v] = (score[v] == gmax[v]) ? gidx[v] : INT64_MAX; an all-reduce MIN of cand then
+ * yields the global first-index argmax (projection.py:62 semantics across atom shards). */
+int cbb_argmax_select(const double* score, const int64_t* gidx, const double* gmax, int64_t n,
+                      int64_t* cand_out, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COVERBLIP_B200_H_ */

@@ -1,0 +1,207 @@
+// Shared device helpers for the CoverBLIP B200 hot path (sm_100a only).
+//
+// PTX wrappers for mbarriers, bulk async copies (TMA engine, SASS UBLKCP),
+// tcgen05 (TMEM alloc / MMA / commit / ld) and the exact fp64 rescoring used
+// by every matched-filter variant.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "coverblip_b200 is written for sm_100a only"
+#endif
+
+namespace cbb {
+
+// ---------------------------------------------------------------- status
+enum Status : int {
+  kOk = 0,
+  kErrArgument = 1,   // maps to ValueError in the Python shim
+  kErrCuda = 2,
+  kErrUnsupported = 3,
+  kErrCufft = 4,
+};
+
+#define CBB_CUDA_TRY(expr)                                  \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) {                                \
+      cbb::set_last_error(cudaGetErrorString(_e));          \
+      return cbb::kErrCuda;                                 \
+    }                                                       \
+  } while (0)
+
+void set_last_error(const char* msg);
+
+// ---------------------------------------------------------------- layout
+// Tensor-core operand rows: K_PAD bf16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, 0..]
+// stored in 128-row tiles with the UMMA K-major SWIZZLE_64B (K_PAD=32) or
+// SWIZZLE_128B (K_PAD=64) canonical layout so a flat bulk copy lands a tile in
+// shared memory ready for tcgen05.mma.
+constexpr int kTileRows = 128;
+
+__host__ __device__ inline int kpad_for(int s) { return (2 * s <= 32) ? 32 : 64; }
+
+// Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.
+__host__ __device__ inline uint32_t tile_chunk_offset(int r, int c, int kpad) {
+  if (kpad == 32) {  // 64 B rows, Swizzle<2,4,3>: chunk bits [4,6) ^= addr bits [7,9)
+    return uint32_t(r) * 64u + uint32_t((c ^ ((r >> 1) & 3)) * 16);
+  }
+  // 128 B rows, Swizzle<3,4,3>: chunk bits [4,7) ^= addr bits [7,10)
+  return uint32_t(r) * 128u + uint32_t((c ^ (r & 7)) * 16);
+}
+
+// ---------------------------------------------------------------- misc device
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+__device__ __forceinline__ unsigned short bf16_bits_rn(float x) {
+  __nv_bfloat16 h = __float2bfloat16_rn(x);
+  return *reinterpret_cast<unsigned short*>(&h);
+}
+__device__ __forceinline__ float bf16_bits_to_float(unsigned short b) {
+  return __uint_as_float(uint32_t(b) << 16);
+}
+
+// ---------------------------------------------------------------- mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- bulk copy (TMA engine)
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---------------------------------------------------------------- tcgen05
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate).
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets lane (base_lane + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+// UMMA shared-memory descriptor, K-major, swizzled rows (SBO = 8 rows).
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, int kpad) {
+  const uint32_t row_bytes = uint32_t(kpad) * 2u;
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFFu);           // start address
+  d |= uint64_t(1u) << 16;                             // LBO (unused for swizzled K-major)
+  d |= uint64_t(((8u * row_bytes) >> 4) & 0x3FFFu) << 32;  // SBO: 8-row group stride
+  d |= uint64_t(1u) << 46;                             // descriptor version (sm_100)
+  const uint64_t layout = (kpad == 32) ? 4u /*SWIZZLE_64B*/ : 2u /*SWIZZLE_128B*/;
+  d |= layout << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A/B = BF16, D = F32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------- exact scoring
+// Re<z, d_j> in fp64 over the 2s real components, z given as fp64 re/im.
+template <int S>
+__device__ __forceinline__ double exact_score(const double (&zr)[S], const double (&zi)[S],
+                                              const double2* __restrict__ atom) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    double2 a = atom[k];
+    acc = fma(zr[k], a.x, acc);
+    acc = fma(zi[k], a.y, acc);
+  }
+  return acc;
+}
+
+}  // namespace cbb

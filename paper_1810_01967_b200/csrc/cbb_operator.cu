@@ -1,0 +1,418 @@
+// Cartesian acquisition operator A = P_Omega F (unitary DFT per frame) on B200,
+// plus the SVD-subspace maps and the fused reductions that drive the IPG step rule.
+//
+// Reference: coverblip/forward_model.py:123-167 (apply/adjoint, cartesian_dft, c = 1),
+//            coverblip/dictionary.py:116-122 (compress = rows @ V, decompress = rows @ V^H),
+//            coverblip/solver.py:130,135,180-190 (squared norms, residual, weighted residual).
+//
+// Internal layout: frame-major.  A frame stack is (L, n) complex64 with n = prod(dims) in C
+// order (v = row*w + col, forward_model.py:138), so cuFFT runs one batched C2C over L
+// contiguous frames; measurements are (L, m) complex64 (frame t, sample i -> Omega_t(i)).
+// The unitary 1/sqrt(n) is folded into the gather / compress kernels.
+#include "cbb_common.cuh"
+
+#include <cufft.h>
+#include <cmath>
+#include <new>
+
+namespace cbb {
+
+constexpr int kRedBlocks = 256;
+
+// ---------------------------------------------------------------- reductions (deterministic)
+__device__ __forceinline__ double block_sum_256(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) finish_sum(const double* __restrict__ partial, int np,
+                                                  double* __restrict__ out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += 256) acc += partial[i];
+  double r = block_sum_256(acc, sh);
+  if (threadIdx.x == 0) *out = r;
+}
+
+// ---------------------------------------------------------------- subspace maps
+// F[t][v] = sum_k Xc[v][k] * conj(V[t][k])    (decompress, dictionary.py:122)
+__global__ void __launch_bounds__(256) decompress_frames_kernel(const float2* __restrict__ Xc,
+                                                                const float2* __restrict__ V,
+                                                                int s, int64_t n, int L,
+                                                                int t_per_block,
+                                                                float2* __restrict__ F) {
+  extern __shared__ float2 sV[];  // t_per_block x s
+  const int t0 = blockIdx.y * t_per_block;
+  const int tn = min(t_per_block, L - t0);
+  for (int i = threadIdx.x; i < tn * s; i += blockDim.x) sV[i] = V[size_t(t0) * s + i];
+  __syncthreads();
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  float2 x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = (k < s) ? Xc[v * s + k] : make_float2(0.f, 0.f);
+  for (int tt = 0; tt < tn; ++tt) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k < s) {
+        const float2 b = sV[tt * s + k];
+        // x * conj(b)
+        re = fmaf(x[k].x, b.x, fmaf(x[k].y, b.y, re));
+        im = fmaf(x[k].y, b.x, fmaf(-x[k].x, b.y, im));
+      }
+    }
+    F[size_t(t0 + tt) * n + v] = make_float2(re, im);
+  }
+}
+
+// Gc[v][k] = scale * sum_t F[t][v] * V[t][k]    (compress, dictionary.py:118)
+__global__ void __launch_bounds__(256) compress_frames_kernel(const float2* __restrict__ F,
+                                                              const float2* __restrict__ V,
+                                                              int s, int64_t n, int L,
+                                                              float scale,
+                                                              float2* __restrict__ Gc) {
+  constexpr int TB = 64;
+  __shared__ float2 sV[TB * 32];
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  float2 acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = make_float2(0.f, 0.f);
+  for (int t0 = 0; t0 < L; t0 += TB) {
+    const int tn = min(TB, L - t0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < tn * s; i += blockDim.x) sV[i] = V[size_t(t0) * s + i];
+    __syncthreads();
+    if (v < n) {
+      for (int tt = 0; tt < tn; ++tt) {
+        const float2 f = F[size_t(t0 + tt) * n + v];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          if (k < s) {
+            const float2 b = sV[tt * s + k];
+            acc[k].x = fmaf(f.x, b.x, fmaf(-f.y, b.y, acc[k].x));
+            acc[k].y = fmaf(f.x, b.y, fmaf(f.y, b.x, acc[k].y));
+          }
+        }
+      }
+    }
+  }
+  if (v < n) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < s) Gc[v * s + k] = make_float2(acc[k].x * scale, acc[k].y * scale);
+  }
+}
+
+// Voxel-major (n, L) <-> frame-major (L, n) transposes with scaling.
+__global__ void transpose_kernel(const float2* __restrict__ in, int64_t rows, int64_t cols,
+                                 float scale, float2* __restrict__ out) {
+  __shared__ float2 tile[32][33];
+  const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      float2 x = tile[threadIdx.x][i];
+      out[c * rows + r] = make_float2(x.x * scale, x.y * scale);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sampling
+// mode 0: Y[t][i] = scale * F[t][Omega_t(i)]
+// mode 1: partial ||scale * F[Omega]||^2 only (apply_diff denominator, solver.py:135)
+// mode 2: R[t][i] = scale * F[t][Omega] - Ymeas[t][i] (+ partial of w*|R|^2), R stored as w*R
+__global__ void __launch_bounds__(256) gather_kernel(const float2* __restrict__ F,
+                                                     const int* __restrict__ pat, int64_t n,
+                                                     int L, int m, float scale, int mode,
+                                                     const float2* __restrict__ Ymeas,
+                                                     const float* __restrict__ w,
+                                                     float2* __restrict__ Y,
+                                                     double* __restrict__ partial) {
+  __shared__ double sh[256];
+  const int64_t total = int64_t(L) * m;
+  double acc = 0.0;
+  for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * 256) {
+    const int64_t t = e / m;
+    const float2 f = F[t * n + pat[e]];
+    float2 y = make_float2(f.x * scale, f.y * scale);
+    if (mode == 2) {
+      const float2 ym = Ymeas[e];
+      y.x -= ym.x;
+      y.y -= ym.y;
+      const float ww = w ? w[e] : 1.f;
+      acc += double(ww) * (double(y.x) * y.x + double(y.y) * y.y);
+      Y[e] = make_float2(ww * y.x, ww * y.y);
+    } else {
+      if (mode == 0) Y[e] = y;
+      acc += double(y.x) * y.x + double(y.y) * y.y;
+    }
+  }
+  if (partial) {
+    double r = block_sum_256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+  }
+}
+
+// K[t][Omega_t(i)] = R[t][i]   (put_along_axis zero-fill, forward_model.py:160-162); K zeroed first
+__global__ void __launch_bounds__(256) scatter_kernel(const float2* __restrict__ R,
+                                                      const int* __restrict__ pat, int64_t n,
+                                                      int L, int m, float2* __restrict__ K) {
+  const int64_t total = int64_t(L) * m;
+  for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * 256) {
+    const int64_t t = e / m;
+    K[t * n + pat[e]] = R[e];
+  }
+}
+
+// ---------------------------------------------------------------- elementwise + norms
+// mode 0: R = a - b, partial w|R|^2 ; mode 1: partial only of w|alpha a - b|^2 ; mode 2: partial |a|^2
+__global__ void __launch_bounds__(256) vec_kernel(const float2* __restrict__ a, double alpha,
+                                                  const float2* __restrict__ b, int64_t count,
+                                                  const float* __restrict__ w, int mode,
+                                                  float2* __restrict__ R,
+                                                  double* __restrict__ partial) {
+  __shared__ double sh[256];
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = per * blockIdx.x, hi = min(count, lo + per);
+  double acc = 0.0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += 256) {
+    const float2 x = a[e];
+    if (mode == 2) {
+      acc += double(x.x) * x.x + double(x.y) * x.y;
+      continue;
+    }
+    const float2 y = b[e];
+    double rr, ri;
+    if (mode == 1) {
+      rr = alpha * x.x - y.x;
+      ri = alpha * x.y - y.y;
+    } else {
+      const float r0 = x.x - y.x, r1 = x.y - y.y;
+      rr = r0;
+      ri = r1;
+      if (R) {
+        const float ww = w ? w[e] : 1.f;
+        R[e] = make_float2(ww * r0, ww * r1);
+      }
+    }
+    const double ww = w ? double(w[e]) : 1.0;
+    acc += ww * (rr * rr + ri * ri);
+  }
+  double r = block_sum_256(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = r;
+}
+
+__global__ void scale_kernel(float2* a, float alpha, int64_t count) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    float2 x = a[e];
+    a[e] = make_float2(x.x * alpha, x.y * alpha);
+  }
+}
+
+// ---------------------------------------------------------------- multi-GPU argmax combine
+// cand = (score == global max) ? global index : INT64_MAX   (then all-reduce MIN)
+__global__ void argmax_select_kernel(const double* __restrict__ score,
+                                     const int64_t* __restrict__ gidx,
+                                     const double* __restrict__ gmax, int64_t n,
+                                     int64_t* __restrict__ cand) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v < n) cand[v] = (score[v] == gmax[v]) ? gidx[v] : INT64_MAX;
+}
+
+// ================================================================ host side
+struct Op {
+  int ndim;
+  int dims[3];
+  int64_t n;
+  int L, m;
+  const int* pattern;
+  cufftHandle plan;
+  float scale;  // 1/sqrt(n)
+};
+
+static int grid_for(int64_t work, int per_block = 256) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g > 148 * 16) g = 148 * 16;
+  return int(g > 0 ? g : 1);
+}
+
+size_t op_ws_bytes(const Op* op) {
+  const size_t frames = (size_t(op->L) * op->n * sizeof(float2) + 255) & ~size_t(255);
+  return frames + kRedBlocks * sizeof(double) + 256;
+}
+static float2* ws_frames(void* ws) { return static_cast<float2*>(ws); }
+static double* ws_partial(const Op* op, void* ws) {
+  const size_t frames = (size_t(op->L) * op->n * sizeof(float2) + 255) & ~size_t(255);
+  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + frames);
+}
+
+int op_create(int ndim, const int* dims, int L, int m, const int* pattern, Op** out) {
+  if ((ndim != 2 && ndim != 3) || L <= 0 || m <= 0) return kErrArgument;
+  Op* op = new (std::nothrow) Op{};
+  if (!op) return kErrArgument;
+  op->ndim = ndim;
+  op->n = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (dims[i] <= 0) { delete op; return kErrArgument; }
+    op->dims[i] = dims[i];
+    op->n *= dims[i];
+  }
+  op->L = L;
+  op->m = m;
+  op->pattern = pattern;
+  op->scale = float(1.0 / std::sqrt(double(op->n)));
+  int nd[3] = {dims[0], dims[1], ndim == 3 ? dims[2] : 1};
+  if (cufftPlanMany(&op->plan, ndim, nd, nullptr, 1, int(op->n), nullptr, 1, int(op->n), CUFFT_C2C,
+                    L) != CUFFT_SUCCESS) {
+    delete op;
+    set_last_error("cufftPlanMany failed");
+    return kErrCufft;
+  }
+  *out = op;
+  return kOk;
+}
+
+int op_destroy(Op* op) {
+  if (!op) return kOk;
+  cufftDestroy(op->plan);
+  delete op;
+  return kOk;
+}
+
+static int fft(Op* op, float2* F, int dir, cudaStream_t st) {
+  if (cufftSetStream(op->plan, st) != CUFFT_SUCCESS) return kErrCufft;
+  if (cufftExecC2C(op->plan, reinterpret_cast<cufftComplex*>(F), reinterpret_cast<cufftComplex*>(F),
+                   dir) != CUFFT_SUCCESS) {
+    set_last_error("cufftExecC2C failed");
+    return kErrCufft;
+  }
+  return kOk;
+}
+
+static int finish(const double* partial, int np, double* out, cudaStream_t st) {
+  finish_sum<<<1, 256, 0, st>>>(partial, np, out);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+static int decompress(const Op* op, const float2* Xc, const float2* V, int s, float2* F,
+                      cudaStream_t st) {
+  if (s < 1 || s > 32) return kErrUnsupported;
+  const int tpb = 32;
+  dim3 grid(unsigned((op->n + 255) / 256), unsigned((op->L + tpb - 1) / tpb));
+  decompress_frames_kernel<<<grid, 256, tpb * s * sizeof(float2), st>>>(Xc, V, s, op->n, op->L,
+                                                                         tpb, F);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+static int gather(const Op* op, const float2* F, int mode, const float2* Ymeas, const float* w,
+                  float2* Y, double* partial, cudaStream_t st) {
+  gather_kernel<<<kRedBlocks, 256, 0, st>>>(F, op->pattern, op->n, op->L, op->m, op->scale, mode,
+                                            Ymeas, w, Y, partial);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st) {
+  float2* F = ws_frames(ws);
+  dim3 grid(unsigned((op->L + 31) / 32), unsigned((op->n + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(X, op->n, op->L, 1.f, F);
+  CBB_CUDA_TRY(cudaGetLastError());
+  int rc = fft(op, F, CUFFT_FORWARD, st);
+  if (rc) return rc;
+  return gather(op, F, 0, nullptr, nullptr, Y, nullptr, st);
+}
+
+int op_adjoint(Op* op, const float2* Y, float2* X, void* ws, cudaStream_t st) {
+  float2* F = ws_frames(ws);
+  CBB_CUDA_TRY(cudaMemsetAsync(F, 0, size_t(op->L) * op->n * sizeof(float2), st));
+  scatter_kernel<<<grid_for(int64_t(op->L) * op->m), 256, 0, st>>>(Y, op->pattern, op->n, op->L,
+                                                                     op->m, F);
+  CBB_CUDA_TRY(cudaGetLastError());
+  int rc = fft(op, F, CUFFT_INVERSE, st);
+  if (rc) return rc;
+  dim3 grid(unsigned((op->n + 31) / 32), unsigned((op->L + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(F, op->L, op->n, op->scale, X);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2* Y, void* ws,
+                        const float2* Ymeas, const float* w, double* norm_out, cudaStream_t st) {
+  float2* F = ws_frames(ws);
+  int rc = decompress(op, Xc, V, s, F, st);
+  if (rc) return rc;
+  rc = fft(op, F, CUFFT_FORWARD, st);
+  if (rc) return rc;
+  double* part = ws_partial(op, ws);
+  if (Y == nullptr) {  // norm only
+    rc = gather(op, F, 1, nullptr, nullptr, nullptr, part, st);
+  } else if (Ymeas != nullptr) {
+    rc = gather(op, F, 2, Ymeas, w, Y, part, st);
+  } else {
+    rc = gather(op, F, 0, nullptr, nullptr, Y, norm_out ? part : nullptr, st);
+  }
+  if (rc) return rc;
+  if (norm_out) return finish(part, kRedBlocks, norm_out, st);
+  return kOk;
+}
+
+int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float2* Gc, void* ws,
+                          cudaStream_t st) {
+  if (s < 1 || s > 32) return kErrUnsupported;
+  float2* F = ws_frames(ws);
+  CBB_CUDA_TRY(cudaMemsetAsync(F, 0, size_t(op->L) * op->n * sizeof(float2), st));
+  scatter_kernel<<<grid_for(int64_t(op->L) * op->m), 256, 0, st>>>(R, op->pattern, op->n, op->L,
+                                                                     op->m, F);
+  CBB_CUDA_TRY(cudaGetLastError());
+  int rc = fft(op, F, CUFFT_INVERSE, st);
+  if (rc) return rc;
+  compress_frames_kernel<<<unsigned((op->n + 255) / 256), 256, 0, st>>>(F, V, s, op->n, op->L,
+                                                                        op->scale, Gc);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int vec_op(const float2* a, double alpha, const float2* b, int64_t count, const float* w,
+           int mode, float2* R, double* out, void* ws, cudaStream_t st) {
+  double* part = static_cast<double*>(ws);
+  vec_kernel<<<kRedBlocks, 256, 0, st>>>(a, alpha, b, count, w, mode, R, part);
+  CBB_CUDA_TRY(cudaGetLastError());
+  if (out) return finish(part, kRedBlocks, out, st);
+  return kOk;
+}
+
+int scale_c64(float2* a, double alpha, int64_t count, cudaStream_t st) {
+  scale_kernel<<<grid_for(count), 256, 0, st>>>(a, float(alpha), count);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int argmax_select(const double* score, const int64_t* gidx, const double* gmax, int64_t n,
+                  int64_t* cand, cudaStream_t st) {
+  if (n == 0) return kOk;
+  argmax_select_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(score, gidx, gmax, n, cand);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+size_t reduce_ws_bytes() { return kRedBlocks * sizeof(double); }
+
+}  // namespace cbb

@@ -1,0 +1,60 @@
+// Exact cone projection (matched filter) -- shared host/device declarations.
+//
+// Reference semantics (coverblip/projection.py:45-67):
+//   j*_v  = argmax_j Re<Z_v, D_j>   (first index on ties, projection.py:62)
+//   g_v   = max(Re<Z_v, D_j*>, 0)    (projection.py:38-42)
+//   P_v   = g_v * D_j*               (projection.py:64)
+//
+// B200 design: a screening pass scores every (voxel, atom) pair in low
+// precision (bf16 tcgen05 MMA, or fp32 FFMA) and keeps, per voxel, every atom
+// whose approximate score lies inside a CERTIFIED window below the running
+// maximum (window = 2 * rigorous bound on |approx - exact|).  The surviving
+// candidates are rescored in fp64 from the caller's own atoms and voxels, so
+// the selected index is the fp64 argmax (lowest index on exact ties); voxels
+// whose candidate list overflows are rescanned exhaustively in fp64.
+#pragma once
+#include <cstdint>
+
+namespace cbb {
+
+constexpr int kCandCap = 16;       // candidate slots per voxel in the screening kernels
+
+// Device view of a prepared dictionary (all pointers are device memory).
+struct DictView {
+  int64_t d;
+  int32_t s;
+  int32_t s_pad;       // FFMA register width (>= s)
+  int32_t kpad;        // tensor-core K (32 or 64)
+  int32_t n_btiles;    // ceil(d / 128)
+  const double2* atoms64;      // d x s   complex128 (exact rescoring)
+  const float* atoms32;        // d x 2*s_pad planar fp32 [re.., im..]
+  const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad bf16, swizzled tiles
+  const float* bounds;         // [0]=delta_bf16 [1]=dmax [2]=dbf_max [3]=delta32 [4]=d32max
+};
+
+// Bounds slots.
+enum { kBDeltaBf16 = 0, kBDmax = 1, kBDbfMax = 2, kBDelta32 = 3, kBD32Max = 4, kBCount = 8 };
+
+// Where the projection input Z comes from.
+struct ZSource {
+  const void* z;       // n x s complex (c64 if !z128 else c128), may be null in IPG mode
+  int32_t z128;
+  const float2* x;     // IPG mode: Z = x - mu * g (complex64), written to z_out
+  const float2* g;
+  float mu;
+  float2* z_out;
+};
+
+// Outputs.  Any pointer may be null (not produced).
+struct ProjOut {
+  void* idx;           // int32 or int64 (idx64)
+  int32_t idx64;
+  double* gamma;       // fp64
+  void* proj;          // c64 or c128 (proj128)
+  int32_t proj128;
+  const float2* x;     // IPG: dX = proj(c64) - x
+  float2* dx;
+  double* nd_v;        // per-voxel ||dX_v||^2 (fp64), or ||proj - z||^2-free if null
+};
+
+}  // namespace cbb

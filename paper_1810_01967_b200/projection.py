@@ -1,0 +1,130 @@
+"""Exact cone projection -- drop-in for ``coverblip.projection.project_cone_exact``.
+
+Reference semantics (``coverblip/projection.py:45-67``): for every voxel row
+``Z_v`` pick ``j* = argmax_j Re<Z_v, D_j>`` (first index on ties, ``:62``), set
+``gamma_v = max(Re<Z_v, D_j*>, 0)`` (``_gammas_for``, ``:38-42``) and
+``projected_v = gamma_v * D_j*`` (``:64``); ``cost = n * d`` (``:67``); a shape
+mismatch raises ``ValueError("dimension mismatch: ...")`` (``:53-56``).
+
+B200 path: ``cbb_project_cone_exact`` (tcgen05 bf16 screening with a certified
+window + fp64 rescoring, see ``csrc/cbb_project.cuh``).  numpy inputs return
+numpy outputs with the reference dtypes (int64 / float64 / complex128); torch
+CUDA inputs stay on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import require_cuda, workspace
+from .dictionary import DeviceDictionary, atoms_of, device_dictionary
+
+__all__ = ["ConeProjection", "project_cone_exact", "project_device"]
+
+
+@dataclass
+class ConeProjection:
+    """Mirror of ``projection.py:18-23``."""
+    indices: object      # n chosen atom ids (int64)
+    gammas: object       # n nonnegative scales (float64)
+    projected: object    # n x dim complex, row v = gammas[v] * atoms[j_v]
+    cost: int            # distance evaluations (n * d for the exact path)
+
+
+def _as_array(Z):
+    """``projection.py:32-35``: ``.data`` else the array itself."""
+    if hasattr(Z, "data") and not isinstance(Z, (np.ndarray, torch.Tensor)):
+        Z = Z.data
+    if isinstance(Z, torch.Tensor):
+        return Z
+    return np.asarray(Z)
+
+
+def _atoms_shape(dictionary):
+    a = atoms_of(dictionary)
+    if isinstance(a, DeviceDictionary):
+        return a.shape
+    return tuple(a.shape)
+
+
+def project_device(Z: torch.Tensor, dd: DeviceDictionary, *, algo: str = "auto",
+                   idx_int64: bool = True, proj_c128: bool = None, out=None):
+    """Device-resident projection.  ``Z`` is a CUDA complex64/complex128 (n, s) tensor.
+
+    Returns ``(indices, gammas, projected)`` device tensors.
+    """
+    lib = _lib.load()
+    n, s = int(Z.shape[0]), int(Z.shape[1])
+    z128 = Z.dtype == torch.complex128
+    if proj_c128 is None:
+        proj_c128 = z128
+    dev = Z.device
+    if out is None:
+        idx = torch.empty(n, dtype=torch.int64 if idx_int64 else torch.int32, device=dev)
+        gam = torch.empty(n, dtype=torch.float64, device=dev)
+        proj = torch.empty((n, s), dtype=torch.complex128 if proj_c128 else torch.complex64,
+                           device=dev)
+    else:
+        idx, gam, proj = out
+    wsb = lib.cbb_project_workspace_bytes(n, s)
+    ws = workspace(wsb, dev, "project")
+    rc = lib.cbb_project_cone_exact(Z.data_ptr() if n else None, int(z128), n,
+                                    ctypes.byref(dd.view), idx.data_ptr(),
+                                    int(idx.dtype == torch.int64), gam.data_ptr(),
+                                    proj.data_ptr(), int(proj.dtype == torch.complex128),
+                                    ws.data_ptr(), wsb, _lib.ALGOS[algo], _lib.stream_ptr())
+    _lib.check(rc, "cbb_project_cone_exact")
+    return idx, gam, proj
+
+
+def project_cone_exact(Z, dictionary, *, algo: str = "auto") -> ConeProjection:
+    """Drop-in for ``coverblip.projection.project_cone_exact`` (projection.py:45-67)."""
+    Z = _as_array(Z)
+    ashape = _atoms_shape(dictionary)
+    if Z.ndim != 2 or Z.shape[1] != ashape[1]:
+        raise ValueError(
+            f"dimension mismatch: image is {tuple(Z.shape)}, atoms are {ashape}")
+    n, d = int(Z.shape[0]), int(ashape[0])
+    if isinstance(Z, torch.Tensor):
+        dev = require_cuda(Z.device if Z.is_cuda else None)
+        dd = device_dictionary(dictionary, dev)
+        zt = Z.to(dev)
+        if zt.dtype not in (torch.complex64, torch.complex128):
+            zt = zt.to(torch.complex128)
+        with torch.cuda.device(dev):
+            idx, gam, proj = project_device(zt.contiguous(), dd, algo=algo)
+        return ConeProjection(indices=idx, gammas=gam, projected=proj, cost=n * d)
+    dev = require_cuda()
+    dd = device_dictionary(dictionary, dev)
+    if not np.iscomplexobj(Z) or Z.dtype not in (np.complex64, np.complex128):
+        Z = Z.astype(np.complex128)
+    zt = torch.from_numpy(np.ascontiguousarray(Z)).to(dev, non_blocking=True)
+    proj_dtype = torch.complex128
+    with torch.cuda.device(dev):
+        idx, gam, proj = project_device(zt, dd, algo=algo, proj_c128=True)
+        h_idx = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        h_gam = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        h_proj = torch.empty((n, Z.shape[1]), dtype=proj_dtype, pin_memory=True)
+        h_idx.copy_(idx, non_blocking=True)
+        h_gam.copy_(gam, non_blocking=True)
+        h_proj.copy_(proj, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    return ConeProjection(indices=h_idx.numpy(), gammas=h_gam.numpy(),
+                          projected=h_proj.numpy(), cost=n * d)
+
+
+def overflow_count(n: int, s: int) -> int:
+    """Voxels that needed the exhaustive fp64 rescan in the last projection (diagnostic)."""
+    lib = _lib.load()
+    dev = require_cuda()
+    wsb = lib.cbb_project_workspace_bytes(n, s)
+    ws = workspace(wsb, dev, "project")
+    out = ctypes.c_int(0)
+    _lib.check(lib.cbb_project_overflow_count(ws.data_ptr(), n, s, ctypes.byref(out),
+                                              _lib.stream_ptr()), "overflow_count")
+    return int(out.value)

@@ -1,0 +1,181 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations (host numpy).
+
+No public dataset is named by the benchmark; the paper's Brainweb phantom and
+in-vivo scans are absent, so every config is generated from fixed seeds
+(SURVEY 8d): seed 0 sequence / dictionary, 1 phantom / voxels, 2 masks, 3 noise.
+
+* cfg0  64x64, 4 tissue classes, T=200 IR-bSSFP frames (flip/TR schedule of
+        BASELINE configs[0]), T1 50 x T2 60 log grids (T2 < T1, D = 2242),
+        Bloch-simulated atoms (``bloch_irbssfp``; the reference has only an
+        analytic surrogate), unit-normalised, SVD s = 10; 8 of 64
+        random lines per frame; 30 dB noise (reference ``harness.py:145-153`` rule).
+* cfg1  N = 2^20 voxels x D = 2^17 random unit atoms, s = 10, voxel = atom x
+        PD~U(0.2,1) x random phase + complex noise at 20 dB.
+* cfg2/3 shapes are provided for the parity tests at reduced size.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .dictionary import CompressedDictionary, Dictionary, svd_compress
+
+__all__ = ["sequence_schedule", "bloch_irbssfp", "cfg0_dictionary", "Cfg0", "make_cfg0",
+           "random_atoms", "cone_voxels", "make_cfg1", "random_line_pattern"]
+
+
+def sequence_schedule(L: int, seed: int = 0):
+    """alpha_t = 10 + 50 |sin(2 pi t / 250)| + N(0, 1) degrees; TR_t = 10 + U(0, 2) ms."""
+    rng = np.random.default_rng(seed)
+    t = np.arange(L)
+    alpha = 10.0 + 50.0 * np.abs(np.sin(2 * np.pi * t / 250.0)) + rng.normal(0.0, 1.0, L)
+    tr = 10.0 + rng.uniform(0.0, 2.0, L)
+    return np.deg2rad(alpha), tr
+
+
+def bloch_irbssfp(params, alpha, tr):
+    """Single-isochromat Bloch simulation of an inversion-recovery bSSFP train.
+
+    params (d, 3) = (T1 ms, T2 ms, B0 Hz).  Ideal 180 deg inversion, then per
+    frame: RF rotation about x by alpha_t with alternating sign (0/180 phase
+    cycling), relaxation + off-resonance precession for TR_t/2, readout
+    (demodulated by the RF sign), another TR_t/2.  Returns (d, L) complex128.
+    """
+    p = np.atleast_2d(np.asarray(params, dtype=float))
+    t1, t2, b0 = p[:, 0], p[:, 1], p[:, 2]
+    d, L = p.shape[0], len(alpha)
+    mx = np.zeros(d)
+    my = np.zeros(d)
+    mz = -np.ones(d)
+    out = np.empty((d, L), dtype=complex)
+
+    def relax(mx, my, mz, tau):
+        e1 = np.exp(-tau / t1)
+        e2 = np.exp(-tau / t2)
+        phi = 2.0 * np.pi * b0 * tau / 1000.0
+        c, s = np.cos(phi), np.sin(phi)
+        mx, my = e2 * (c * mx - s * my), e2 * (s * mx + c * my)
+        mz = e1 * mz + (1.0 - e1)
+        return mx, my, mz
+
+    for t in range(L):
+        a = alpha[t] * (1.0 if t % 2 == 0 else -1.0)
+        ca, sa = np.cos(a), np.sin(a)
+        my, mz = ca * my + sa * mz, -sa * my + ca * mz
+        mx, my, mz = relax(mx, my, mz, tr[t] / 2.0)
+        sign = 1.0 if t % 2 == 0 else -1.0
+        out[:, t] = sign * (mx + 1j * my)
+        mx, my, mz = relax(mx, my, mz, tr[t] / 2.0)
+    return out
+
+
+def cfg0_dictionary(L: int = 200, n_t1: int = 50, n_t2: int = 60, seed: int = 0,
+                    b0_values=(0.0,)) -> Dictionary:
+    alpha, tr = sequence_schedule(L, seed)
+    t1 = np.geomspace(100.0, 5000.0, n_t1)
+    t2 = np.geomspace(20.0, 2000.0, n_t2)
+    g1, g2, g3 = np.meshgrid(t1, t2, np.asarray(b0_values, float), indexing="ij")
+    triples = np.stack([g1.ravel(), g2.ravel(), g3.ravel()], axis=1)
+    triples = triples[triples[:, 1] < triples[:, 0]]
+    raw = bloch_irbssfp(triples, alpha, tr)
+    norms = np.linalg.norm(raw, axis=1)
+    return Dictionary(atoms=raw / norms[:, None], norms=norms, lookup_table=triples,
+                      tr_ms=float(np.mean(tr)), L=L)
+
+
+def random_line_pattern(h: int, w: int, lines: int, L: int, seed: int = 2) -> np.ndarray:
+    """Per-frame random Cartesian lines: `lines` of h rows without replacement, all columns.
+    Returns (L, lines*w) int64 flat indices row*w + col (forward_model.py:138 order)."""
+    rng = np.random.default_rng(seed)
+    cols = np.arange(w)
+    out = np.empty((L, lines * w), dtype=np.int64)
+    for t in range(L):
+        rows = np.sort(rng.choice(h, size=lines, replace=False))
+        out[t] = (rows[:, None] * w + cols[None, :]).ravel()
+    return out
+
+
+@dataclass
+class Cfg0:
+    dictionary: Dictionary
+    cdict: CompressedDictionary
+    pattern: np.ndarray          # (L, m)
+    spatial_shape: tuple
+    gt: np.ndarray               # (n, L) ground-truth image
+    gt_indices: np.ndarray
+    pd: np.ndarray
+    Y: np.ndarray                # (m, L) reference layout
+
+
+def make_cfg0(h=64, w=64, L=200, s=10, lines=8, snr_db=30.0, n_t1=50, n_t2=60,
+              classes=4) -> Cfg0:
+    """BASELINE configs[0] (PR1): the CPU-runnable IPG reconstruction."""
+    dct = cfg0_dictionary(L, n_t1, n_t2, seed=0)
+    cd = svd_compress(dct, s)
+    rng = np.random.default_rng(1)
+    seg = np.zeros((h, w), dtype=np.int64)
+    b = max(1, min(h, w) // 16)
+    rr, cc = np.mgrid[0:h, 0:w]
+    inside = (rr >= b) & (rr < h - b) & (cc >= b) & (cc < w - b)
+    if classes == 4:
+        lab = 1 + 2 * (rr >= h // 2) + (cc >= w // 2)
+    else:
+        lab = 1 + (rr * classes) // h
+    seg[inside] = lab[inside]
+    class_atoms = rng.integers(dct.d, size=classes + 1)
+    pd = np.where(seg > 0, rng.uniform(0.5, 1.0, size=(h, w)), 0.0).ravel()
+    idx = np.where(seg.ravel() > 0, class_atoms[seg.ravel()], 0)
+    gt = pd[:, None] * dct.atoms[idx]
+    pattern = random_line_pattern(h, w, lines, L, seed=2)
+    # Y = A X0 + xi with ||xi|| = ||A X0|| 10^(-snr/20)  (harness.py:145-153)
+    n = h * w
+    F = np.fft.fft2(gt.reshape(h, w, L), axes=(0, 1), norm="ortho").reshape(n, L)
+    Y0 = np.take_along_axis(F, pattern.T, axis=0)
+    nrng = np.random.default_rng(3)
+    xi = nrng.standard_normal(Y0.shape) + 1j * nrng.standard_normal(Y0.shape)
+    xi *= np.linalg.norm(Y0) / np.linalg.norm(xi) * 10 ** (-snr_db / 20.0)
+    return Cfg0(dictionary=dct, cdict=cd, pattern=pattern, spatial_shape=(h, w), gt=gt,
+                gt_indices=np.where(seg.ravel() > 0, idx, -1), pd=pd, Y=Y0 + xi)
+
+
+def random_atoms(D: int, s: int, seed: int = 0, dtype=np.complex128) -> np.ndarray:
+    """i.i.d. CN(0, 1)^s atoms, unit-normalised (cfg1/cfg3)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((D, s), dtype=dtype)
+    step = 1 << 18
+    for lo in range(0, D, step):
+        k = min(step, D - lo)
+        a = rng.standard_normal((k, s)) + 1j * rng.standard_normal((k, s))
+        a /= np.linalg.norm(a, axis=1)[:, None]
+        out[lo:lo + k] = a
+    return out
+
+
+def cone_voxels(atoms: np.ndarray, N: int, seed: int = 1, snr_db: float = 20.0,
+                pd_range=(0.2, 1.0), dtype=np.complex128):
+    """Each voxel = atom_j x PD x e^{i phi} + complex noise at `snr_db` (per voxel)."""
+    rng = np.random.default_rng(seed)
+    D, s = atoms.shape
+    out = np.empty((N, s), dtype=dtype)
+    gen = np.empty(N, dtype=np.int64)
+    step = 1 << 18
+    for lo in range(0, N, step):
+        k = min(step, N - lo)
+        j = rng.integers(D, size=k)
+        pd = rng.uniform(pd_range[0], pd_range[1], size=k)
+        ph = np.exp(1j * rng.uniform(0.0, 2 * np.pi, size=k))
+        x = (pd * ph)[:, None] * atoms[j]
+        nz = (rng.standard_normal((k, s)) + 1j * rng.standard_normal((k, s))) / np.sqrt(2.0)
+        sig = np.linalg.norm(x, axis=1) / np.sqrt(s) * 10 ** (-snr_db / 20.0)
+        out[lo:lo + k] = x + nz * sig[:, None]
+        gen[lo:lo + k] = j
+    return out, gen
+
+
+def make_cfg1(N: int = 1 << 20, D: int = 1 << 17, s: int = 10, dtype=np.complex64):
+    """BASELINE configs[1]: standalone projection microbenchmark inputs."""
+    atoms = random_atoms(D, s, seed=0)
+    Z, gen = cone_voxels(atoms, N, seed=1, dtype=dtype)
+    return atoms, Z, gen
