@@ -93,9 +93,10 @@ int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_ti
 
 /* ---- Cartesian operator (forward_model.py:123-167) + subspace maps (dictionary.py:116-122) ---- */
 typedef struct cbb_op cbb_op;
-/* spatial dims (ndim 2 or 3), L frames, m samples per frame, pattern (L x m int32 device). */
+/* spatial dims (ndim 2 or 3), L frames, m samples per frame, pattern (L x m int32 device,
+ * flat C-order index per sample).  flags bit 0: identity_transform hook (no DFT). */
 int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const int32_t* pattern,
-                  cbb_op** out);
+                  int32_t flags, cbb_op** out);
 int cbb_op_destroy(cbb_op* op);
 size_t cbb_op_workspace_bytes(const cbb_op* op);
 /* Y = A X.  X: n x L complex64 voxel-major (reference layout); Y: L x m complex64

@@ -48,7 +48,7 @@ SIGNATURES = {
     "cbb_project_prologue": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_size,
                                      c_vp]),
     "cbb_debug_tc_scores": (c_int, [c_vp, ctypes.POINTER(DictView), c_i32, c_i32, c_vp, c_vp]),
-    "cbb_op_create": (c_int, [c_i32, ctypes.POINTER(c_i32), c_i32, c_i32, c_vp,
+    "cbb_op_create": (c_int, [c_i32, ctypes.POINTER(c_i32), c_i32, c_i32, c_vp, c_i32,
                               ctypes.POINTER(c_vp)]),
     "cbb_op_destroy": (c_int, [c_vp]),
     "cbb_op_workspace_bytes": (c_size, [c_vp]),

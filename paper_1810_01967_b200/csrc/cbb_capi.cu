@@ -25,7 +25,7 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
 
 // cbb_operator.cu
 struct Op;
-int op_create(int ndim, const int* dims, int L, int m, const int* pattern, Op** out);
+int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int flags, Op** out);
 int op_destroy(Op* op);
 size_t op_ws_bytes(const Op* op);
 int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st);
@@ -167,13 +167,13 @@ struct cbb_op {
 };
 
 int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const int32_t* pattern,
-                  cbb_op** out) {
+                  int32_t flags, cbb_op** out) {
   if (!dims || !pattern || !out) {
     set_last_error("cbb_op_create: null argument");
     return kErrArgument;
   }
   Op* impl = nullptr;
-  int rc = op_create(ndim, dims, L, m, pattern, &impl);
+  int rc = op_create(ndim, dims, L, m, pattern, flags, &impl);
   if (rc) return rc;
   *out = new cbb_op{impl};
   return kOk;

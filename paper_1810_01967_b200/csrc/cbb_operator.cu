@@ -243,7 +243,8 @@ struct Op {
   int L, m;
   const int* pattern;
   cufftHandle plan;
-  float scale;  // 1/sqrt(n)
+  float scale;     // 1/sqrt(n) (1 for the identity hook)
+  bool identity;   // forward_model.py:95,137,163 identity_transform test hook: skip the DFT
 };
 
 static int grid_for(int64_t work, int per_block = 256) {
@@ -262,7 +263,7 @@ static double* ws_partial(const Op* op, void* ws) {
   return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + frames);
 }
 
-int op_create(int ndim, const int* dims, int L, int m, const int* pattern, Op** out) {
+int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int flags, Op** out) {
   if ((ndim != 2 && ndim != 3) || L <= 0 || m <= 0) return kErrArgument;
   Op* op = new (std::nothrow) Op{};
   if (!op) return kErrArgument;
@@ -276,7 +277,13 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, Op** 
   op->L = L;
   op->m = m;
   op->pattern = pattern;
-  op->scale = float(1.0 / std::sqrt(double(op->n)));
+  op->identity = (flags & 1) != 0;
+  op->scale = op->identity ? 1.f : float(1.0 / std::sqrt(double(op->n)));
+  if (op->identity) {
+    op->plan = 0;
+    *out = op;
+    return kOk;
+  }
   int nd[3] = {dims[0], dims[1], ndim == 3 ? dims[2] : 1};
   if (cufftPlanMany(&op->plan, ndim, nd, nullptr, 1, int(op->n), nullptr, 1, int(op->n), CUFFT_C2C,
                     L) != CUFFT_SUCCESS) {
@@ -290,12 +297,13 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, Op** 
 
 int op_destroy(Op* op) {
   if (!op) return kOk;
-  cufftDestroy(op->plan);
+  if (!op->identity) cufftDestroy(op->plan);
   delete op;
   return kOk;
 }
 
 static int fft(Op* op, float2* F, int dir, cudaStream_t st) {
+  if (op->identity) return kOk;
   if (cufftSetStream(op->plan, st) != CUFFT_SUCCESS) return kErrCufft;
   if (cufftExecC2C(op->plan, reinterpret_cast<cufftComplex*>(F), reinterpret_cast<cufftComplex*>(F),
                    dir) != CUFFT_SUCCESS) {

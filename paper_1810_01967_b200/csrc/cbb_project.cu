@@ -15,6 +15,8 @@
 
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 
 namespace cbb {
 
@@ -33,16 +35,39 @@ __device__ __forceinline__ double2 load_z(const ZSource& zs, int64_t v, int s, i
   return make_double2(a.x, a.y);
 }
 
+// Exact Re<z_v, d_j> in fp64 (projection.py:61 arithmetic).  The z dtype is resolved once and
+// the k loop is unrolled so all loads of a candidate are in flight together.
+template <typename ZT>
+__device__ __forceinline__ double dot_re(const ZT* __restrict__ z, const double2* __restrict__ a,
+                                         int s) {
+  double acc0 = 0.0, acc1 = 0.0;
+  int k = 0;
+  for (; k + 4 <= s; k += 4) {
+    const ZT z0 = z[k], z1 = z[k + 1], z2 = z[k + 2], z3 = z[k + 3];
+    const double2 a0 = a[k], a1 = a[k + 1], a2 = a[k + 2], a3 = a[k + 3];
+    acc0 = fma(double(z0.x), a0.x, acc0);
+    acc0 = fma(double(z0.y), a0.y, acc0);
+    acc1 = fma(double(z1.x), a1.x, acc1);
+    acc1 = fma(double(z1.y), a1.y, acc1);
+    acc0 = fma(double(z2.x), a2.x, acc0);
+    acc0 = fma(double(z2.y), a2.y, acc0);
+    acc1 = fma(double(z3.x), a3.x, acc1);
+    acc1 = fma(double(z3.y), a3.y, acc1);
+  }
+  for (; k < s; ++k) {
+    const ZT zk = z[k];
+    const double2 ak = a[k];
+    acc0 = fma(double(zk.x), ak.x, acc0);
+    acc0 = fma(double(zk.y), ak.y, acc0);
+  }
+  return acc0 + acc1;
+}
+
 __device__ __forceinline__ double exact_score_g(const ZSource& zs, int64_t v, int s,
                                                 const double2* __restrict__ atom) {
-  double acc = 0.0;
-  for (int k = 0; k < s; ++k) {
-    double2 z = load_z(zs, v, s, k);
-    double2 a = atom[k];
-    acc = fma(z.x, a.x, acc);
-    acc = fma(z.y, a.y, acc);
-  }
-  return acc;
+  if (zs.x != nullptr) return dot_re(zs.z_out + v * s, atom, s);
+  if (zs.z128) return dot_re(reinterpret_cast<const double2*>(zs.z) + v * s, atom, s);
+  return dot_re(reinterpret_cast<const float2*>(zs.z) + v * s, atom, s);
 }
 
 // Winner write-back: idx, gamma = max(score, 0) (projection.py:42), gamma * D_j (projection.py:64),
@@ -114,30 +139,64 @@ struct CandList {
   }
 };
 
+// Rescore in fp64 every atom of the list entries that survive the final window.  An entry is
+// (first atom index, approximate max over its `span` atoms): span 1 for the FFMA screen (one
+// atom per entry), 32 for the tcgen05 screen (one 32-atom chunk per entry).  Ties keep the
+// lowest index (np.argmax, projection.py:62).
+__device__ __forceinline__ void rescore_one(const ZSource& zs, const DictView& dv, int64_t v,
+                                            int64_t j, int64_t& best, double& bs) {
+  const double sc = exact_score_g(zs, v, dv.s, dv.atoms64 + j * dv.s);
+  if (sc > bs || (sc == bs && j < best)) {
+    bs = sc;
+    best = j;
+  }
+}
+
+// Chunk entries of the tcgen05 screen: (first atom / 32) in bits [0,20), and a 12-bit mask of
+// the 3-wide groups (bits 0..9 -> atoms 3g..3g+2) and the two trailing atoms (bits 10, 11)
+// whose approximate scores reached the window when the chunk was recorded.
+constexpr int kChunkShift = 20;
+__device__ __forceinline__ int pack_chunk(int64_t jb, uint32_t mask) {
+  return int(uint32_t(jb >> 5) | (mask << kChunkShift));
+}
+
+__device__ __forceinline__ void rescore_entries(const ZSource& zs, const DictView& dv, int64_t v,
+                                                const int* cj, const float* cs, int stride,
+                                                int cnt, float thr, int span, int64_t& best,
+                                                double& bs) {
+  for (int c = 0; c < cnt; ++c) {
+    if (cs[c * stride] >= thr) {
+      const int e = cj[c * stride];
+      if (span == 1) {
+        rescore_one(zs, dv, v, e, best, bs);
+        continue;
+      }
+      const int64_t j0 = int64_t(uint32_t(e) & ((1u << kChunkShift) - 1)) << 5;
+      uint32_t mask = uint32_t(e) >> kChunkShift;
+      while (mask) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int lo = b < 10 ? 3 * b : 20 + b, hi = b < 10 ? lo + 3 : lo + 1;
+        for (int i = lo; i < hi; ++i)
+          if (j0 + i < dv.d) rescore_one(zs, dv, v, j0 + i, best, bs);
+      }
+    }
+  }
+}
+
 // Rescore the certified candidates in fp64 and write the winner; zero voxels go
 // straight to index 0 (np.argmax of an all-zero row); overflow -> exhaustive list.
 __device__ void finalize_voxel(const ZSource& zs, const DictView& dv, const ProjOut& out,
                                int64_t v, float win, float runmax, const CandList& cl,
-                               int* ovf_count, int64_t* ovf_list) {
+                               int* ovf_count, int64_t* ovf_list, int span = 1) {
   if (win < 0.f) {
     write_winner(out, dv, v, 0, 0.0);
     return;
   }
   int64_t best = -1;
   double bs = -INFINITY;
-  if (!cl.ovf) {
-    const float thr = runmax - win;
-    for (int c = 0; c < cl.cnt; ++c) {
-      if (cl.cs[c * cl.stride] >= thr) {
-        const int64_t j = cl.cj[c * cl.stride];
-        const double sc = exact_score_g(zs, v, dv.s, dv.atoms64 + j * dv.s);
-        if (sc > bs || (sc == bs && j < best)) {
-          bs = sc;
-          best = j;
-        }
-      }
-    }
-  }
+  if (!cl.ovf)
+    rescore_entries(zs, dv, v, cl.cj, cl.cs, cl.stride, cl.cnt, runmax - win, span, best, bs);
   if (best < 0) {
     int slot = atomicAdd(ovf_count, 1);
     ovf_list[slot] = v;
@@ -207,6 +266,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 int s_pad) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
+  // bf16 rows in 128-row UMMA tiles (K-major, swizzled): one bulk copy lands them in SMEM
   const int tile = int(v / kTileRows), r = int(v % kTileRows);
   uint8_t* trow = ztiles ? ztiles + size_t(tile) * kTileRows * kpad * 2 : nullptr;
   if (v >= n) {
@@ -378,50 +438,135 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
 }
 
 // ============================================================== tcgen05 screening
-template <int KP>
+// One CTA per SM (persistent, warp specialised).
+//   warp 0      bulk-copy producer: voxel tiles (SUBS x 128 rows) and a ring of atom tiles
+//               (BN rows), both pre-swizzled in global memory so one flat copy lands a tile
+//   warp 1      MMA issuer: whole warp runs the loop, one elected lane issues
+//               SUBS x KP/16 tcgen05.mma (M=128, N=BN, K=16, A and B from SMEM) per atom tile
+//               into one of two TMEM accumulator stages
+//   warp 2      TMEM allocator
+//   warps 4..   epilogue: warp (sub, q, half) owns TMEM lanes 32q..32q+31 of sub-tile `sub`
+//               (one voxel per thread) and 1/SPLIT of the stage's columns; running max +
+//               certified candidate list per (voxel, part); at the end of the voxel tile the
+//               part-0 thread rescores every part's candidates in fp64 and writes the winner.
+// Shapes follow measured sm_100a rates (scripts/ubench_mma.cu): an M=128 x N=128 x K=16 SS-MMA
+// reads 8 KB of operands per 64 clk, exactly the 128 B/clk shared-memory rate, and runs at
+// 4096 MAC/clk/SM when issued through elect.sync; smaller N or lane-0-only issue fall far
+// below.  Atom tiles are visited in a per-CTA rotated order so the 148 CTAs spread over L2.
+template <int KP, int SUBS, int BN, int SPLIT>
 struct TcCfg {
-  static constexpr int kTileBytes = kTileRows * KP * 2;  // one 128-row operand tile
-  static constexpr int kABytes = 2 * kTileBytes;         // 256 voxels
-  static constexpr int kStages = (KP == 32) ? 8 : 4;
-  static constexpr int kEpiWarps = 8;
+  static constexpr int kATileBytes = kTileRows * KP * 2;  // one 128-voxel sub-tile
+  static constexpr int kABytes = SUBS * kATileBytes;
+  static constexpr int kBBytes = BN * KP * 2;
+  static constexpr int kStages = (64 * 1024) / kBBytes;
+  static constexpr int kAccCols = SUBS * BN;
+  static constexpr int kAcc = 512 / kAccCols;
+  static_assert(kAcc >= 2 && kAcc * kAccCols == 512, "accumulator stages must tile 512 columns");
+  static constexpr int kCols = BN / SPLIT;                 // columns per epilogue thread per stage
+  static_assert(kCols % 32 == 0, "epilogue chunks are 32 columns");
+  static constexpr int kEpiWarps = SUBS * 4 * SPLIT;
   static constexpr int kThreads = (4 + kEpiWarps) * 32;
+  static constexpr int kVox = SUBS * 128;
+  static constexpr int kSlots = kVox * SPLIT;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + 2 * kABytes;
-  static constexpr int kOffCj = kOffB + kStages * kTileBytes;
-  static constexpr int kOffCs = kOffCj + kCandCap * 256 * 4;
-  static constexpr int kOffBar = kOffCs + kCandCap * 256 * 4;
-  static constexpr int kNumBars = 2 + 2 + 2 * kStages + 2 + 2;
+  static constexpr int kOffCj = kOffB + kStages * kBBytes;
+  static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
+  static constexpr int kOffX = kOffCs + kCandCap * kSlots * 4;   // part-thread exchange
+  static constexpr int kOffBar = kOffX + kSlots * 8;
+  static constexpr int kNumBars = 4 + 2 * kStages + 2 * kAcc;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
-  static constexpr uint32_t kIdesc = idesc_bf16_f32(128, 128);
+  static_assert(kSmem <= 227 * 1024, "shared memory");
+  static constexpr uint32_t kIdesc = idesc_bf16_f32(128, BN);
 };
 
-template <int KP>
-__global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
+__device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);  // keeps the shared address space
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Screen 32 approximate scores of one voxel (one thread): running max + certified window.
+// Fast path: 16 three-input maxes + one compare.  When the chunk max enters the window the
+// chunk itself (first atom index + its max) is recorded -- no per-value work; the finalize
+// rescans recorded chunks exactly.  Any atom inside the final window lies in a recorded chunk
+// whose max is at least its score, so the certificate is unchanged.
+__device__ __forceinline__ void screen32(float (&r)[32], int64_t jb, bool tail, int64_t d,
+                                         float win, float& runmax, float& thr, bool& active,
+                                         CandList& cl, int epi_mode = 0,
+                                         unsigned long long* dbg = nullptr) {
+  if (tail) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (jb + i >= d) r[i] = -INFINITY;
+  }
+  float m[10];
+#pragma unroll
+  for (int g = 0; g < 10; ++g) m[g] = fmax3(r[3 * g], r[3 * g + 1], r[3 * g + 2]);
+  const float n0 = fmax3(m[0], m[1], m[2]), n1 = fmax3(m[3], m[4], m[5]);
+  const float n2 = fmax3(m[6], m[7], m[8]), n3 = fmax3(m[9], r[30], r[31]);
+  const float cm = fmax3(n0, n1, fmaxf(n2, n3));
+  if (epi_mode == 5 && dbg) {  // dev: count warp-level slow-path entries
+    const unsigned any = __ballot_sync(0xffffffffu, cm >= thr);
+    if (any && (threadIdx.x & 31) == 0) atomicAdd(dbg, 1ull);
+  }
+  if (cm >= thr) {
+    runmax = fmaxf(runmax, cm);
+    if (active) {
+      thr = runmax - win;
+      if (epi_mode != 4) {
+        uint32_t mask = (r[30] >= thr ? (1u << 10) : 0u) | (r[31] >= thr ? (1u << 11) : 0u);
+#pragma unroll
+        for (int g = 0; g < 10; ++g) mask |= (m[g] >= thr) ? (1u << g) : 0u;
+        cl.insert(pack_chunk(jb, mask), cm, thr);
+      }
+      if (cl.ovf) {
+        active = false;
+        thr = INFINITY;
+      }
+    }
+  }
+}
+
+template <int KP, int SUBS, int BN, int SPLIT>
+__global__ void __launch_bounds__(TcCfg<KP, SUBS, BN, SPLIT>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ ztiles, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, ZSource zs, DictView dv, ProjOut out,
-                 int* ovf_count, int64_t* ovf_list) {
-  using C = TcCfg<KP>;
+                 int* ovf_count, int64_t* ovf_list, int epi_mode) {
+  using C = TcCfg<KP, SUBS, BN, SPLIT>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = align1024_smem(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 2;
   uint64_t* b_full = bars + 4;
-  uint64_t* b_empty = bars + 4 + C::kStages;
-  uint64_t* t_full = bars + 4 + 2 * C::kStages;
-  uint64_t* t_empty = bars + 6 + 2 * C::kStages;
+  uint64_t* b_empty = b_full + C::kStages;
+  uint64_t* t_full = b_empty + C::kStages;
+  uint64_t* t_empty = t_full + C::kAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nB = dv.n_btiles;
   const int64_t d = dv.d;
+  const int nB = int((d + BN - 1) / BN);
+  const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(a_full + i, 1);
       mbar_init(a_empty + i, 1);
+    }
+    for (int i = 0; i < C::kAcc; ++i) {
       mbar_init(t_full + i, 1);
       mbar_init(t_empty + i, C::kEpiWarps);
     }
@@ -438,51 +583,56 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   const uint32_t tbase = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ producer (bulk copies)
-      const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
-      int st = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
-        const int buf = it & 1;
-        mbar_wait(a_empty + buf, ((it >> 1) & 1) ^ 1);
+    // ------------------------------------------------ producer (bulk copies)
+    const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
+    int st = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(a_empty + buf, ((it >> 1) & 1) ^ 1);
+      if (elect_one()) {
         mbar_arrive_expect_tx(a_full + buf, C::kABytes);
         bulk_g2s(smem + C::kOffA + buf * C::kABytes, ztiles + size_t(vt) * C::kABytes,
                  C::kABytes, a_full + buf, pol_a);
-        for (int b = 0; b < nB; ++b) {
-          mbar_wait(b_empty + st, ph ^ 1);
-          mbar_arrive_expect_tx(b_full + st, C::kTileBytes);
-          bulk_g2s(smem + C::kOffB + st * C::kTileBytes, dv.atoms_tc + size_t(b) * C::kTileBytes,
-                   C::kTileBytes, b_full + st, pol_b);
-          if (++st == C::kStages) { st = 0; ph ^= 1; }
+      }
+      __syncwarp();
+      int ba = rot;
+      for (int b = 0; b < nB; ++b) {
+        mbar_wait(b_empty + st, ph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(b_full + st, C::kBBytes);
+          bulk_g2s(smem + C::kOffB + st * C::kBBytes, dv.atoms_tc + size_t(ba) * C::kBBytes,
+                   C::kBBytes, b_full + st, pol_b);
         }
+        __syncwarp();
+        if (++st == C::kStages) { st = 0; ph ^= 1; }
+        if (++ba == nB) ba = 0;
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      int st = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      uint32_t tcount = 0;
-      const uint32_t a_base = smem_u32(smem + C::kOffA), b_base = smem_u32(smem + C::kOffB);
-      for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
-        const int buf = it & 1;
-        mbar_wait(a_full + buf, (it >> 1) & 1);
+    // ------------------------------------------------ MMA issuer (warp-uniform, elected lane)
+    int st = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    uint32_t tcount = 0;
+    const uint32_t a_base = smem_u32(smem + C::kOffA), b_base = smem_u32(smem + C::kOffB);
+    for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(a_full + buf, (it >> 1) & 1);
+      tc_fence_after();
+      for (int b = 0; b < nB; ++b) {
+        const int acc = int(tcount % C::kAcc);
+        mbar_wait(b_full + st, ph);
+        mbar_wait(t_empty + acc, ((tcount / C::kAcc) & 1) ^ 1);
         tc_fence_after();
-        for (int b = 0; b < nB; ++b) {
-          const int acc = tcount & 1;
-          mbar_wait(b_full + st, ph);
-          mbar_wait(t_empty + acc, ((tcount >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kTileBytes, KP);
+        if (elect_one()) {
+          const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
 #pragma unroll
-          for (int sub = 0; sub < 2; ++sub) {
+          for (int sub = 0; sub < SUBS; ++sub) {
             const uint64_t adesc =
-                umma_desc_kmajor(a_base + buf * C::kABytes + sub * C::kTileBytes, KP);
-            const uint32_t dcol = tbase + uint32_t(acc * 256 + sub * 128);
+                umma_desc_kmajor(a_base + buf * C::kABytes + sub * C::kATileBytes, KP);
+            const uint32_t dcol = tbase + uint32_t(acc * C::kAccCols + sub * BN);
 #pragma unroll
             for (int k = 0; k < KP / 16; ++k)
               tc_mma_bf16(dcol, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), C::kIdesc,
@@ -490,78 +640,127 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
           }
           tc_commit(b_empty + st);
           tc_commit(t_full + acc);
-          ++tcount;
-          if (++st == C::kStages) { st = 0; ph ^= 1; }
         }
-        tc_commit(a_empty + buf);
+        __syncwarp();
+        ++tcount;
+        if (++st == C::kStages) { st = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(a_empty + buf);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // -------------------------------------------------- epilogue
-    const int q = warp & 3, sub = (warp - 4) >> 2;
-    const int row = sub * 128 + q * 32 + lane;  // voxel row inside the 256-voxel tile
-    int* cj = reinterpret_cast<int*>(smem + C::kOffCj) + row;
-    float* cs = reinterpret_cast<float*>(smem + C::kOffCs) + row;
+    const int e = warp - 4;
+    const int q = warp & 3, sub = (e >> 2) % SUBS, part = e / (4 * SUBS);
+    const int row = sub * 128 + q * 32 + lane;  // voxel row inside the voxel tile
+    const int slot = part * C::kVox + row;
+    int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
+    float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
+    float* xmax = reinterpret_cast<float*>(smem + C::kOffX);          // [slot] part runmax
+    int* xcnt = reinterpret_cast<int*>(smem + C::kOffX) + C::kSlots;  // [slot] count / -1 = ovf
     const uint32_t lane_off = uint32_t(q * 32) << 16;
+    unsigned long long* dbg = reinterpret_cast<unsigned long long*>(ovf_list) + 1;
     uint32_t tcount = 0;
     for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x) {
-      const int64_t v = int64_t(vt) * 256 + row;
+      const int64_t v = int64_t(vt) * C::kVox + row;
       const bool live = v < n;
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
-      CandList cl{cj, cs, 256, 0, false};
+      CandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0, false};
       float runmax = -INFINITY, thr = active ? -INFINITY : INFINITY;
+      int ba = rot;
       for (int b = 0; b < nB; ++b) {
-        const int acc = tcount & 1;
-        mbar_wait(t_full + acc, (tcount >> 1) & 1);
+        const int acc = int(tcount % C::kAcc);
+        mbar_wait(t_full + acc, (tcount / C::kAcc) & 1);
         tc_fence_after();
-        const bool last = (b == nB - 1);
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          float ra[32], rb[32];
-          __syncwarp();
-          const uint32_t taddr = tbase + lane_off + uint32_t(acc * 256 + sub * 128 + h * 64);
-          tmem_ld32(taddr, ra);
-          tmem_ld32(taddr + 32, rb);
-          tc_wait_ld();
+        const bool tail = (ba == nB - 1) && (int64_t(nB) * BN > d);
+        const uint32_t col0 = uint32_t(acc * C::kAccCols + sub * BN + part * C::kCols);
+        const int64_t jb0 = int64_t(ba) * BN + part * C::kCols;
+        if (epi_mode != 2) {
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            float* r = half ? rb : ra;
-            const int64_t jb = int64_t(b) * 128 + h * 64 + half * 32;
-            if (last) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (jb + i >= d) r[i] = -INFINITY;
+          for (int h = 0; h + 64 <= C::kCols; h += 64) {
+            float ra[32], rb[32];
+            __syncwarp();
+            const uint32_t taddr = tbase + lane_off + col0 + uint32_t(h);
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tc_wait_ld();
+            if (epi_mode == 1) {  // dev experiment: TMEM loads only
+              runmax = fmaxf(runmax, fmaxf(ra[0], rb[31]));
+              continue;
             }
-            // 32 -> 1 with 16 three-input maxes
-            float m0 = fmax3(r[0], r[1], r[2]), m1 = fmax3(r[3], r[4], r[5]);
-            float m2 = fmax3(r[6], r[7], r[8]), m3 = fmax3(r[9], r[10], r[11]);
-            float m4 = fmax3(r[12], r[13], r[14]), m5 = fmax3(r[15], r[16], r[17]);
-            float m6 = fmax3(r[18], r[19], r[20]), m7 = fmax3(r[21], r[22], r[23]);
-            float m8 = fmax3(r[24], r[25], r[26]), m9 = fmax3(r[27], r[28], r[29]);
-            float n0 = fmax3(m0, m1, m2), n1 = fmax3(m3, m4, m5), n2 = fmax3(m6, m7, m8);
-            float n3 = fmax3(m9, r[30], r[31]);
-            float cm = fmax3(n0, n1, fmaxf(n2, n3));
-            if (cm >= thr) {
-              runmax = fmaxf(runmax, cm);
-              if (active) {
-                thr = runmax - win;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  if (r[i] >= thr && !cl.ovf) cl.insert(int(jb + i), r[i], thr);
-                }
-                if (cl.ovf) { active = false; thr = INFINITY; }
-              }
-            }
+            screen32(ra, jb0 + h, tail, d, win, runmax, thr, active, cl, epi_mode, dbg);
+            screen32(rb, jb0 + h + 32, tail, d, win, runmax, thr, active, cl, epi_mode, dbg);
+          }
+          if (C::kCols % 64 == 32) {  // odd 32-column remainder
+            float ra[32];
+            __syncwarp();
+            tmem_ld32(tbase + lane_off + col0 + uint32_t(C::kCols - 32), ra);
+            tc_wait_ld();
+            if (epi_mode == 1) runmax = fmaxf(runmax, ra[0]);
+            else
+              screen32(ra, jb0 + C::kCols - 32, tail, d, win, runmax, thr, active, cl, epi_mode,
+                       dbg);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(t_empty + acc);
         ++tcount;
+        if (++ba == nB) ba = 0;
       }
-      if (live) finalize_voxel(zs, dv, out, v, win, runmax, cl, ovf_count, ovf_list);
+      if (epi_mode != 0 && epi_mode != 5 && epi_mode < 6) {  // dev experiments: keep live
+        if (runmax == 12345.f) ovf_list[0] = v;
+        continue;
+      }
+      if (SPLIT == 1) {
+        if (live) finalize_voxel(zs, dv, out, v, win, runmax, cl, ovf_count, ovf_list, 32);
+        continue;
+      }
+      // ---- merge the SPLIT per-part lists of each voxel and finalize (part-0 thread)
+      xmax[slot] = runmax;
+      xcnt[slot] = cl.ovf ? -1 : cl.cnt;
+      named_bar_sync(1, C::kEpiWarps * 32);
+      if (part == 0 && live) {
+        if (win < 0.f) {
+          write_winner(out, dv, v, 0, 0.0);
+        } else {
+          float gmax = runmax;
+          bool ovf = false;
+          for (int p2 = 0; p2 < SPLIT; ++p2) {
+            gmax = fmaxf(gmax, xmax[p2 * C::kVox + row]);
+            ovf |= xcnt[p2 * C::kVox + row] < 0;
+          }
+          int64_t best = -1;
+          double bs = -INFINITY;
+          if (epi_mode == 6 || epi_mode == 7) {  // dev: no rescoring
+            best = xcnt[row] > 0 ? cj_base[row] : 0;
+            bs = 1.0;
+            if (epi_mode == 7) best = -2;  // skip the write-back too
+          } else if (!ovf) {
+            const float thr_f = gmax - win;
+            for (int p2 = 0; p2 < SPLIT; ++p2) {
+              const int sl = p2 * C::kVox + row;
+              if (epi_mode == 5) {  // dev: count surviving chunks
+                int sv = 0;
+                for (int c = 0; c < xcnt[sl]; ++c) sv += cs_base[c * C::kSlots + sl] >= thr_f;
+                atomicAdd(reinterpret_cast<unsigned long long*>(ovf_list) + 2,
+                          (unsigned long long)sv);
+              }
+              rescore_entries(zs, dv, v, cj_base + sl, cs_base + sl, C::kSlots, xcnt[sl], thr_f,
+                              32, best, bs);
+            }
+          }
+          if (best == -2) {
+          } else if (best < 0) {
+            const int sl2 = atomicAdd(ovf_count, 1);
+            ovf_list[sl2] = v;
+          } else {
+            write_winner(out, dv, v, best, bs);
+          }
+        }
+      }
+      named_bar_sync(1, C::kEpiWarps * 32);
     }
   }
   __syncthreads();
@@ -571,16 +770,15 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   }
 }
 
-// Debug: raw bf16 tcgen05 scores for the first 128 voxels x first 128 atoms
-// (validates descriptors / swizzle against a host emulation).
+// Debug: raw bf16 tcgen05 scores for voxel tile a_tile x atom tile b_tile (128 x 128, SS)
+// -- validates descriptors / swizzle against a host emulation.
 template <int KP>
 __global__ void __launch_bounds__(128, 1)
     tc_debug_scores_kernel(const uint8_t* __restrict__ ztiles, const uint8_t* __restrict__ atiles,
                            int a_tile, int b_tile, float* __restrict__ out) {
   constexpr int kTileBytes = kTileRows * KP * 2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = align1024_smem(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kTileBytes);
   uint32_t* holder = reinterpret_cast<uint32_t*>(smem + 2 * kTileBytes + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -724,10 +922,11 @@ struct ProjWs {
   double* partial;
 };
 constexpr int kReduceBlocks = 256;
+constexpr int kVoxPad = 512;  // voxel tiles are padded to a multiple of the largest TC voxel tile
 
 size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   const int kp = kpad_for(s);
-  const int64_t n_vt = (n + 255) / 256;
+  const int64_t n_vt = (n + kVoxPad - 1) / kVoxPad;
   size_t o = 0;
   uint8_t* base = static_cast<uint8_t*>(base_ptr);
   auto take = [&](size_t bytes) {
@@ -736,9 +935,9 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
     return base ? base + r : nullptr;
   };
   ProjWs w{};
-  w.ztiles = take(size_t(n_vt) * 256 * kp * 2);
-  w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * 256 * 4));
-  w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * 256 * 4));
+  w.ztiles = take(size_t(n_vt) * kVoxPad * kp * 2);
+  w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
+  w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.ovf_count = reinterpret_cast<int*>(take(16));
   w.ovf_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   w.nd_v = reinterpret_cast<double*>(take(size_t(n) * 8));
@@ -758,24 +957,43 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int KP>
+template <int KP, int SUBS, int BN, int SPLIT>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
-  using C = TcCfg<KP>;
+  using C = TcCfg<KP, SUBS, BN, SPLIT>;
   static bool attr_set = false;
   if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SUBS, BN, SPLIT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
-  const int n_vt = int((n + 255) / 256);
+  const int n_vt = int((n + C::kVox - 1) / C::kVox);
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
-  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, zs, dv, out,
-                                                        w.ovf_count, w.ovf_list);
+  static int epi_mode = -1;
+  if (epi_mode < 0) {
+    const char* e = getenv("CBB_TC_EPI_MODE");  // development experiments only
+    epi_mode = e ? atoi(e) : 0;
+  }
+  mf_tc_kernel<KP, SUBS, BN, SPLIT><<<grid, C::kThreads, C::kSmem, st>>>(
+      w.ztiles, n, n_vt, w.win_tc, zs, dv, out, w.ovf_count, w.ovf_list, epi_mode);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
+}
+
+static int launch_tc32(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                       const ProjOut& out, int max_ctas, cudaStream_t st) {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("CBB_TC_CFG");  // development sweep only
+    cfg = e ? atoi(e) : 0;
+  }
+  switch (cfg) {
+    case 1: return launch_tc<32, 2, 128, 1>(w, n, zs, dv, out, max_ctas, st);
+    case 2: return launch_tc<32, 1, 256, 2>(w, n, zs, dv, out, max_ctas, st);
+    default: return launch_tc<32, 2, 128, 2>(w, n, zs, dv, out, max_ctas, st);
+  }
 }
 
 template <int S>
@@ -841,25 +1059,37 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   }
   ProjOut o = out;
   if (nd_sum && !o.nd_v) o.nd_v = w.nd_v;
-  const bool tc_ok = (2 * dv.s <= 64);
+  // tcgen05 path: K = 2s <= 64, and chunk entries pack (atom / 32) into 20 bits
+  const bool tc_ok = (2 * dv.s <= 64) && (dv.d <= (int64_t(1) << 25));
   if (algo == 0) algo = tc_ok ? 1 : 3;
   if (algo == 1 && !tc_ok) return kErrUnsupported;
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
+  const bool dbg5 = getenv("CBB_TC_EPI_MODE") && atoi(getenv("CBB_TC_EPI_MODE")) == 5;
+  if (dbg5) CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_list, 0, 3 * sizeof(int64_t), st));
   if (algo == 1 || algo == 2) {
-    const int64_t n_pad = ((n + 255) / 256) * 256;
+    const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
         zs, n, n_pad, dv.s, dv.kpad, dv.bounds, algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32,
         dv.s_pad);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
-    int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
-                                          : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
+    int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc32(w, n, zr, dv, o, max_ctas, st)
+                                          : launch_tc<64, 2, 128, 2>(w, n, zr, dv, o, max_ctas, st))
                          : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
-    rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
-    if (rc) return rc;
+    if (dbg5) {
+      unsigned long long h[3];
+      cudaMemcpyAsync(h, w.ovf_list, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "[dbg] slow warp-chunks=%llu surviving chunks=%llu\n", h[1], h[2]);
+    }
+    if (!getenv("CBB_TC_EPI_MODE") || atoi(getenv("CBB_TC_EPI_MODE")) == 0 ||
+        atoi(getenv("CBB_TC_EPI_MODE")) >= 5 || algo != 1) {
+      rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
+      if (rc) return rc;
+    }
   } else if (algo == 3) {
     if (zs.x != nullptr) {
       // materialise Z = X - mu G (same fp32 rounding as the prologue)
@@ -911,7 +1141,7 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
                   cudaStream_t st) {
   ProjWs w;
   project_ws_bytes(n, dv.s, &w, ws_ptr);
-  const int64_t n_pad = ((n + 255) / 256) * 256;
+  const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
   prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
                                                              w.win32, dv.s_pad);
