@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoverblip_b200.so")
+LIB_PATH = os.environ.get("CBB_LIB_PATH") or os.path.join(_HERE, "libcoverblip_b200.so")
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32

@@ -22,6 +22,7 @@ int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cuda
 int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile, int b_tile,
                     float* out, cudaStream_t st);
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr, cudaStream_t st);
+int trace_dump(long long* host, int count);
 
 // cbb_operator.cu
 struct Op;
@@ -159,6 +160,11 @@ int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_ti
   if (2 * dict->s > 64) return kErrUnsupported;
   // voxel tiles sit at the start of the projection workspace
   return tc_debug_scores(workspace, dict->atoms_tc, dict->kpad, a_tile, b_tile, out, S(stream));
+}
+
+// development only (not in the public header): per-tile clock stamps of CTA 0
+__attribute__((visibility("default"))) int cbb_dev_trace_dump(long long* host, int count) {
+  return trace_dump(host, count);
 }
 
 // ---------------------------------------------------------------- operator

@@ -266,13 +266,12 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 int s_pad) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
-  // bf16 rows in 128-row UMMA tiles (K-major, swizzled): one bulk copy lands them in SMEM
-  const int tile = int(v / kTileRows), r = int(v % kTileRows);
-  uint8_t* trow = ztiles ? ztiles + size_t(tile) * kTileRows * kpad * 2 : nullptr;
+  // plain row-major bf16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
+  uint8_t* trow = ztiles ? ztiles + size_t(v) * kpad * 2 : nullptr;
   if (v >= n) {
     if (trow)
       for (int c = 0; c < kpad / 8; ++c)
-        *reinterpret_cast<uint4*>(trow + tile_chunk_offset(r, c, kpad)) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
   }
   unsigned short row[64];
@@ -313,7 +312,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       pk.y = uint32_t(row[c * 8 + 2]) | (uint32_t(row[c * 8 + 3]) << 16);
       pk.z = uint32_t(row[c * 8 + 4]) | (uint32_t(row[c * 8 + 5]) << 16);
       pk.w = uint32_t(row[c * 8 + 6]) | (uint32_t(row[c * 8 + 7]) << 16);
-      *reinterpret_cast<uint4*>(trow + tile_chunk_offset(r, c, kpad)) = pk;
+      *reinterpret_cast<uint4*>(trow + c * 16) = pk;
     }
   }
   const double dmax = bounds[kBDmax], dbf = bounds[kBDbfMax], delbf = bounds[kBDeltaBf16];
@@ -437,48 +436,74 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
   }
 }
 
+#ifdef CBB_TRACE
+// development tracing: per-tile clock64 stamps of CTA 0 (issuer: after b_full wait, after
+// commit; epilogue part warp q0: after t_full wait, after wait::ld)
+constexpr int kTraceTiles = 2048;
+__device__ long long g_trace[kTraceTiles * 4];
+#define CBB_STAMP(slot, k)                                                          \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (k) < uint32_t(kTraceTiles))                             \
+      g_trace[(k) * 4 + (slot)] = clock64();                                        \
+  } while (0)
+#else
+#define CBB_STAMP(slot, k) \
+  do {                     \
+  } while (0)
+#endif
+
 // ============================================================== tcgen05 screening
-// One CTA per SM (persistent, warp specialised).
-//   warp 0      bulk-copy producer: voxel tiles (SUBS x 128 rows) and a ring of atom tiles
-//               (BN rows), both pre-swizzled in global memory so one flat copy lands a tile
-//   warp 1      MMA issuer: whole warp runs the loop, one elected lane issues
-//               SUBS x KP/16 tcgen05.mma (M=128, N=BN, K=16, A and B from SMEM) per atom tile
-//               into one of two TMEM accumulator stages
-//   warp 2      TMEM allocator
-//   warps 4..   epilogue: warp (sub, q, half) owns TMEM lanes 32q..32q+31 of sub-tile `sub`
-//               (one voxel per thread) and 1/SPLIT of the stage's columns; running max +
-//               certified candidate list per (voxel, part); at the end of the voxel tile the
-//               part-0 thread rescores every part's candidates in fp64 and writes the winner.
-// Shapes follow measured sm_100a rates (scripts/ubench_mma.cu): an M=128 x N=128 x K=16 SS-MMA
-// reads 8 KB of operands per 64 clk, exactly the 128 B/clk shared-memory rate, and runs at
-// 4096 MAC/clk/SM when issued through elect.sync; smaller N or lane-0-only issue fall far
-// below.  Atom tiles are visited in a per-CTA rotated order so the 148 CTAs spread over L2.
-template <int KP, int SUBS, int BN, int SPLIT>
+// One CTA per SM (persistent).  Per voxel tile (128 voxels):
+//   * the voxel operand A (bf16, K = KP) lives in TENSOR MEMORY (double buffered): part-0
+//     epilogue threads tcgen05.st their own voxel row into their TMEM lane one tile ahead;
+//   * warp 0 streams atom tiles (BN = 64 rows, pre-swizzled bf16) through a bulk-copy ring;
+//   * warps 1..kParts issue the MMAs: issuer i owns the CTA's atom tiles k = i (mod kParts),
+//     i.e. accumulator stages i, i + kParts (kAcc = 2 kParts stages of 64 columns) and the
+//     B-ring stages st = i (mod kParts); per tile it waits ONE barrier, b_full[st], whose phase
+//     completes when the tile's bytes have landed AND the epilogue released the accumulator
+//     stage (the epilogue arrives on the b_full of the tile that will reuse its stage), then
+//     issues KP/16 MMAs (M=128, N=64, K=16, A from TMEM, B from SMEM) and commits;
+//   * epilogue part p (4 warps, one per TMEM lane quarter) consumes tiles k = p (mod kParts):
+//     it copies the 64 scores per lane into registers and releases the stage immediately, so
+//     the screening runs while the tensor core refills it;
+// Every mbarrier has a single waiter role that consumes its phases in order (no parity
+// aliasing): b_full[st] -> issuer st % kParts (kStages % kParts == 0), t_full[s] -> part
+// s % kParts, b_empty -> producer, a_full -> issuers, a_empty -> part 0.  An epilogue arrival
+// for tile k + kAcc lands on b_full[(k + kAcc) % kStages] only after that barrier's previous
+// phase (tile k + kAcc - kStages) completed: the same issuer issued that tile before tile k.
+// Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
+constexpr int kParts = 3;
+
+template <int KP>
 struct TcCfg {
-  static constexpr int kATileBytes = kTileRows * KP * 2;  // one 128-voxel sub-tile
-  static constexpr int kABytes = SUBS * kATileBytes;
+  static constexpr int BN = 64;
+  static constexpr int kAColsPerSub = KP / 2;                // packed bf16 pairs per lane
+  static constexpr int kACols = kAColsPerSub;                // one A buffer (128 voxels)
+  static constexpr int kAcc = 2 * kParts;                    // 6 stages x 64 columns
+  static constexpr int kAccCols = BN;
+  static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
+  static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
   static constexpr int kBBytes = BN * KP * 2;
-  static constexpr int kStages = (64 * 1024) / kBBytes;
-  static constexpr int kAccCols = SUBS * BN;
-  static constexpr int kAcc = 512 / kAccCols;
-  static_assert(kAcc >= 2 && kAcc * kAccCols == 512, "accumulator stages must tile 512 columns");
-  static constexpr int kCols = BN / SPLIT;                 // columns per epilogue thread per stage
-  static_assert(kCols % 32 == 0, "epilogue chunks are 32 columns");
-  static constexpr int kEpiWarps = SUBS * 4 * SPLIT;
-  static constexpr int kThreads = (4 + kEpiWarps) * 32;
-  static constexpr int kVox = SUBS * 128;
-  static constexpr int kSlots = kVox * SPLIT;
-  static constexpr int kOffA = 0;
-  static constexpr int kOffB = kOffA + 2 * kABytes;
+  static constexpr int kStagesRaw = (96 * 1024) / kBBytes > 24 ? 24 : (96 * 1024) / kBBytes;
+  static constexpr int kStages = (kStagesRaw / kParts) * kParts;
+  static_assert(kStages >= 2 * kAcc, "B ring too shallow");
+  static constexpr int kEpiWarps = 4 * kParts;
+  static constexpr int kFirstEpiWarp = 1 + kParts;          // warp 0 producer, 1..3 issuers
+  static constexpr int kThreads = (kFirstEpiWarp + kEpiWarps) * 32;
+  static constexpr int kVox = 128;
+  static constexpr int kSlots = kVox * kParts;
+  static constexpr int kOffB = 0;
   static constexpr int kOffCj = kOffB + kStages * kBBytes;
   static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
-  static constexpr int kOffX = kOffCs + kCandCap * kSlots * 4;   // part-thread exchange
-  static constexpr int kOffBar = kOffX + kSlots * 8;
-  static constexpr int kNumBars = 4 + 2 * kStages + 2 * kAcc;
+  static constexpr int kOffX = kOffCs + kCandCap * kSlots * 4;  // per-slot exchange (24 B)
+  static constexpr int kOffBar = kOffX + kSlots * 24;
+  static constexpr int kNumBars = 4 + 2 * kStages + kAcc;
+  static_assert(kStages % kParts == 0 && kAcc % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
   static constexpr uint32_t kIdesc = idesc_bf16_f32(128, BN);
+  static constexpr int kMinTiles = kAcc;  // nB >= kAcc: every part owns >= 2 tiles per voxel tile
 };
 
 __device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
@@ -497,40 +522,52 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Screen 32 approximate scores of one voxel (one thread): running max + certified window.
-// Fast path: 16 three-input maxes + one compare.  When the chunk max enters the window the
-// chunk itself (first atom index + its max) is recorded -- no per-value work; the finalize
-// rescans recorded chunks exactly.  Any atom inside the final window lies in a recorded chunk
-// whose max is at least its score, so the certificate is unchanged.
-__device__ __forceinline__ void screen32(float (&r)[32], int64_t jb, bool tail, int64_t d,
-                                         float win, float& runmax, float& thr, bool& active,
-                                         CandList& cl, int epi_mode = 0,
-                                         unsigned long long* dbg = nullptr) {
+// Screen approximate scores of one voxel (one thread): running max + certified window.
+// Fast path per 64 scores: 32 three-input maxes + one compare.  When a 32-chunk max enters
+// the window the chunk (first atom, mask of 3-wide groups inside the window, chunk max) is
+// recorded -- no per-value inserts; the finalize rescans only the flagged groups exactly.
+// Any atom inside the final window lies in a flagged group of a recorded chunk, so the
+// certificate is unchanged.
+struct ChunkMax {
+  float m[10];
+  float cm;
+};
+
+__device__ __forceinline__ void chunk_max(float (&r)[32], int64_t jb, bool tail, int64_t d,
+                                          ChunkMax& c) {
   if (tail) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
       if (jb + i >= d) r[i] = -INFINITY;
   }
-  float m[10];
 #pragma unroll
-  for (int g = 0; g < 10; ++g) m[g] = fmax3(r[3 * g], r[3 * g + 1], r[3 * g + 2]);
-  const float n0 = fmax3(m[0], m[1], m[2]), n1 = fmax3(m[3], m[4], m[5]);
-  const float n2 = fmax3(m[6], m[7], m[8]), n3 = fmax3(m[9], r[30], r[31]);
-  const float cm = fmax3(n0, n1, fmaxf(n2, n3));
-  if (epi_mode == 5 && dbg) {  // dev: count warp-level slow-path entries
-    const unsigned any = __ballot_sync(0xffffffffu, cm >= thr);
-    if (any && (threadIdx.x & 31) == 0) atomicAdd(dbg, 1ull);
-  }
+  for (int g = 0; g < 10; ++g) c.m[g] = fmax3(r[3 * g], r[3 * g + 1], r[3 * g + 2]);
+  const float n0 = fmax3(c.m[0], c.m[1], c.m[2]), n1 = fmax3(c.m[3], c.m[4], c.m[5]);
+  const float n2 = fmax3(c.m[6], c.m[7], c.m[8]);
+  c.cm = fmax3(n0, n1, fmax3(n2, c.m[9], fmaxf(r[30], r[31])));
+}
+
+__device__ __forceinline__ void record_chunk(const float (&r)[32], const ChunkMax& c,
+                                             int64_t jb, float thr, CandList& cl) {
+  uint32_t mask = (r[30] >= thr ? (1u << 10) : 0u) | (r[31] >= thr ? (1u << 11) : 0u);
+#pragma unroll
+  for (int g = 0; g < 10; ++g) mask |= (c.m[g] >= thr) ? (1u << g) : 0u;
+  cl.insert(pack_chunk(jb, mask), c.cm, thr);
+}
+
+__device__ __forceinline__ void screen64(float (&ra)[32], float (&rb)[32], int64_t jb, bool tail,
+                                         int64_t d, float win, float& runmax, float& thr,
+                                         bool& active, CandList& cl) {
+  ChunkMax ca, cb;
+  chunk_max(ra, jb, tail, d, ca);
+  chunk_max(rb, jb + 32, tail, d, cb);
+  const float cm = fmaxf(ca.cm, cb.cm);
   if (cm >= thr) {
     runmax = fmaxf(runmax, cm);
     if (active) {
       thr = runmax - win;
-      if (epi_mode != 4) {
-        uint32_t mask = (r[30] >= thr ? (1u << 10) : 0u) | (r[31] >= thr ? (1u << 11) : 0u);
-#pragma unroll
-        for (int g = 0; g < 10; ++g) mask |= (m[g] >= thr) ? (1u << g) : 0u;
-        cl.insert(pack_chunk(jb, mask), cm, thr);
-      }
+      if (ca.cm >= thr && !cl.ovf) record_chunk(ra, ca, jb, thr, cl);
+      if (cb.cm >= thr && !cl.ovf) record_chunk(rb, cb, jb + 32, thr, cl);
       if (cl.ovf) {
         active = false;
         thr = INFINITY;
@@ -539,12 +576,34 @@ __device__ __forceinline__ void screen32(float (&r)[32], int64_t jb, bool tail, 
   }
 }
 
-template <int KP, int SUBS, int BN, int SPLIT>
-__global__ void __launch_bounds__(TcCfg<KP, SUBS, BN, SPLIT>::kThreads, 1)
-    mf_tc_kernel(const uint8_t* __restrict__ ztiles, int64_t n, int n_vt,
+template <int KP>
+__device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrows, int64_t v,
+                                                bool live, uint32_t taddr) {
+#pragma unroll
+  for (int half = 0; half < KP / 32; ++half) {
+    uint32_t wz[16];
+    const uint4* src = reinterpret_cast<const uint4*>(zrows + size_t(v) * KP * 2) + half * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 x = live ? src[c] : make_uint4(0, 0, 0, 0);
+      wz[4 * c + 0] = x.x;
+      wz[4 * c + 1] = x.y;
+      wz[4 * c + 2] = x.z;
+      wz[4 * c + 3] = x.w;
+    }
+    __syncwarp();
+    tmem_st16(taddr + uint32_t(half * 16), wz);
+  }
+  tc_wait_st();
+}
+
+template <int KP>
+__global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
+    mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, ZSource zs, DictView dv, ProjOut out,
-                 int* ovf_count, int64_t* ovf_list, int epi_mode) {
-  using C = TcCfg<KP, SUBS, BN, SPLIT>;
+                 int* ovf_count, int64_t* ovf_list) {
+  using C = TcCfg<KP>;
+  constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -553,206 +612,183 @@ __global__ void __launch_bounds__(TcCfg<KP, SUBS, BN, SPLIT>::kThreads, 1)
   uint64_t* b_full = bars + 4;
   uint64_t* b_empty = b_full + C::kStages;
   uint64_t* t_full = b_empty + C::kStages;
-  uint64_t* t_empty = t_full + C::kAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t d = dv.d;
   const int nB = int((d + BN - 1) / BN);
   const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
+  const int my_vts = (n_vt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  const uint32_t total = uint32_t(my_vts) * uint32_t(nB);  // this CTA's atom tiles
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(a_full + i, 1);
-      mbar_init(a_empty + i, 1);
+      mbar_init(a_full + i, 4);         // the 4 part-0 warps stage A
+      mbar_init(a_empty + i, kParts);   // each issuer commits after its last tile of a voxel tile
     }
-    for (int i = 0; i < C::kAcc; ++i) {
-      mbar_init(t_full + i, 1);
-      mbar_init(t_empty + i, C::kEpiWarps);
-    }
+    for (int i = 0; i < C::kAcc; ++i) mbar_init(t_full + i, 1);
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(b_full + i, 1);
+      mbar_init(b_full + i, 1 + 4);     // producer (with tx) + the 4 warps releasing the stage
       mbar_init(b_empty + i, 1);
     }
+    // tiles 0 .. kAcc-1 find their accumulator stage free: pre-release their first phase
+    for (int i = 0; i < C::kAcc; ++i)
+      for (int w = 0; w < 4; ++w) mbar_arrive(b_full + i);
     mbar_fence_init();
   }
-  if (warp == 2) tmem_alloc(tmem_holder, 512);
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
   if (warp == 0) {
-    // ------------------------------------------------ producer (bulk copies)
-    const uint64_t pol_b = policy_evict_last(), pol_a = policy_evict_first();
-    int st = 0;
-    uint32_t ph = 0;
-    int it = 0;
-    for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
-      const int buf = it & 1;
-      mbar_wait(a_empty + buf, ((it >> 1) & 1) ^ 1);
-      if (elect_one()) {
-        mbar_arrive_expect_tx(a_full + buf, C::kABytes);
-        bulk_g2s(smem + C::kOffA + buf * C::kABytes, ztiles + size_t(vt) * C::kABytes,
-                 C::kABytes, a_full + buf, pol_a);
-      }
-      __syncwarp();
+    // ------------------------------------------------ producer (bulk copies of atom tiles)
+    const uint64_t pol_b = policy_evict_last();
+    uint32_t k = 0;
+    for (int it = 0; it < my_vts; ++it) {
       int ba = rot;
-      for (int b = 0; b < nB; ++b) {
-        mbar_wait(b_empty + st, ph ^ 1);
+      for (int b = 0; b < nB; ++b, ++k) {
+        const int st = int(k % C::kStages);
+        mbar_wait(b_empty + st, ((k / C::kStages) & 1) ^ 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
           bulk_g2s(smem + C::kOffB + st * C::kBBytes, dv.atoms_tc + size_t(ba) * C::kBBytes,
                    C::kBBytes, b_full + st, pol_b);
         }
         __syncwarp();
-        if (++st == C::kStages) { st = 0; ph ^= 1; }
         if (++ba == nB) ba = 0;
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (warp-uniform, elected lane)
-    int st = 0;
-    uint32_t ph = 0;
-    int it = 0;
-    uint32_t tcount = 0;
-    const uint32_t a_base = smem_u32(smem + C::kOffA), b_base = smem_u32(smem + C::kOffB);
-    for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x, ++it) {
-      const int buf = it & 1;
-      mbar_wait(a_full + buf, (it >> 1) & 1);
-      tc_fence_after();
-      for (int b = 0; b < nB; ++b) {
-        const int acc = int(tcount % C::kAcc);
-        mbar_wait(b_full + st, ph);
-        mbar_wait(t_empty + acc, ((tcount / C::kAcc) & 1) ^ 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
-#pragma unroll
-          for (int sub = 0; sub < SUBS; ++sub) {
-            const uint64_t adesc =
-                umma_desc_kmajor(a_base + buf * C::kABytes + sub * C::kATileBytes, KP);
-            const uint32_t dcol = tbase + uint32_t(acc * C::kAccCols + sub * BN);
-#pragma unroll
-            for (int k = 0; k < KP / 16; ++k)
-              tc_mma_bf16(dcol, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), C::kIdesc,
-                          k > 0 ? 1u : 0u);
-          }
-          tc_commit(b_empty + st);
-          tc_commit(t_full + acc);
-        }
-        __syncwarp();
-        ++tcount;
-        if (++st == C::kStages) { st = 0; ph ^= 1; }
+  } else if (warp >= 1 && warp <= kParts) {
+    // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
+    const int me = warp - 1;
+    const uint32_t b_base = smem_u32(smem + C::kOffB);
+    int a_ready = -1;
+    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
+      const int itk = int(kk / uint32_t(nB));
+      const int buf = itk & 1;
+      if (itk > a_ready) {
+        mbar_wait(a_full + buf, (itk >> 1) & 1);
+        a_ready = itk;
       }
-      if (elect_one()) tc_commit(a_empty + buf);
+      const int st = int(kk % C::kStages), s = int(kk % C::kAcc);
+      mbar_wait(b_full + st, (kk / C::kStages) & 1);
+      tc_fence_after();
+      if (lane == 0) CBB_STAMP(0, kk);
+      if (elect_one()) {
+        const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
+        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + buf * C::kACols);
+#pragma unroll
+        for (int kq = 0; kq < KP / 16; ++kq)
+          tc_mma_bf16_ts(tbase + uint32_t(s * C::kAccCols), a_tm + uint32_t(kq * 8),
+                         bdesc + uint64_t(2 * kq), C::kIdesc, kq > 0 ? 1u : 0u);
+        tc_commit(b_empty + st);
+        tc_commit(t_full + s);
+        // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
+        if (kk + kParts >= uint32_t(itk + 1) * uint32_t(nB)) tc_commit(a_empty + buf);
+        CBB_STAMP(1, kk);
+      }
       __syncwarp();
     }
-  } else if (warp >= 4) {
-    // -------------------------------------------------- epilogue
-    const int e = warp - 4;
-    const int q = warp & 3, sub = (e >> 2) % SUBS, part = e / (4 * SUBS);
-    const int row = sub * 128 + q * 32 + lane;  // voxel row inside the voxel tile
+  } else if (warp >= C::kFirstEpiWarp) {
+    // -------------------------------------------------- epilogue parts
+    const int e = warp - C::kFirstEpiWarp;
+    const int part = e >> 2, q = warp & 3;
+    const int row = q * 32 + lane;  // voxel row inside the voxel tile (= TMEM lane)
     const int slot = part * C::kVox + row;
     int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
     float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
-    float* xmax = reinterpret_cast<float*>(smem + C::kOffX);          // [slot] part runmax
-    int* xcnt = reinterpret_cast<int*>(smem + C::kOffX) + C::kSlots;  // [slot] count / -1 = ovf
+    float* xmax = reinterpret_cast<float*>(smem + C::kOffX);           // [slot] part runmax
+    int* xcnt = reinterpret_cast<int*>(smem + C::kOffX) + C::kSlots;   // [slot] count, -1 ovf
+    double* xbs = reinterpret_cast<double*>(smem + C::kOffX + 8 * C::kSlots);  // part best
+    int* xbest = reinterpret_cast<int*>(smem + C::kOffX + 16 * C::kSlots);     // part best atom
     const uint32_t lane_off = uint32_t(q * 32) << 16;
-    unsigned long long* dbg = reinterpret_cast<unsigned long long*>(ovf_list) + 1;
-    uint32_t tcount = 0;
-    for (int vt = blockIdx.x; vt < n_vt; vt += gridDim.x) {
+    const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
+
+    // ---- A for the first voxel tile
+    if (part == 0 && my_vts > 0) {
+      const int64_t v0 = int64_t(blockIdx.x) * C::kVox + row;
+      stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + 0);
+    }
+
+    uint32_t kk = uint32_t(part);  // this part's next tile
+    for (int it = 0; it < my_vts; ++it) {
+      const int vt = int(blockIdx.x) + it * int(gridDim.x);
       const int64_t v = int64_t(vt) * C::kVox + row;
       const bool live = v < n;
+      // ---- stage the NEXT voxel tile's rows into the other A buffer (one tile ahead)
+      if (part == 0 && it + 1 < my_vts) {
+        const int nbuf = (it + 1) & 1;
+        mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const int64_t vn = int64_t(vt + int(gridDim.x)) * C::kVox + row;
+        stage_voxel_row<KP>(zrows, vn, vn < n, a_lane + uint32_t(nbuf * C::kACols));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + nbuf);
+      }
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
       CandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0, false};
       float runmax = -INFINITY, thr = active ? -INFINITY : INFINITY;
-      int ba = rot;
-      for (int b = 0; b < nB; ++b) {
-        const int acc = int(tcount % C::kAcc);
-        mbar_wait(t_full + acc, (tcount / C::kAcc) & 1);
+      const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
+      for (; kk < kend; kk += kParts) {
+        const int s = int(kk % C::kAcc);
+        int ba = rot + int(kk - uint32_t(it) * uint32_t(nB));
+        if (ba >= nB) ba -= nB;
+        mbar_wait(t_full + s, (kk / C::kAcc) & 1);
         tc_fence_after();
-        const bool tail = (ba == nB - 1) && (int64_t(nB) * BN > d);
-        const uint32_t col0 = uint32_t(acc * C::kAccCols + sub * BN + part * C::kCols);
-        const int64_t jb0 = int64_t(ba) * BN + part * C::kCols;
-        if (epi_mode != 2) {
-#pragma unroll
-          for (int h = 0; h + 64 <= C::kCols; h += 64) {
-            float ra[32], rb[32];
-            __syncwarp();
-            const uint32_t taddr = tbase + lane_off + col0 + uint32_t(h);
-            tmem_ld32(taddr, ra);
-            tmem_ld32(taddr + 32, rb);
-            tc_wait_ld();
-            if (epi_mode == 1) {  // dev experiment: TMEM loads only
-              runmax = fmaxf(runmax, fmaxf(ra[0], rb[31]));
-              continue;
-            }
-            screen32(ra, jb0 + h, tail, d, win, runmax, thr, active, cl, epi_mode, dbg);
-            screen32(rb, jb0 + h + 32, tail, d, win, runmax, thr, active, cl, epi_mode, dbg);
-          }
-          if (C::kCols % 64 == 32) {  // odd 32-column remainder
-            float ra[32];
-            __syncwarp();
-            tmem_ld32(tbase + lane_off + col0 + uint32_t(C::kCols - 32), ra);
-            tc_wait_ld();
-            if (epi_mode == 1) runmax = fmaxf(runmax, ra[0]);
-            else
-              screen32(ra, jb0 + C::kCols - 32, tail, d, win, runmax, thr, active, cl, epi_mode,
-                       dbg);
-          }
-        }
+        if (q == 0 && lane == 0) CBB_STAMP(2, kk);
+        float ra[32], rb[32];
+        __syncwarp();
+        const uint32_t taddr = tbase + lane_off + uint32_t(s * C::kAccCols);
+        tmem_ld32(taddr, ra);
+        tmem_ld32(taddr + 32, rb);
+        tc_wait_ld();
+        if (q == 0 && lane == 0) CBB_STAMP(3, kk);
+        // early release: stage s may be overwritten by tile kk + kAcc while we screen
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(t_empty + acc);
-        ++tcount;
-        if (++ba == nB) ba = 0;
+        if (lane == 0) mbar_arrive(b_full + int((kk + C::kAcc) % C::kStages));
+        const bool tail = (ba == nB - 1) && (int64_t(nB) * BN > d);
+        screen64(ra, rb, int64_t(ba) * BN, tail, d, win, runmax, thr, active, cl);
       }
-      if (epi_mode != 0 && epi_mode != 5 && epi_mode < 6) {  // dev experiments: keep live
-        if (runmax == 12345.f) ovf_list[0] = v;
-        continue;
-      }
-      if (SPLIT == 1) {
-        if (live) finalize_voxel(zs, dv, out, v, win, runmax, cl, ovf_count, ovf_list, 32);
-        continue;
-      }
-      // ---- merge the SPLIT per-part lists of each voxel and finalize (part-0 thread)
+      // ---- finalize: every part rescores its own surviving groups, part 0 merges
       xmax[slot] = runmax;
       xcnt[slot] = cl.ovf ? -1 : cl.cnt;
+      named_bar_sync(1, C::kEpiWarps * 32);
+      float gmax = -INFINITY;
+      bool ovf = false;
+#pragma unroll
+      for (int p2 = 0; p2 < kParts; ++p2) {
+        gmax = fmaxf(gmax, xmax[p2 * C::kVox + row]);
+        ovf |= xcnt[p2 * C::kVox + row] < 0;
+      }
+      int64_t best = -1;
+      double bs = -INFINITY;
+      if (live && win >= 0.f && !ovf)
+        rescore_entries(zs, dv, v, cj_base + slot, cs_base + slot, C::kSlots, cl.cnt, gmax - win,
+                        32, best, bs);
+      xbs[slot] = bs;
+      xbest[slot] = int(best);
       named_bar_sync(1, C::kEpiWarps * 32);
       if (part == 0 && live) {
         if (win < 0.f) {
           write_winner(out, dv, v, 0, 0.0);
         } else {
-          float gmax = runmax;
-          bool ovf = false;
-          for (int p2 = 0; p2 < SPLIT; ++p2) {
-            gmax = fmaxf(gmax, xmax[p2 * C::kVox + row]);
-            ovf |= xcnt[p2 * C::kVox + row] < 0;
-          }
-          int64_t best = -1;
-          double bs = -INFINITY;
-          if (epi_mode == 6 || epi_mode == 7) {  // dev: no rescoring
-            best = xcnt[row] > 0 ? cj_base[row] : 0;
-            bs = 1.0;
-            if (epi_mode == 7) best = -2;  // skip the write-back too
-          } else if (!ovf) {
-            const float thr_f = gmax - win;
-            for (int p2 = 0; p2 < SPLIT; ++p2) {
-              const int sl = p2 * C::kVox + row;
-              if (epi_mode == 5) {  // dev: count surviving chunks
-                int sv = 0;
-                for (int c = 0; c < xcnt[sl]; ++c) sv += cs_base[c * C::kSlots + sl] >= thr_f;
-                atomicAdd(reinterpret_cast<unsigned long long*>(ovf_list) + 2,
-                          (unsigned long long)sv);
-              }
-              rescore_entries(zs, dv, v, cj_base + sl, cs_base + sl, C::kSlots, xcnt[sl], thr_f,
-                              32, best, bs);
+          for (int p2 = 1; p2 < kParts; ++p2) {
+            const double b2 = xbs[p2 * C::kVox + row];
+            const int64_t j2 = xbest[p2 * C::kVox + row];
+            if (j2 >= 0 && (best < 0 || b2 > bs || (b2 == bs && j2 < best))) {
+              bs = b2;
+              best = j2;
             }
           }
-          if (best == -2) {
-          } else if (best < 0) {
+          if (ovf || best < 0) {
             const int sl2 = atomicAdd(ovf_count, 1);
             ovf_list[sl2] = v;
           } else {
@@ -760,50 +796,55 @@ __global__ void __launch_bounds__(TcCfg<KP, SUBS, BN, SPLIT>::kThreads, 1)
           }
         }
       }
-      named_bar_sync(1, C::kEpiWarps * 32);
+      // the exchange slots of this tile are rewritten only after every part has streamed the
+      // whole next tile, which needs part 0's stage releases: no third barrier is required
     }
   }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, 512);
   }
 }
 
-// Debug: raw bf16 tcgen05 scores for voxel tile a_tile x atom tile b_tile (128 x 128, SS)
-// -- validates descriptors / swizzle against a host emulation.
+// Debug: raw bf16 tcgen05 scores (A = voxel rows staged into TMEM, B = swizzled atom tile in
+// SMEM) of voxel rows [128 a_tile, +128) x atoms [128 b_tile, +128) -- validates descriptors,
+// the swizzled atom tiles and the TMEM A-operand layout against a host emulation.
 template <int KP>
 __global__ void __launch_bounds__(128, 1)
-    tc_debug_scores_kernel(const uint8_t* __restrict__ ztiles, const uint8_t* __restrict__ atiles,
+    tc_debug_scores_kernel(const uint8_t* __restrict__ zrows, const uint8_t* __restrict__ atiles,
                            int a_tile, int b_tile, float* __restrict__ out) {
   constexpr int kTileBytes = kTileRows * KP * 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kTileBytes);
-  uint32_t* holder = reinterpret_cast<uint32_t*>(smem + 2 * kTileBytes + 16);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kTileBytes);
+  uint32_t* holder = reinterpret_cast<uint32_t*>(smem + kTileBytes + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     mbar_fence_init();
   }
-  if (warp == 0) tmem_alloc(holder, 128);
+  if (warp == 0) tmem_alloc(holder, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *holder;
+  const uint32_t a_col = 128;
+  stage_voxel_row<KP>(zrows, int64_t(a_tile) * 128 + threadIdx.x, true,
+                      tbase + (uint32_t(warp * 32) << 16) + a_col);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(bar, 2 * kTileBytes);
-    bulk_g2s(smem, ztiles + size_t(a_tile) * kTileBytes, kTileBytes, bar, policy_evict_first());
-    bulk_g2s(smem + kTileBytes, atiles + size_t(b_tile) * kTileBytes, kTileBytes, bar,
-             policy_evict_first());
+    mbar_arrive_expect_tx(bar, kTileBytes);
+    bulk_g2s(smem, atiles + size_t(b_tile) * kTileBytes, kTileBytes, bar, policy_evict_first());
     mbar_wait(bar, 0);
     tc_fence_after();
-    const uint64_t ad = umma_desc_kmajor(smem_u32(smem), KP);
-    const uint64_t bd = umma_desc_kmajor(smem_u32(smem + kTileBytes), KP);
+    const uint64_t bd = umma_desc_kmajor(smem_u32(smem), KP);
     for (int k = 0; k < KP / 16; ++k)
-      tc_mma_bf16(tbase, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc_bf16_f32(128, 128),
-                  k > 0);
+      tc_mma_bf16_ts(tbase, tbase + a_col + k * 8, bd + uint64_t(2 * k),
+                     idesc_bf16_f32(128, 128), k > 0);
     tc_commit(bar + 1);
   }
   __syncwarp();
@@ -819,7 +860,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tbase, 128);
+    tmem_dealloc(tbase, 256);
   }
 }
 
@@ -957,13 +998,13 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int KP, int SUBS, int BN, int SPLIT>
+template <int KP>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
-  using C = TcCfg<KP, SUBS, BN, SPLIT>;
+  using C = TcCfg<KP>;
   static bool attr_set = false;
   if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SUBS, BN, SPLIT>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
@@ -971,29 +1012,10 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
-  static int epi_mode = -1;
-  if (epi_mode < 0) {
-    const char* e = getenv("CBB_TC_EPI_MODE");  // development experiments only
-    epi_mode = e ? atoi(e) : 0;
-  }
-  mf_tc_kernel<KP, SUBS, BN, SPLIT><<<grid, C::kThreads, C::kSmem, st>>>(
-      w.ztiles, n, n_vt, w.win_tc, zs, dv, out, w.ovf_count, w.ovf_list, epi_mode);
+  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, zs, dv, out,
+                                                        w.ovf_count, w.ovf_list);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
-}
-
-static int launch_tc32(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                       const ProjOut& out, int max_ctas, cudaStream_t st) {
-  static int cfg = -1;
-  if (cfg < 0) {
-    const char* e = getenv("CBB_TC_CFG");  // development sweep only
-    cfg = e ? atoi(e) : 0;
-  }
-  switch (cfg) {
-    case 1: return launch_tc<32, 2, 128, 1>(w, n, zs, dv, out, max_ctas, st);
-    case 2: return launch_tc<32, 1, 256, 2>(w, n, zs, dv, out, max_ctas, st);
-    default: return launch_tc<32, 2, 128, 2>(w, n, zs, dv, out, max_ctas, st);
-  }
 }
 
 template <int S>
@@ -1059,14 +1081,13 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   }
   ProjOut o = out;
   if (nd_sum && !o.nd_v) o.nd_v = w.nd_v;
-  // tcgen05 path: K = 2s <= 64, and chunk entries pack (atom / 32) into 20 bits
-  const bool tc_ok = (2 * dv.s <= 64) && (dv.d <= (int64_t(1) << 25));
-  if (algo == 0) algo = tc_ok ? 1 : 3;
+  // tcgen05 path: K = 2s <= 64; chunk entries pack (atom / 32) into 20 bits; every epilogue
+  // part needs >= 2 atom tiles of 64 per voxel tile (d > 320; smaller dictionaries use FFMA)
+  const bool tc_ok = (2 * dv.s <= 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
+  if (algo == 0) algo = tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
   if (algo == 1 && !tc_ok) return kErrUnsupported;
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
-  const bool dbg5 = getenv("CBB_TC_EPI_MODE") && atoi(getenv("CBB_TC_EPI_MODE")) == 5;
-  if (dbg5) CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_list, 0, 3 * sizeof(int64_t), st));
   if (algo == 1 || algo == 2) {
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
@@ -1075,18 +1096,11 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
         dv.s_pad);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
-    int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc32(w, n, zr, dv, o, max_ctas, st)
-                                          : launch_tc<64, 2, 128, 2>(w, n, zr, dv, o, max_ctas, st))
+    int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
+                                          : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
                          : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
-    if (dbg5) {
-      unsigned long long h[3];
-      cudaMemcpyAsync(h, w.ovf_list, sizeof(h), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      fprintf(stderr, "[dbg] slow warp-chunks=%llu surviving chunks=%llu\n", h[1], h[2]);
-    }
-    if (!getenv("CBB_TC_EPI_MODE") || atoi(getenv("CBB_TC_EPI_MODE")) == 0 ||
-        atoi(getenv("CBB_TC_EPI_MODE")) >= 5 || algo != 1) {
+    {
       rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
       if (rc) return rc;
     }
@@ -1119,7 +1133,7 @@ int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cuda
 int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile, int b_tile,
                     float* out, cudaStream_t st) {
   const int tile_bytes = kTileRows * kpad * 2;
-  const int smem = 2 * tile_bytes + 64 + 1024;
+  const int smem = tile_bytes + 64 + 1024;
   if (kpad == 32) {
     CBB_CUDA_TRY(cudaFuncSetAttribute(tc_debug_scores_kernel<32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1136,6 +1150,15 @@ int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
+
+#ifdef CBB_TRACE
+int trace_dump(long long* host, int count) {
+  CBB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 4 * count));
+  return kOk;
+}
+#else
+int trace_dump(long long*, int) { return kErrUnsupported; }
+#endif
 
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr,
                   cudaStream_t st) {

@@ -1,0 +1,33 @@
+"""Per-hop latency trace of the tcgen05 pipeline (development aid; needs the TRACE=1 build)."""
+import ctypes, os, sys
+os.environ.setdefault("CBB_LIB_PATH", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1810_01967_b200", "libcoverblip_b200_trace.so"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1810_01967_b200 as cb
+from paper_1810_01967_b200 import _lib
+from paper_1810_01967_b200.workloads import random_atoms, cone_voxels
+from paper_1810_01967_b200.projection import project_device
+N = 1 << 18; D = 1 << 17
+atoms = random_atoms(D, 10, seed=0)
+Z, _ = cone_voxels(atoms, N, seed=1, dtype=np.complex64)
+dd = cb.device_dictionary(atoms); zt = torch.from_numpy(Z).cuda()
+for _ in range(3):
+    project_device(zt, dd, algo="tcgen05", proj_c128=False)
+torch.cuda.synchronize()
+lib = _lib.load()
+fn = lib.cbb_dev_trace_dump; fn.restype = ctypes.c_int; fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+T = 2048
+buf = np.zeros(T * 4, dtype=np.int64)
+assert fn(buf.ctypes.data, T) == 0
+t = buf.reshape(T, 4).astype(np.float64)
+ks = np.arange(200, 1900)
+def med(x): return float(np.median(x))
+print("issue wait->commit (issuer)      ", med(t[ks, 1] - t[ks, 0]))
+print("commit -> epi t_full wake        ", med(t[ks, 2] - t[ks, 1]))
+print("epi wake -> loaded (LDTM)        ", med(t[ks, 3] - t[ks, 2]))
+print("release(k-6) -> issuer wake(k)   ", med(t[ks, 0] - t[ks - 6, 3]))
+print("period between issues            ", med(t[ks + 1, 0] - t[ks, 0]))
+print("epi wake period (same part, k->k+3)", med(t[ks + 3, 2] - t[ks, 2]))
+print("epi loaded(k) -> wake(k+3) (screen+wait)", med(t[ks + 3, 2] - t[ks, 3]))
+for k in range(600, 612):
+    print(k, [int(x) for x in (t[k] - t[600, 0])])

@@ -125,11 +125,11 @@ def test_reference_kats():
 def test_ties_zero_rows_and_duplicates():
     p = _pkg()
     rng = np.random.default_rng(9)
-    base = random_atoms(rng, 200, 10)
+    base = random_atoms(rng, 400, 10)
     atoms = np.concatenate([base, base[:50]])      # exact duplicate atoms: ties -> lowest index
     Z = rng.standard_normal((300, 10)) + 1j * rng.standard_normal((300, 10))
     Z[::7] = 0.0                                   # all-zero rows -> index 0, gamma 0
-    Z[5] = 3.0 * atoms[210]                        # duplicate of atom 10 -> must pick 10
+    Z[5] = 3.0 * atoms[410]                        # duplicate of atom 10 -> must pick 10
     for algo in ("tcgen05", "ffma", "exhaustive"):
         r = p.project_cone_exact(Z, atoms, algo=algo)
         assert r.indices[5] == 10
