@@ -61,6 +61,15 @@ int cbb_abi_version(void);
 const char* cbb_last_error(void);
 int cbb_device_sm_count(int* out);
 
+/* ---- diagnostics ---- */
+/* Number of kernels this library has enqueued (process lifetime). */
+unsigned long long cbb_stats_kernel_launches(void);
+/* When enabled, CUDA events are recorded immediately before and after the matched-filter
+ * kernel of every projection on the caller's stream; cbb_timing_last_ms returns the last
+ * interval (synchronises on the end event).  Thread-local. */
+int cbb_timing_enable(int32_t on);
+int cbb_timing_last_ms(float* ms);
+
 /* ---- dictionary (projection.py:26-29) ---- */
 size_t cbb_dict_storage_bytes(int64_t d, int32_t s);
 int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s, void* storage,
@@ -80,6 +89,16 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
                      const cbb_dict_view* dict, int32_t* idx_out, double* gamma_out,
                      void* xnext_out, void* dx_out, double* nd_out, void* workspace,
                      size_t workspace_bytes, int32_t algo, void* stream);
+/* Atom-sharded building block (multi-GPU): per voxel the shard-local exact argmax
+ * reported as a GLOBAL atom index (local + atom_offset, int64) and its raw fp64 score
+ * Re<z, d_j*> (not clipped at 0), for the cross-rank combine (cbb_argmax_select). */
+int cbb_project_best(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
+                     int64_t atom_offset, int64_t* idx_out, double* score_out, void* workspace,
+                     size_t workspace_bytes, int32_t algo, void* stream);
+/* out[v] = gamma[v] * atoms[idx[v] - atom_offset] if this shard owns idx[v], else 0
+ * (projection.py:64 write-back of the winners a shard owns; outputs are summed over ranks). */
+int cbb_scaled_rows(const cbb_dict_view* dict, int64_t atom_offset, const int64_t* idx,
+                    const double* gamma, int64_t n, void* out, int32_t out_c128, void* stream);
 /* Number of voxels that needed the exhaustive fp64 rescan in the last call (synchronises). */
 int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count_host,
                                void* stream);

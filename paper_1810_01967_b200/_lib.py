@@ -37,6 +37,9 @@ SIGNATURES = {
     "cbb_abi_version": (c_int, []),
     "cbb_last_error": (ctypes.c_char_p, []),
     "cbb_device_sm_count": (c_int, [ctypes.POINTER(c_int)]),
+    "cbb_stats_kernel_launches": (ctypes.c_ulonglong, []),
+    "cbb_timing_enable": (c_int, [c_i32]),
+    "cbb_timing_last_ms": (c_int, [ctypes.POINTER(ctypes.c_float)]),
     "cbb_dict_storage_bytes": (c_size, [c_i64, c_i32]),
     "cbb_dict_prepare": (c_int, [c_vp, c_i32, c_i64, c_i32, c_vp, ctypes.POINTER(DictView), c_vp]),
     "cbb_project_workspace_bytes": (c_size, [c_i64, c_i32]),
@@ -44,6 +47,10 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_step": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, ctypes.POINTER(DictView), c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32, c_vp]),
+    "cbb_project_best": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_i64, c_vp, c_vp,
+                                 c_vp, c_size, c_i32, c_vp]),
+    "cbb_scaled_rows": (c_int, [ctypes.POINTER(DictView), c_i64, c_vp, c_vp, c_i64, c_vp, c_i32,
+                                c_vp]),
     "cbb_project_overflow_count": (c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_int), c_vp]),
     "cbb_project_prologue": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_size,
                                      c_vp]),

@@ -6,9 +6,21 @@
 #include <cstring>
 #include <string>
 
+#include <atomic>
+
 namespace cbb {
 static thread_local std::string g_last_error;
 void set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(int k) { g_launches.fetch_add((unsigned long long)k); }
+
+// Optional CUDA events bracketing the matched-filter kernel (enabled by cbb_timing_enable).
+static thread_local cudaEvent_t g_ev[2] = {nullptr, nullptr};
+static thread_local bool g_timing = false;
+void timing_mark(int which, cudaStream_t st) {
+  if (g_timing && g_ev[which]) cudaEventRecord(g_ev[which], st);
+}
 
 // cbb_project.cu
 size_t dict_bytes(int64_t d, int s, size_t*, size_t*, size_t*, size_t*);
@@ -23,6 +35,8 @@ int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile
                     float* out, cudaStream_t st);
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr, cudaStream_t st);
 int trace_dump(long long* host, int count);
+int scaled_rows(const DictView& dv, int64_t offset, const int64_t* idx, const double* gamma,
+                int64_t n, void* out, int out128, cudaStream_t st);
 
 // cbb_operator.cu
 struct Op;
@@ -120,9 +134,30 @@ int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_d
     return kErrArgument;
   }
   ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr};
-  ProjOut o{idx_out, idx_int64, gamma_out, proj_out, proj_c128, nullptr, nullptr, nullptr};
+  ProjOut o{idx_out, idx_int64, gamma_out, proj_out, proj_c128, nullptr, nullptr, nullptr,
+            nullptr, 0};
   return project(zs, n, to_view(dict), o, nullptr, workspace, workspace_bytes, algo, 0,
                  S(stream));
+}
+
+int cbb_project_best(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
+                     int64_t atom_offset, int64_t* idx_out, double* score_out, void* workspace,
+                     size_t workspace_bytes, int32_t algo, void* stream) {
+  if (int rc = check_view(dict)) return rc;
+  if (n > 0 && (!z || !idx_out || !score_out)) {
+    set_last_error("cbb_project_best: null argument");
+    return kErrArgument;
+  }
+  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr};
+  ProjOut o{idx_out, 1, nullptr, nullptr, 0, nullptr, nullptr, nullptr, score_out, atom_offset};
+  return project(zs, n, to_view(dict), o, nullptr, workspace, workspace_bytes, algo, 0,
+                 S(stream));
+}
+
+int cbb_scaled_rows(const cbb_dict_view* dict, int64_t atom_offset, const int64_t* idx,
+                    const double* gamma, int64_t n, void* out, int32_t out_c128, void* stream) {
+  if (int rc = check_view(dict)) return rc;
+  return scaled_rows(to_view(dict), atom_offset, idx, gamma, n, out, out_c128, S(stream));
 }
 
 int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64_t n,
@@ -137,7 +172,7 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
   ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), float(mu),
              static_cast<float2*>(z_out)};
   ProjOut o{idx_out, 0, gamma_out, xnext_out, 0, static_cast<const float2*>(x),
-            static_cast<float2*>(dx_out), nullptr};
+            static_cast<float2*>(dx_out), nullptr, nullptr, 0};
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));
 }
 
@@ -165,6 +200,24 @@ int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_ti
 // development only (not in the public header): per-tile clock stamps of CTA 0
 __attribute__((visibility("default"))) int cbb_dev_trace_dump(long long* host, int count) {
   return trace_dump(host, count);
+}
+
+unsigned long long cbb_stats_kernel_launches(void) { return g_launches.load(); }
+
+int cbb_timing_enable(int32_t on) {
+  if (on && !g_ev[0]) {
+    CBB_CUDA_TRY(cudaEventCreate(&g_ev[0]));
+    CBB_CUDA_TRY(cudaEventCreate(&g_ev[1]));
+  }
+  g_timing = on != 0;
+  return kOk;
+}
+
+int cbb_timing_last_ms(float* ms) {
+  if (!g_ev[0]) return kErrArgument;
+  CBB_CUDA_TRY(cudaEventSynchronize(g_ev[1]));
+  CBB_CUDA_TRY(cudaEventElapsedTime(ms, g_ev[0], g_ev[1]));
+  return kOk;
 }
 
 // ---------------------------------------------------------------- operator

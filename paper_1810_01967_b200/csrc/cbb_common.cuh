@@ -35,6 +35,10 @@ enum Status : int {
 
 void set_last_error(const char* msg);
 
+// Diagnostics shared by all translation units (defined in cbb_capi.cu).
+void count_launches(int k);                    // kernels enqueued by this library
+void timing_mark(int which, cudaStream_t st);  // 0 = before / 1 = after the matched filter
+
 // ---------------------------------------------------------------- layout
 // Tensor-core operand rows: K_PAD bf16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, 0..]
 // stored in 128-row tiles with the UMMA K-major SWIZZLE_64B (K_PAD=32) or

@@ -345,6 +345,7 @@ int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st) {
   CBB_CUDA_TRY(cudaGetLastError());
   int rc = fft(op, F, CUFFT_FORWARD, st);
   if (rc) return rc;
+  count_launches(2);
   return gather(op, F, 0, nullptr, nullptr, Y, nullptr, st);
 }
 
@@ -359,6 +360,7 @@ int op_adjoint(Op* op, const float2* Y, float2* X, void* ws, cudaStream_t st) {
   dim3 grid(unsigned((op->n + 31) / 32), unsigned((op->L + 31) / 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(F, op->L, op->n, op->scale, X);
   CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(2);
   return kOk;
 }
 
@@ -378,6 +380,7 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
     rc = gather(op, F, 0, nullptr, nullptr, Y, norm_out ? part : nullptr, st);
   }
   if (rc) return rc;
+  count_launches(norm_out ? 3 : 2);
   if (norm_out) return finish(part, kRedBlocks, norm_out, st);
   return kOk;
 }
@@ -395,6 +398,7 @@ int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float
   compress_frames_kernel<<<unsigned((op->n + 255) / 256), 256, 0, st>>>(F, V, s, op->n, op->L,
                                                                         op->scale, Gc);
   CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(2);
   return kOk;
 }
 
@@ -403,6 +407,7 @@ int vec_op(const float2* a, double alpha, const float2* b, int64_t count, const 
   double* part = static_cast<double*>(ws);
   vec_kernel<<<kRedBlocks, 256, 0, st>>>(a, alpha, b, count, w, mode, R, part);
   CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(out ? 2 : 1);
   if (out) return finish(part, kRedBlocks, out, st);
   return kOk;
 }
@@ -410,6 +415,7 @@ int vec_op(const float2* a, double alpha, const float2* b, int64_t count, const 
 int scale_c64(float2* a, double alpha, int64_t count, cudaStream_t st) {
   scale_kernel<<<grid_for(count), 256, 0, st>>>(a, float(alpha), count);
   CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return kOk;
 }
 

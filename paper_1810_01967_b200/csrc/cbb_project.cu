@@ -77,10 +77,11 @@ __device__ void write_winner(const ProjOut& out, const DictView& dv, int64_t v, 
   const int s = dv.s;
   const double gamma = score > 0.0 ? score : 0.0;
   if (out.idx) {
-    if (out.idx64) reinterpret_cast<int64_t*>(out.idx)[v] = j;
-    else reinterpret_cast<int32_t*>(out.idx)[v] = int32_t(j);
+    if (out.idx64) reinterpret_cast<int64_t*>(out.idx)[v] = j + out.idx_offset;
+    else reinterpret_cast<int32_t*>(out.idx)[v] = int32_t(j + out.idx_offset);
   }
   if (out.gamma) out.gamma[v] = gamma;
+  if (out.score) out.score[v] = score;
   const double2* a = dv.atoms64 + j * s;
   double nd = 0.0;
   for (int k = 0; k < s; ++k) {
@@ -864,6 +865,38 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
+// ============================================================== atom-shard write-back
+// out[v] = gamma[v] * atoms[idx[v] - offset] when this shard owns idx[v], else 0 (the shards'
+// outputs are then summed across ranks).  One thread per (voxel, component).
+__global__ void scaled_rows_kernel(const double2* __restrict__ atoms64, int64_t d, int s,
+                                   int64_t offset, const int64_t* __restrict__ idx,
+                                   const double* __restrict__ gamma, int64_t n, void* out,
+                                   int out128) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * s) return;
+  const int64_t v = e / s, k = e % s;
+  const int64_t j = idx[v] - offset;
+  double2 r = make_double2(0.0, 0.0);
+  if (j >= 0 && j < d) {
+    const double2 a = atoms64[j * s + k];
+    r = make_double2(gamma[v] * a.x, gamma[v] * a.y);
+  }
+  if (out128) reinterpret_cast<double2*>(out)[e] = r;
+  else reinterpret_cast<float2*>(out)[e] = make_float2(float(r.x), float(r.y));
+}
+
+int scaled_rows(const DictView& dv, int64_t offset, const int64_t* idx, const double* gamma,
+                int64_t n, void* out, int out128, cudaStream_t st) {
+  if (n == 0) return kOk;
+  const int64_t total = n * dv.s;
+  scaled_rows_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(dv.atoms64, dv.d, dv.s,
+                                                                    offset, idx, gamma, n, out,
+                                                                    out128);
+  CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  return kOk;
+}
+
 // ============================================================== deterministic sums
 __global__ void __launch_bounds__(256) reduce_stage1(const double* __restrict__ x, int64_t n,
                                                      double* __restrict__ partial) {
@@ -1096,10 +1129,13 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
         dv.s_pad);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
+    timing_mark(0, st);
     int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
                                           : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
                          : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
+    timing_mark(1, st);
+    count_launches(3);  // prologue, screening kernel, exhaustive rescan
     {
       rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
       if (rc) return rc;
@@ -1115,10 +1151,14 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     }
     int rc = launch_exhaustive(n, zs, dv, nullptr, nullptr, o, st);
     if (rc) return rc;
+    count_launches(zs.x != nullptr ? 2 : 1);
   } else {
     return kErrArgument;
   }
-  if (nd_sum) return reduce_sum(o.nd_v, n, w.partial, nd_sum, st);
+  if (nd_sum) {
+    count_launches(2);
+    return reduce_sum(o.nd_v, n, w.partial, nd_sum, st);
+  }
   return kOk;
 }
 

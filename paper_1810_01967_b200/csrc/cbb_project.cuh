@@ -54,7 +54,9 @@ struct ProjOut {
   int32_t proj128;
   const float2* x;     // IPG: dX = proj(c64) - x
   float2* dx;
-  double* nd_v;        // per-voxel ||dX_v||^2 (fp64), or ||proj - z||^2-free if null
+  double* nd_v;        // per-voxel ||dX_v||^2 (fp64)
+  double* score;       // raw fp64 best score Re<z, d_j*> (before the clip at 0), atom sharding
+  int64_t idx_offset;  // added to the written index (global atom id of this dictionary shard)
 };
 
 }  // namespace cbb
