@@ -103,19 +103,76 @@ def project_cone_exact(Z, dictionary, *, algo: str = "auto") -> ConeProjection:
     dd = device_dictionary(dictionary, dev)
     if not np.iscomplexobj(Z) or Z.dtype not in (np.complex64, np.complex128):
         Z = Z.astype(np.complex128)
-    zt = torch.from_numpy(np.ascontiguousarray(Z)).to(dev, non_blocking=True)
-    proj_dtype = torch.complex128
+    Z = np.ascontiguousarray(Z)
+    zh = torch.from_numpy(Z)
     with torch.cuda.device(dev):
-        idx, gam, proj = project_device(zt, dd, algo=algo, proj_c128=True)
-        h_idx = torch.empty(n, dtype=torch.int64, pin_memory=True)
-        h_gam = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        h_proj = torch.empty((n, Z.shape[1]), dtype=proj_dtype, pin_memory=True)
-        h_idx.copy_(idx, non_blocking=True)
-        h_gam.copy_(gam, non_blocking=True)
-        h_proj.copy_(proj, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-    return ConeProjection(indices=h_idx.numpy(), gammas=h_gam.numpy(),
-                          projected=h_proj.numpy(), cost=n * d)
+        if zh.is_pinned() and n >= _PIPELINE_MIN:
+            idx, gam, proj = _project_pipelined(zh, dd, algo, dev)
+        else:
+            zt = zh.to(dev, non_blocking=True)
+            didx, dgam, dproj = project_device(zt, dd, algo=algo, proj_c128=True)
+            idx = torch.empty(n, dtype=torch.int64, pin_memory=True)
+            gam = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            proj = torch.empty((n, Z.shape[1]), dtype=torch.complex128, pin_memory=True)
+            idx.copy_(didx, non_blocking=True)
+            gam.copy_(dgam, non_blocking=True)
+            proj.copy_(dproj, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+    return ConeProjection(indices=idx.numpy(), gammas=gam.numpy(), projected=proj.numpy(),
+                          cost=n * d)
+
+
+_PIPELINE_MIN = 1 << 16
+_PIPELINE_CHUNK = 1 << 17
+_streams: dict = {}
+
+
+def _pipe_streams(dev):
+    key = dev.index
+    if key not in _streams:
+        _streams[key] = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
+    return _streams[key]
+
+
+def _project_pipelined(zh: torch.Tensor, dd: DeviceDictionary, algo: str, dev):
+    """Pinned host input: H2D of chunk i+1 and D2H of chunk i-1 overlap the projection of
+    chunk i (copy engines in both directions run concurrently with the SMs)."""
+    n, s = int(zh.shape[0]), int(zh.shape[1])
+    s_in, s_cmp, s_out = _pipe_streams(dev)
+    cur = torch.cuda.current_stream(dev)
+    for st in (s_in, s_cmp, s_out):
+        st.wait_stream(cur)
+    zt = torch.empty((n, s), dtype=zh.dtype, device=dev)
+    didx = torch.empty(n, dtype=torch.int64, device=dev)
+    dgam = torch.empty(n, dtype=torch.float64, device=dev)
+    dproj = torch.empty((n, s), dtype=torch.complex128, device=dev)
+    hidx = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    hgam = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hproj = torch.empty((n, s), dtype=torch.complex128, pin_memory=True)
+    chunk = _PIPELINE_CHUNK
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        e_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            zt[lo:hi].copy_(zh[lo:hi], non_blocking=True)
+            e_in.record(s_in)
+        s_cmp.wait_event(e_in)
+        e_cmp = torch.cuda.Event()
+        with torch.cuda.stream(s_cmp):
+            project_device(zt[lo:hi], dd, algo=algo, proj_c128=True,
+                           out=(didx[lo:hi], dgam[lo:hi], dproj[lo:hi]))
+            e_cmp.record(s_cmp)
+        s_out.wait_event(e_cmp)
+        with torch.cuda.stream(s_out):
+            hidx[lo:hi].copy_(didx[lo:hi], non_blocking=True)
+            hgam[lo:hi].copy_(dgam[lo:hi], non_blocking=True)
+            hproj[lo:hi].copy_(dproj[lo:hi], non_blocking=True)
+    s_out.synchronize()
+    for t in (zt, didx, dgam, dproj):
+        t.record_stream(s_in)
+        t.record_stream(s_cmp)
+        t.record_stream(s_out)
+    return hidx, hgam, hproj
 
 
 def overflow_count(n: int, s: int) -> int:

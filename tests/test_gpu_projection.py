@@ -175,3 +175,22 @@ def test_device_tensor_roundtrip():
     rh = p.project_cone_exact(Z, atoms)
     np.testing.assert_array_equal(r.indices.cpu().numpy(), rh.indices)
     np.testing.assert_array_equal(r.gammas.cpu().numpy(), rh.gammas)
+
+
+def test_pinned_pipelined_path_matches_device_path():
+    """numpy + pinned host buffers take the chunked H2D/compute/D2H pipeline."""
+    p = _pkg()
+    from paper_1810_01967_b200.device import pinned_empty
+    from paper_1810_01967_b200.workloads import cone_voxels, random_atoms as ra
+    atoms = ra(4096, 10, seed=3)
+    Z, _ = cone_voxels(atoms, 300_000, seed=4)
+    Zp = pinned_empty(Z.shape, np.complex128)
+    Zp[:] = Z
+    r_pipe = p.project_cone_exact(Zp, atoms)
+    r_dev = p.project_cone_exact(torch.from_numpy(Z).cuda(), atoms)
+    np.testing.assert_array_equal(r_pipe.indices, r_dev.indices.cpu().numpy())
+    np.testing.assert_array_equal(r_pipe.gammas, r_dev.gammas.cpu().numpy())
+    np.testing.assert_array_equal(r_pipe.projected, r_dev.projected.cpu().numpy())
+    sub = slice(0, 2000)
+    assert_parity(Z[sub], atoms, type(r_pipe)(r_pipe.indices[sub], r_pipe.gammas[sub],
+                                               r_pipe.projected[sub], 0), allow_ties=False)
