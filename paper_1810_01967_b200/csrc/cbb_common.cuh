@@ -102,6 +102,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Blocking wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes instead of re-issuing try_wait (spinning steals issue slots from the epilogue).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAITS_%=;\n\t}" ::"r"(addr),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- bulk copy (TMA engine)
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                          uint64_t* bar, uint64_t policy) {

@@ -441,11 +441,11 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
 // development tracing: per-tile clock64 stamps of CTA 0 (issuer: after b_full wait, after
 // commit; epilogue part warp q0: after t_full wait, after wait::ld)
 constexpr int kTraceTiles = 2048;
-__device__ long long g_trace[kTraceTiles * 4];
+__device__ long long g_trace[kTraceTiles * 8];
 #define CBB_STAMP(slot, k)                                                          \
   do {                                                                              \
     if (blockIdx.x == 0 && (k) < uint32_t(kTraceTiles))                             \
-      g_trace[(k) * 4 + (slot)] = clock64();                                        \
+      g_trace[(k) * 8 + (slot)] = clock64();                                        \
   } while (0)
 #else
 #define CBB_STAMP(slot, k) \
@@ -563,15 +563,18 @@ __device__ __forceinline__ void screen64(float (&ra)[32], float (&rb)[32], int64
   chunk_max(ra, jb, tail, d, ca);
   chunk_max(rb, jb + 32, tail, d, cb);
   const float cm = fmaxf(ca.cm, cb.cm);
-  if (cm >= thr) {
-    runmax = fmaxf(runmax, cm);
-    if (active) {
-      thr = runmax - win;
-      if (ca.cm >= thr && !cl.ovf) record_chunk(ra, ca, jb, thr, cl);
-      if (cb.cm >= thr && !cl.ovf) record_chunk(rb, cb, jb + 32, thr, cl);
-      if (cl.ovf) {
-        active = false;
-        thr = INFINITY;
+  // warp-uniform test: the fast path carries no divergent branch / reconvergence
+  if (__any_sync(0xffffffffu, cm >= thr)) {
+    if (cm >= thr) {
+      runmax = fmaxf(runmax, cm);
+      if (active) {
+        thr = runmax - win;
+        if (ca.cm >= thr && !cl.ovf) record_chunk(ra, ca, jb, thr, cl);
+        if (cb.cm >= thr && !cl.ovf) record_chunk(rb, cb, jb + 32, thr, cl);
+        if (cl.ovf) {
+          active = false;
+          thr = INFINITY;
+        }
       }
     }
   }
@@ -674,7 +677,8 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         a_ready = itk;
       }
       const int st = int(kk % C::kStages), s = int(kk % C::kAcc);
-      mbar_wait(b_full + st, (kk / C::kStages) & 1);
+      if (lane == 0) CBB_STAMP(4, kk);
+      mbar_wait_sleep(b_full + st, (kk / C::kStages) & 1);
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
@@ -737,11 +741,16 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       CandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0, false};
       float runmax = -INFINITY, thr = active ? -INFINITY : INFINITY;
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
+      // incremental tile bookkeeping (no per-tile div/mod): stage s = kk % kAcc with phase
+      // (kk / kAcc) & 1, release barrier (kk + kAcc) % kStages, atom tile (rot + b) % nB
+      int s = int(kk % C::kAcc);
+      uint32_t ph = (kk / C::kAcc) & 1;
+      int rel = int((kk + C::kAcc) % C::kStages);
+      int ba = rot + int(kk - uint32_t(it) * uint32_t(nB));
+      if (ba >= nB) ba -= nB;
       for (; kk < kend; kk += kParts) {
-        const int s = int(kk % C::kAcc);
-        int ba = rot + int(kk - uint32_t(it) * uint32_t(nB));
-        if (ba >= nB) ba -= nB;
-        mbar_wait(t_full + s, (kk / C::kAcc) & 1);
+        if (q == 0 && lane == 0) CBB_STAMP(5, kk);
+        mbar_wait_sleep(t_full + s, ph);
         tc_fence_after();
         if (q == 0 && lane == 0) CBB_STAMP(2, kk);
         float ra[32], rb[32];
@@ -754,9 +763,19 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         // early release: stage s may be overwritten by tile kk + kAcc while we screen
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(b_full + int((kk + C::kAcc) % C::kStages));
+        if (lane == 0) mbar_arrive(b_full + rel);
         const bool tail = (ba == nB - 1) && (int64_t(nB) * BN > d);
         screen64(ra, rb, int64_t(ba) * BN, tail, d, win, runmax, thr, active, cl);
+        if (q == 0 && lane == 0) CBB_STAMP(6, kk);
+        s += kParts;
+        if (s >= C::kAcc) {
+          s -= C::kAcc;
+          ph ^= 1u;
+        }
+        rel += kParts;
+        if (rel >= C::kStages) rel -= C::kStages;
+        ba += kParts;
+        if (ba >= nB) ba -= nB;
       }
       // ---- finalize: every part rescores its own surviving groups, part 0 merges
       xmax[slot] = runmax;
@@ -1193,7 +1212,7 @@ int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile
 
 #ifdef CBB_TRACE
 int trace_dump(long long* host, int count) {
-  CBB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 4 * count));
+  CBB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 8 * count));
   return kOk;
 }
 #else

@@ -17,17 +17,19 @@ torch.cuda.synchronize()
 lib = _lib.load()
 fn = lib.cbb_dev_trace_dump; fn.restype = ctypes.c_int; fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 T = 2048
-buf = np.zeros(T * 4, dtype=np.int64)
+buf = np.zeros(T * 8, dtype=np.int64)
 assert fn(buf.ctypes.data, T) == 0
-t = buf.reshape(T, 4).astype(np.float64)
+t = buf.reshape(T, 8).astype(np.float64)
 ks = np.arange(200, 1900)
 def med(x): return float(np.median(x))
-print("issue wait->commit (issuer)      ", med(t[ks, 1] - t[ks, 0]))
-print("commit -> epi t_full wake        ", med(t[ks, 2] - t[ks, 1]))
-print("epi wake -> loaded (LDTM)        ", med(t[ks, 3] - t[ks, 2]))
-print("release(k-6) -> issuer wake(k)   ", med(t[ks, 0] - t[ks - 6, 3]))
-print("period between issues            ", med(t[ks + 1, 0] - t[ks, 0]))
-print("epi wake period (same part, k->k+3)", med(t[ks + 3, 2] - t[ks, 2]))
-print("epi loaded(k) -> wake(k+3) (screen+wait)", med(t[ks + 3, 2] - t[ks, 3]))
-for k in range(600, 612):
-    print(k, [int(x) for x in (t[k] - t[600, 0])])
+print("issuer: wait b_full (4->0)          ", med(t[ks, 0] - t[ks, 4]))
+print("issuer: issue+commit (0->1)         ", med(t[ks, 1] - t[ks, 0]))
+print("issuer: loop overhead (1 -> next 4) ", med(t[ks + 3, 4] - t[ks, 1]))
+print("epi: wait t_full (5->2)             ", med(t[ks, 2] - t[ks, 5]))
+print("epi: load (2->3)                    ", med(t[ks, 3] - t[ks, 2]))
+print("epi: screen (3->6)                  ", med(t[ks, 6] - t[ks, 3]))
+print("epi: loop overhead (6 -> next 5)    ", med(t[ks + 3, 5] - t[ks, 6]))
+print("epi: part period (2 -> next 2)      ", med(t[ks + 3, 2] - t[ks, 2]))
+print("commit -> t_full ready (1->2)       ", med(t[ks, 2] - t[ks, 1]))
+print("release(k-6) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 6, 3]))
+print("frac of part time waiting           ", med((t[ks, 2] - t[ks, 5]) / (t[ks + 3, 2] - t[ks, 2])))

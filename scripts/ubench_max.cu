@@ -36,6 +36,9 @@ __global__ void k(float* out, int iters, float seed) {
       else if (MODE == 1) a[i] = fmaxf(a[i], b);
       else if (MODE == 2) a[i] = __fmaf_rn(a[i], b, c);
       else if (MODE == 4) { double t = fma(double(a[i]), double(b), double(c)); a[i] = float(t); }
+      else if (MODE == 5) { unsigned u = __float_as_uint(a[i]); u = max(max(u, __float_as_uint(b)), __float_as_uint(c)); a[i] = __uint_as_float(u); }
+      else if (MODE == 6) { unsigned u = __float_as_uint(a[i]); u = max(u, __float_as_uint(b)); a[i] = __uint_as_float(u); }
+      else if (MODE == 7) { if (i & 1) { unsigned u = __float_as_uint(a[i]); u = max(max(u, __float_as_uint(b)), __float_as_uint(c)); a[i] = __uint_as_float(u); } else a[i] = max3(a[i], b, c); }
       else a[i] = (i & 1) ? fmaxf(a[i], b) : max3(a[i], b, c);
     }
     b += 1e-7f; c -= 1e-7f;
@@ -46,8 +49,9 @@ __global__ void k(float* out, int iters, float seed) {
 int main() {
   float* out; cudaMalloc(&out, 148 * 8 * 1024 * 4);
   const int iters = 1 << 14;
-  const char* names[5] = {"FMNMX3", "FMNMX", "FFMA", "FMNMX3+FMNMX interleaved", "DFMA(+cvt)"};
-  for (int mode = 0; mode < 5; ++mode) {
+  const char* names[8] = {"FMNMX3", "FMNMX", "FFMA", "FMNMX3+FMNMX interleaved", "DFMA(+cvt)",
+                          "VIMNMX3.U32", "VIMNMX.U32", "VIMNMX3+FMNMX3 interleaved"};
+  for (int mode = 0; mode < 8; ++mode) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
@@ -56,6 +60,9 @@ int main() {
       if (mode == 2) k<2><<<148 * 8, 1024>>>(out, iters, 1.0f);
       if (mode == 3) k<3><<<148 * 8, 1024>>>(out, iters, 1.0f);
       if (mode == 4) k<4><<<148 * 8, 1024>>>(out, iters / 16, 1.0f);
+      if (mode == 5) k<5><<<148 * 8, 1024>>>(out, iters, 1.0f);
+      if (mode == 6) k<6><<<148 * 8, 1024>>>(out, iters, 1.0f);
+      if (mode == 7) k<7><<<148 * 8, 1024>>>(out, iters, 1.0f);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
     }
     float ms; cudaEventElapsedTime(&ms, e0, e1);
