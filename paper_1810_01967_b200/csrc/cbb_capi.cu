@@ -192,7 +192,7 @@ int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dic
 int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_tile,
                         int32_t b_tile, float* out, void* stream) {
   if (int rc = check_view(dict)) return rc;
-  if (2 * dict->s > 64) return kErrUnsupported;
+  if (2 * dict->s >= 64) return kErrUnsupported;
   // voxel tiles sit at the start of the projection workspace
   return tc_debug_scores(workspace, dict->atoms_tc, dict->kpad, a_tile, b_tile, out, S(stream));
 }

@@ -7,7 +7,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "coverblip_b200 is written for sm_100a only"
@@ -40,13 +40,16 @@ void count_launches(int k);                    // kernels enqueued by this libra
 void timing_mark(int which, cudaStream_t st);  // 0 = before / 1 = after the matched filter
 
 // ---------------------------------------------------------------- layout
-// Tensor-core operand rows: K_PAD bf16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, 0..]
+// Tensor-core operand rows: K_PAD fp16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, 0.., sentinel]
+// with 2s < K_PAD: the last column is the padding sentinel (voxel rows 1.0, real atoms 0, the
+// zero-padded atom rows of the last tile -65504 so they can never win or enter a window).
 // stored in 128-row tiles with the UMMA K-major SWIZZLE_64B (K_PAD=32) or
 // SWIZZLE_128B (K_PAD=64) canonical layout so a flat bulk copy lands a tile in
 // shared memory ready for tcgen05.mma.
 constexpr int kTileRows = 128;
 
-__host__ __device__ inline int kpad_for(int s) { return (2 * s <= 32) ? 32 : 64; }
+__host__ __device__ inline int kpad_for(int s) { return (2 * s < 32) ? 32 : 64; }
+constexpr unsigned short kF16One = 0x3C00, kF16MinusMax = 0xFBFF;  // 1.0, -65504
 
 // Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.
 __host__ __device__ inline uint32_t tile_chunk_offset(int r, int c, int kpad) {
@@ -68,12 +71,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
-__device__ __forceinline__ unsigned short bf16_bits_rn(float x) {
-  __nv_bfloat16 h = __float2bfloat16_rn(x);
-  return *reinterpret_cast<unsigned short*>(&h);
+// fp16 operand element: round-to-nearest-even straight from fp64 (the rounding error is
+// measured exactly from the returned value, so any rounding would do for the certificate).
+__device__ __forceinline__ unsigned short f16_bits_rn(double x) {
+  return __half_as_ushort(__double2half(x));
 }
-__device__ __forceinline__ float bf16_bits_to_float(unsigned short b) {
-  return __uint_as_float(uint32_t(b) << 16);
+__device__ __forceinline__ double f16_bits_to_double(unsigned short b) {
+  return double(__half2float(__ushort_as_half(b)));
 }
 
 // ---------------------------------------------------------------- mbarrier
@@ -159,18 +163,9 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate).
-__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (A operand resident in tensor memory).
-__device__ __forceinline__ void tc_mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (operand / accumulator types from the idesc;
+// A operand resident in tensor memory).
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                                uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -211,6 +206,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
       : "r"(taddr));
 }
 
+// 32 lanes x 64 consecutive 16-bit accumulator columns packed in pairs (.pack::16b): register
+// i of thread t holds columns 2i (low half) and 2i + 1 (high half) of lane (base_lane + t).
+__device__ __forceinline__ void tmem_ld32_pack16(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
 // UMMA shared-memory descriptor, K-major, swizzled rows (SBO = 8 rows).
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, int kpad) {
   const uint32_t row_bytes = uint32_t(kpad) * 2u;
@@ -224,9 +234,13 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, int kpa
   return d;
 }
 
-// Instruction descriptor: kind::f16, A/B = BF16, D = F32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+// Instruction descriptor: kind::f16, A/B = F16, D = F16 (c/a/b format fields 0), K-major.
+// Measured accumulation model (scripts/probe_f16acc.cu, tests/test_gpu_projection.py): each
+// K = 16 instruction forms its products' sum exactly and rounds it ONCE to fp16 (round to
+// nearest even) when adding to the accumulator; the result sits in the low 16 bits of each
+// 32-bit TMEM column.
+__host__ __device__ constexpr uint32_t idesc_f16_f16(int M, int N) {
+  return (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 // ---------------------------------------------------------------- exact scoring

@@ -1,12 +1,13 @@
 // Exact cone projection on B200 (sm_100a).  See cbb_project.cuh for the scheme.
 //
 // Kernels
-//   prep_dict_kernel     dictionary -> fp64 copy, planar fp32 copy, bf16 UMMA tiles, error bounds
-//   prologue_kernel      Z (or X - mu G) -> bf16 UMMA voxel tiles + certified windows
-//   mf_tc_kernel<KP>     tcgen05 bf16 screening, persistent + warp specialised:
-//                          warp 0 bulk-copy producer, warp 1 MMA issuer, warp 2 TMEM owner,
-//                          warps 4..11 epilogue (TMEM -> regs, running max + certified
-//                          candidates, fp64 rescoring and write-back of the winner)
+//   prep_dict_kernel     dictionary -> fp64 copy, planar fp32 copy, max ||d||, fp32 bounds
+//   prep_tc_kernel       dictionary -> scaled fp16 UMMA tiles + their bounds
+//   prologue_kernel      Z (or X - mu G) -> scaled fp16 voxel rows + certified windows
+//   mf_tc_kernel<KP>     tcgen05 fp16 screening (fp16 accumulators), persistent + warp
+//                          specialised: warp 0 bulk-copy producer, warps 1..3 MMA issuers,
+//                          12 epilogue warps in 3 parts (TMEM -> packed regs, running max +
+//                          certified candidates, fp64 rescoring and write-back of the winner)
 //   mf_ffma_kernel<S>    fp32 FFMA screening with the same candidate machinery
 //   exhaustive_kernel    fp64 exhaustive scan for overflowed voxels (and for s > 32)
 //   reduce kernels       deterministic two-stage fp64 sums
@@ -140,10 +141,7 @@ struct CandList {
   }
 };
 
-// Rescore in fp64 every atom of the list entries that survive the final window.  An entry is
-// (first atom index, approximate max over its `span` atoms): span 1 for the FFMA screen (one
-// atom per entry), 32 for the tcgen05 screen (one 32-atom chunk per entry).  Ties keep the
-// lowest index (np.argmax, projection.py:62).
+// Rescore in fp64 one candidate atom; ties keep the lowest index (np.argmax, projection.py:62).
 __device__ __forceinline__ void rescore_one(const ZSource& zs, const DictView& dv, int64_t v,
                                             int64_t j, int64_t& best, double& bs) {
   const double sc = exact_score_g(zs, v, dv.s, dv.atoms64 + j * dv.s);
@@ -153,43 +151,27 @@ __device__ __forceinline__ void rescore_one(const ZSource& zs, const DictView& d
   }
 }
 
-// Chunk entries of the tcgen05 screen: (first atom / 32) in bits [0,20), and a 12-bit mask of
-// the 3-wide groups (bits 0..9 -> atoms 3g..3g+2) and the two trailing atoms (bits 10, 11)
-// whose approximate scores reached the window when the chunk was recorded.
+// Chunk entries of the tcgen05 screen: (first atom / 32) in bits [0,20) and a 6-bit mask of
+// the groups (bit g < 5 -> atoms 6g..6g+5, bit 5 -> atoms 30, 31) whose approximate scores
+// reached the window when the chunk was recorded.
 constexpr int kChunkShift = 20;
 __device__ __forceinline__ int pack_chunk(int64_t jb, uint32_t mask) {
   return int(uint32_t(jb >> 5) | (mask << kChunkShift));
 }
 
+// FFMA screen entries (one atom each) that survive the final window.
 __device__ __forceinline__ void rescore_entries(const ZSource& zs, const DictView& dv, int64_t v,
                                                 const int* cj, const float* cs, int stride,
-                                                int cnt, float thr, int span, int64_t& best,
-                                                double& bs) {
-  for (int c = 0; c < cnt; ++c) {
-    if (cs[c * stride] >= thr) {
-      const int e = cj[c * stride];
-      if (span == 1) {
-        rescore_one(zs, dv, v, e, best, bs);
-        continue;
-      }
-      const int64_t j0 = int64_t(uint32_t(e) & ((1u << kChunkShift) - 1)) << 5;
-      uint32_t mask = uint32_t(e) >> kChunkShift;
-      while (mask) {
-        const int b = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int lo = b < 10 ? 3 * b : 20 + b, hi = b < 10 ? lo + 3 : lo + 1;
-        for (int i = lo; i < hi; ++i)
-          if (j0 + i < dv.d) rescore_one(zs, dv, v, j0 + i, best, bs);
-      }
-    }
-  }
+                                                int cnt, float thr, int64_t& best, double& bs) {
+  for (int c = 0; c < cnt; ++c)
+    if (cs[c * stride] >= thr) rescore_one(zs, dv, v, cj[c * stride], best, bs);
 }
 
 // Rescore the certified candidates in fp64 and write the winner; zero voxels go
 // straight to index 0 (np.argmax of an all-zero row); overflow -> exhaustive list.
 __device__ void finalize_voxel(const ZSource& zs, const DictView& dv, const ProjOut& out,
                                int64_t v, float win, float runmax, const CandList& cl,
-                               int* ovf_count, int64_t* ovf_list, int span = 1) {
+                               int* ovf_count, int64_t* ovf_list) {
   if (win < 0.f) {
     write_winner(out, dv, v, 0, 0.0);
     return;
@@ -197,7 +179,7 @@ __device__ void finalize_voxel(const ZSource& zs, const DictView& dv, const Proj
   int64_t best = -1;
   double bs = -INFINITY;
   if (!cl.ovf)
-    rescore_entries(zs, dv, v, cl.cj, cl.cs, cl.stride, cl.cnt, runmax - win, span, best, bs);
+    rescore_entries(zs, dv, v, cl.cj, cl.cs, cl.stride, cl.cnt, runmax - win, best, bs);
   if (best < 0) {
     int slot = atomicAdd(ovf_count, 1);
     ovf_list[slot] = v;
@@ -207,15 +189,13 @@ __device__ void finalize_voxel(const ZSource& zs, const DictView& dv, const Proj
 }
 
 // ============================================================== dictionary preparation
+// Pass 1: fp64 / fp32 copies, max ||d|| and the fp32 bounds.
 __global__ void prep_dict_kernel(const void* __restrict__ atoms_in, int in128, int64_t d, int s,
-                                 int s_pad, int kpad, double2* __restrict__ atoms64,
-                                 float* __restrict__ atoms32, uint8_t* __restrict__ atoms_tc,
-                                 float* __restrict__ bounds) {
+                                 int s_pad, double2* __restrict__ atoms64,
+                                 float* __restrict__ atoms32, float* __restrict__ bounds) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= d) return;
-  double del_bf = 0, nrm = 0, nrm_bf = 0, del32 = 0, nrm32 = 0;
-  const int tile = int(j / kTileRows), r = int(j % kTileRows);
-  uint8_t* trow = atoms_tc + size_t(tile) * kTileRows * kpad * 2;
+  double nrm = 0, del32 = 0, nrm32 = 0;
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (in128) {
@@ -229,19 +209,7 @@ __global__ void prep_dict_kernel(const void* __restrict__ atoms_in, int in128, i
     const float re32 = float(re), im32 = float(im);
     atoms32[j * 2 * s_pad + k] = re32;
     atoms32[j * 2 * s_pad + s_pad + k] = im32;
-    const unsigned short bre = bf16_bits_rn(re32), bim = bf16_bits_rn(im32);
-    const double fre = bf16_bits_to_float(bre), fim = bf16_bits_to_float(bim);
-    // element e -> 16B chunk e/8, offset (e%8)*2 bytes
-    const int e_re = k, e_im = s + k;
-    if (2 * s <= 64) {
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_re >> 3, kpad) +
-                                       (e_re & 7) * 2) = bre;
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_im >> 3, kpad) +
-                                       (e_im & 7) * 2) = bim;
-    }
     nrm += re * re + im * im;
-    nrm_bf += fre * fre + fim * fim;
-    del_bf += (re - fre) * (re - fre) + (im - fim) * (im - fim);
     nrm32 += double(re32) * re32 + double(im32) * im32;
     del32 += (re - re32) * (re - re32) + (im - im32) * (im - im32);
   }
@@ -249,25 +217,74 @@ __global__ void prep_dict_kernel(const void* __restrict__ atoms_in, int in128, i
     atoms32[j * 2 * s_pad + k] = 0.f;
     atoms32[j * 2 * s_pad + s_pad + k] = 0.f;
   }
-  atomic_max_nonneg(bounds + kBDeltaBf16, __double2float_ru(sqrt(del_bf)));
   atomic_max_nonneg(bounds + kBDmax, __double2float_ru(sqrt(nrm)));
-  atomic_max_nonneg(bounds + kBDbfMax, __double2float_ru(sqrt(nrm_bf)));
   atomic_max_nonneg(bounds + kBDelta32, __double2float_ru(sqrt(del32)));
   atomic_max_nonneg(bounds + kBD32Max, __double2float_ru(sqrt(nrm32)));
 }
 
+// Power-of-two scale putting max||scale * d|| in [0.5, 1) (1 for an all-zero dictionary).
+__device__ __forceinline__ double dict_scale(const float* bounds) {
+  const double dmax = bounds[kBDmax];
+  if (!(dmax > 0.0) || !isfinite(dmax)) return 1.0;
+  int e;
+  frexp(dmax, &e);
+  return ldexp(1.0, -e);
+}
+
+// Pass 2: fp16 UMMA tiles of scale_d * d (pre-swizzled, one bulk copy per 64-atom tile) and
+// their bounds.  2s <= 64 only (tensor-core path).
+__global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, int64_t d_pad,
+                               int s, int kpad, uint8_t* __restrict__ atoms_tc,
+                               float* __restrict__ bounds) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= d_pad) return;
+  const int tile = int(j / kTileRows), r = int(j % kTileRows);
+  uint8_t* trow = atoms_tc + size_t(tile) * kTileRows * kpad * 2;
+  const int e_sent = kpad - 1;
+  if (j >= d) {  // zero-padded row of the last tile: sentinel score -65504 for every voxel
+    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_sent >> 3, kpad) +
+                                       (e_sent & 7) * 2) = kF16MinusMax;
+    return;
+  }
+  const double sc = dict_scale(bounds);
+  if (j == 0) bounds[kBScaleD] = float(sc);
+  double del = 0, nrm_h = 0;
+  for (int k = 0; k < s; ++k) {
+    const double2 a = atoms64[j * s + k];
+    const double re = a.x * sc, im = a.y * sc;
+    const unsigned short hre = f16_bits_rn(re), him = f16_bits_rn(im);
+    const double fre = f16_bits_to_double(hre), fim = f16_bits_to_double(him);
+    // element e -> 16B chunk e/8, offset (e%8)*2 bytes
+    const int e_re = k, e_im = s + k;
+    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_re >> 3, kpad) +
+                                       (e_re & 7) * 2) = hre;
+    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_im >> 3, kpad) +
+                                       (e_im & 7) * 2) = him;
+    nrm_h += fre * fre + fim * fim;
+    del += (re - fre) * (re - fre) + (im - fim) * (im - fim);
+  }
+  atomic_max_nonneg(bounds + kBDeltaH, __double2float_ru(sqrt(del)));
+  atomic_max_nonneg(bounds + kBDhMax, __double2float_ru(sqrt(nrm_h)));
+}
+
 // ============================================================== prologue
-// One thread per voxel (n_pad = whole voxel tiles).  Produces the bf16 UMMA
-// voxel tiles and both certified windows:
-//   |s~ - s| <= ||z - z~|| * max||d|| + ||z~|| * max||d - d~|| + acc(K) * ||z~|| * max||d~||
-// window = 2 * bound (true argmax j* satisfies s~_j* >= max s~ - window).
+// One thread per voxel (n_pad = whole voxel tiles).  Produces the fp16 tensor-core voxel rows
+// z~ = fp16(scale_v z) (scale_v a power of two putting ||scale_v z|| in [2^12, 2^13), so with
+// max||d~|| <= 1 every fp16 partial sum stays far below 65504) and both certified windows.
+// In the scaled units of the tensor-core scores (scale_v * scale_d * Re<z, d>):
+//   |s~ - s| <= ||scale_v z - z~|| * scale_d max||d|| + ||z~|| * max||scale_d d - d~||
+//              + acc * ||z~|| * max||d~||
+// where acc covers the fp16 accumulator: one round-to-nearest per K = 16 instruction of a
+// value bounded by sum|products| (<= ||z~|| ||d~||), i.e. (KP/16) * 2^-11, plus slack for
+// internal alignment and fp16 subnormals.  window = 2 * bound: the true argmax j* satisfies
+// s~_j* >= max s~ - window.  The FFMA window (win32) is in unscaled fp32 units.
 __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int kpad,
                                 const float* __restrict__ bounds, uint8_t* __restrict__ ztiles,
                                 float* __restrict__ win_tc, float* __restrict__ win32,
                                 int s_pad) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
-  // plain row-major bf16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
+  // plain row-major fp16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
   uint8_t* trow = ztiles ? ztiles + size_t(v) * kpad * 2 : nullptr;
   if (v >= n) {
     if (trow)
@@ -275,10 +292,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
         *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
   }
-  unsigned short row[64];
-#pragma unroll
-  for (int e = 0; e < 64; ++e) row[e] = 0;
-  double nz = 0, ez_bf = 0, nz_bf = 0, ez32 = 0, nz32 = 0;
+  double nz = 0, ez32 = 0, nz32 = 0;
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (zs.x != nullptr) {
@@ -294,42 +308,76 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       re = a.x; im = a.y;
     }
     const float re32 = float(re), im32 = float(im);
-    const unsigned short bre = bf16_bits_rn(re32), bim = bf16_bits_rn(im32);
-    if (trow) {  // tensor-core path requires 2s <= 64
-      row[k] = bre;
-      row[s + k] = bim;
-    }
-    const double fre = bf16_bits_to_float(bre), fim = bf16_bits_to_float(bim);
     nz += re * re + im * im;
-    ez_bf += (re - fre) * (re - fre) + (im - fim) * (im - fim);
-    nz_bf += fre * fre + fim * fim;
     ez32 += (re - re32) * (re - re32) + (im - im32) * (im - im32);
     nz32 += double(re32) * re32 + double(im32) * im32;
   }
-  if (trow) {
-    for (int c = 0; c < kpad / 8; ++c) {
-      uint4 pk;
-      pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
-      pk.y = uint32_t(row[c * 8 + 2]) | (uint32_t(row[c * 8 + 3]) << 16);
-      pk.z = uint32_t(row[c * 8 + 4]) | (uint32_t(row[c * 8 + 5]) << 16);
-      pk.w = uint32_t(row[c * 8 + 6]) | (uint32_t(row[c * 8 + 7]) << 16);
-      *reinterpret_cast<uint4*>(trow + c * 16) = pk;
-    }
-  }
-  const double dmax = bounds[kBDmax], dbf = bounds[kBDbfMax], delbf = bounds[kBDeltaBf16];
+  const double dmax = bounds[kBDmax];
   const double d32 = bounds[kBD32Max], del32 = bounds[kBDelta32];
   if (nz == 0.0) {
     if (win_tc) win_tc[v] = -1.f;
     if (win32) win32[v] = -1.f;
+    if (trow)
+      for (int c = 0; c < kpad / 8; ++c)
+        *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
   }
-  // tensor-core fp32 accumulation: generous (K + 32) ulp-of-2^-23 per unit of sum |products|
-  const double acc_tc = double(kpad + 32) * 0x1p-23;
+  if (!isfinite(nz)) {  // inf / NaN voxel: no screening, the exhaustive fp64 scan decides
+    if (win_tc) win_tc[v] = __int_as_float(0x7fc00000);
+    if (win32) win32[v] = __int_as_float(0x7fc00000);
+    if (trow)
+      for (int c = 0; c < kpad / 8; ++c)
+        *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
+    return;
+  }
   const double acc32 = double(2 * s_pad + 4) * 0x1p-24;
-  const double eb = sqrt(ez_bf) * dmax + sqrt(nz_bf) * delbf + acc_tc * sqrt(nz_bf) * dbf;
   const double e3 = sqrt(ez32) * dmax + sqrt(nz32) * del32 + acc32 * sqrt(nz32) * d32;
-  if (win_tc) win_tc[v] = __double2float_ru(2.0 * eb * 1.001 + 1e-30);
   if (win32) win32[v] = __double2float_ru(2.0 * e3 * 1.001 + 1e-30);
+  if (!trow) return;
+  int ez;
+  frexp(sqrt(nz), &ez);
+  const double sv = ldexp(1.0, 13 - ez);
+  unsigned short row[64];
+#pragma unroll
+  for (int e = 0; e < 64; ++e) row[e] = 0;
+  double eh = 0, nzh = 0;
+  for (int k = 0; k < s; ++k) {
+    double re, im;
+    if (zs.x != nullptr) {
+      const float2 xk = zs.x[v * s + k], gk = zs.g[v * s + k];
+      re = __fmaf_rn(-zs.mu, gk.x, xk.x);
+      im = __fmaf_rn(-zs.mu, gk.y, xk.y);
+    } else if (zs.z128) {
+      double2 a = reinterpret_cast<const double2*>(zs.z)[v * s + k];
+      re = a.x; im = a.y;
+    } else {
+      float2 a = reinterpret_cast<const float2*>(zs.z)[v * s + k];
+      re = a.x; im = a.y;
+    }
+    re *= sv;
+    im *= sv;
+    const unsigned short hre = f16_bits_rn(re), him = f16_bits_rn(im);
+    row[k] = hre;
+    row[s + k] = him;
+    const double fre = f16_bits_to_double(hre), fim = f16_bits_to_double(him);
+    eh += (re - fre) * (re - fre) + (im - fim) * (im - fim);
+    nzh += fre * fre + fim * fim;
+  }
+  row[kpad - 1] = kF16One;  // sentinel column (2s < kpad)
+  for (int c = 0; c < kpad / 8; ++c) {
+    uint4 pk;
+    pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
+    pk.y = uint32_t(row[c * 8 + 2]) | (uint32_t(row[c * 8 + 3]) << 16);
+    pk.z = uint32_t(row[c * 8 + 4]) | (uint32_t(row[c * 8 + 5]) << 16);
+    pk.w = uint32_t(row[c * 8 + 6]) | (uint32_t(row[c * 8 + 7]) << 16);
+    *reinterpret_cast<uint4*>(trow + c * 16) = pk;
+  }
+  const double sd = bounds[kBScaleD], dh = bounds[kBDhMax], delh = bounds[kBDeltaH];
+  const double nq = double(kpad / 16);
+  const double acc_tc = nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
+  const double eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh +
+                    nq * 0x1p-24;
+  win_tc[v] = __double2float_ru(2.0 * eb * 1.001 + 1e-30);
 }
 
 // ============================================================== FFMA screening
@@ -442,45 +490,52 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
 // commit; epilogue part warp q0: after t_full wait, after wait::ld)
 constexpr int kTraceTiles = 2048;
 __device__ long long g_trace[kTraceTiles * 8];
+__device__ long long g_trace_vt[256 * 4];  // per voxel tile of CTA 0: loop start, finalize start/end
 #define CBB_STAMP(slot, k)                                                          \
   do {                                                                              \
     if (blockIdx.x == 0 && (k) < uint32_t(kTraceTiles))                             \
       g_trace[(k) * 8 + (slot)] = clock64();                                        \
   } while (0)
+#define CBB_STAMP_VT(slot, it)                                                      \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (it) < 256) g_trace_vt[(it) * 4 + (slot)] = clock64();   \
+  } while (0)
 #else
 #define CBB_STAMP(slot, k) \
   do {                     \
+  } while (0)
+#define CBB_STAMP_VT(slot, it) \
+  do {                         \
   } while (0)
 #endif
 
 // ============================================================== tcgen05 screening
 // One CTA per SM (persistent).  Per voxel tile (128 voxels):
-//   * the voxel operand A (bf16, K = KP) lives in TENSOR MEMORY (double buffered): part-0
+//   * the voxel operand A (fp16, K = KP) lives in TENSOR MEMORY (double buffered): part-0
 //     epilogue threads tcgen05.st their own voxel row into their TMEM lane one tile ahead;
-//   * warp 0 streams atom tiles (BN = 64 rows, pre-swizzled bf16) through a bulk-copy ring;
+//   * warp 0 streams atom tiles (BN = 128 rows, pre-swizzled fp16) through a bulk-copy ring;
 //   * warps 1..kParts issue the MMAs: issuer i owns the CTA's atom tiles k = i (mod kParts),
-//     i.e. accumulator stages i, i + kParts (kAcc = 2 kParts stages of 64 columns) and the
+//     i.e. accumulator stage i (kAcc = kParts stages of 128 fp16 accumulator columns) and the
 //     B-ring stages st = i (mod kParts); per tile it waits ONE barrier, b_full[st], whose phase
 //     completes when the tile's bytes have landed AND the epilogue released the accumulator
 //     stage (the epilogue arrives on the b_full of the tile that will reuse its stage), then
-//     issues KP/16 MMAs (M=128, N=64, K=16, A from TMEM, B from SMEM) and commits;
+//     issues KP/16 MMAs (M=128, N=128, K=16, A from TMEM, B from SMEM) and commits;
 //   * epilogue part p (4 warps, one per TMEM lane quarter) consumes tiles k = p (mod kParts):
-//     it copies the 64 scores per lane into registers and releases the stage immediately, so
-//     the screening runs while the tensor core refills it;
+//     it copies the 128 packed scores per lane into registers and releases the stage at once,
+//     so the screening runs while the tensor core refills it.
 // Every mbarrier has a single waiter role that consumes its phases in order (no parity
-// aliasing): b_full[st] -> issuer st % kParts (kStages % kParts == 0), t_full[s] -> part
-// s % kParts, b_empty -> producer, a_full -> issuers, a_empty -> part 0.  An epilogue arrival
-// for tile k + kAcc lands on b_full[(k + kAcc) % kStages] only after that barrier's previous
-// phase (tile k + kAcc - kStages) completed: the same issuer issued that tile before tile k.
+// aliasing): b_full[st] -> issuer st % kParts (kStages % kParts == 0), t_full[s] -> part s,
+// b_empty -> producer, a_full -> issuers, a_empty -> part 0.  An epilogue arrival for tile
+// k + kAcc lands on b_full[(k + kAcc) % kStages] only after that barrier's previous phase
+// (tile k + kAcc - kStages) completed: the same issuer issued that tile before tile k.
 // Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
 constexpr int kParts = 3;
 
 template <int KP>
 struct TcCfg {
-  static constexpr int BN = 64;
-  static constexpr int kAColsPerSub = KP / 2;                // packed bf16 pairs per lane
-  static constexpr int kACols = kAColsPerSub;                // one A buffer (128 voxels)
-  static constexpr int kAcc = 2 * kParts;                    // 6 stages x 64 columns
+  static constexpr int BN = 128;
+  static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
+  static constexpr int kAcc = kParts;                        // one 128-column stage per part
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
@@ -496,15 +551,14 @@ struct TcCfg {
   static constexpr int kOffB = 0;
   static constexpr int kOffCj = kOffB + kStages * kBBytes;
   static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
-  static constexpr int kOffX = kOffCs + kCandCap * kSlots * 4;  // per-slot exchange (24 B)
-  static constexpr int kOffBar = kOffX + kSlots * 24;
+  static constexpr int kOffBar = kOffCs + kCandCap * kSlots * 4;
   static constexpr int kNumBars = 4 + 2 * kStages + kAcc;
   static_assert(kStages % kParts == 0 && kAcc % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr uint32_t kIdesc = idesc_bf16_f32(128, BN);
-  static constexpr int kMinTiles = kAcc;  // nB >= kAcc: every part owns >= 2 tiles per voxel tile
+  static constexpr uint32_t kIdesc = idesc_f16_f16(128, BN);
+  static constexpr int kMinTiles = kAcc;  // nB >= kAcc: every part owns >= 1 tile per voxel tile
 };
 
 __device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
@@ -524,56 +578,68 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // Screen approximate scores of one voxel (one thread): running max + certified window.
-// Fast path per 64 scores: 32 three-input maxes + one compare.  When a 32-chunk max enters
-// the window the chunk (first atom, mask of 3-wide groups inside the window, chunk max) is
-// recorded -- no per-value inserts; the finalize rescans only the flagged groups exactly.
-// Any atom inside the final window lies in a flagged group of a recorded chunk, so the
-// certificate is unchanged.
-struct ChunkMax {
-  float m[10];
-  float cm;
-};
+// The fp16 accumulators arrive packed (register m = atoms 2m, 2m+1).  Fast path per 128
+// scores: four 3-input packed max chains (VHMNMX, 35 instructions, one chain per 32-atom
+// chunk) + one compare + a warp vote.
+// Only when some lane's max reaches its threshold (rare after the first tiles) the chunks are
+// examined: a 32-atom chunk whose max enters the window is recorded (first atom, mask of
+// 6-atom groups inside the window, chunk max) -- no per-value inserts; the finalize rescans
+// only the flagged groups exactly.  Any atom inside the final window lies in a flagged group of
+// a recorded chunk, so the certificate is unchanged.  Thresholds are rounded DOWN to fp16
+// (never excludes an atom the exact window admits).
+__device__ __forceinline__ __half2 as_h2(uint32_t x) {
+  return *reinterpret_cast<const __half2*>(&x);
+}
+__device__ __forceinline__ __half2 hmax3(__half2 a, __half2 b, __half2 c) {
+  return __hmax2(__hmax2(a, b), c);  // fused by ptxas into one VHMNMX
+}
+__device__ __forceinline__ __half hmax_halves(__half2 m) {
+  return __hmax(__low2half(m), __high2half(m));
+}
 
-__device__ __forceinline__ void chunk_max(float (&r)[32], int64_t jb, bool tail, int64_t d,
-                                          ChunkMax& c) {
-  if (tail) {
+// Record 32-atom chunk (16 packed registers) with max cm: groups g < 5 -> registers
+// 3g..3g+2 (atoms 6g..6g+5), g = 5 -> register 15 (atoms 30, 31).
+__device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64_t jb, __half thr,
+                                             float thr_f, CandList& cl) {
+  uint32_t mask = __hge(hmax_halves(as_h2(r[15])), thr) ? (1u << 5) : 0u;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (jb + i >= d) r[i] = -INFINITY;
+  for (int i = 0; i < 5; ++i)
+    mask |= __hge(hmax_halves(hmax3(as_h2(r[3 * i]), as_h2(r[3 * i + 1]), as_h2(r[3 * i + 2]))),
+                  thr)
+                ? (1u << i)
+                : 0u;
+  cl.insert(pack_chunk(jb, mask), __half2float(cm), thr_f);
+}
+
+__device__ __forceinline__ void screen128(const uint32_t (&r)[64], int64_t jb, float win,
+                                          __half& runmax, __half& thr, bool& active,
+                                          CandList& cl) {
+  // four independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
+  __half2 c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t* q = r + 16 * k;
+    __half2 a = hmax3(as_h2(q[0]), as_h2(q[1]), as_h2(q[2]));
+#pragma unroll
+    for (int i = 3; i < 15; i += 2) a = hmax3(a, as_h2(q[i]), as_h2(q[i + 1]));
+    c[k] = __hmax2(a, as_h2(q[15]));
   }
-#pragma unroll
-  for (int g = 0; g < 10; ++g) c.m[g] = fmax3(r[3 * g], r[3 * g + 1], r[3 * g + 2]);
-  const float n0 = fmax3(c.m[0], c.m[1], c.m[2]), n1 = fmax3(c.m[3], c.m[4], c.m[5]);
-  const float n2 = fmax3(c.m[6], c.m[7], c.m[8]);
-  c.cm = fmax3(n0, n1, fmax3(n2, c.m[9], fmaxf(r[30], r[31])));
-}
-
-__device__ __forceinline__ void record_chunk(const float (&r)[32], const ChunkMax& c,
-                                             int64_t jb, float thr, CandList& cl) {
-  uint32_t mask = (r[30] >= thr ? (1u << 10) : 0u) | (r[31] >= thr ? (1u << 11) : 0u);
-#pragma unroll
-  for (int g = 0; g < 10; ++g) mask |= (c.m[g] >= thr) ? (1u << g) : 0u;
-  cl.insert(pack_chunk(jb, mask), c.cm, thr);
-}
-
-__device__ __forceinline__ void screen64(float (&ra)[32], float (&rb)[32], int64_t jb, bool tail,
-                                         int64_t d, float win, float& runmax, float& thr,
-                                         bool& active, CandList& cl) {
-  ChunkMax ca, cb;
-  chunk_max(ra, jb, tail, d, ca);
-  chunk_max(rb, jb + 32, tail, d, cb);
-  const float cm = fmaxf(ca.cm, cb.cm);
+  const __half cm = hmax_halves(__hmax2(hmax3(c[0], c[1], c[2]), c[3]));
   // warp-uniform test: the fast path carries no divergent branch / reconvergence
-  if (__any_sync(0xffffffffu, cm >= thr)) {
-    if (cm >= thr) {
-      runmax = fmaxf(runmax, cm);
+  if (__any_sync(0xffffffffu, __hge(cm, thr))) {
+    if (__hge(cm, thr)) {
+      runmax = __hmax(runmax, cm);
       if (active) {
-        thr = runmax - win;
-        if (ca.cm >= thr && !cl.ovf) record_chunk(ra, ca, jb, thr, cl);
-        if (cb.cm >= thr && !cl.ovf) record_chunk(rb, cb, jb + 32, thr, cl);
+        thr = __float2half_rd(__half2float(runmax) - win);
+        const float thr_f = __half2float(thr);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __half ck = hmax_halves(c[k]);
+          if (__hge(ck, thr) && !cl.ovf) record_chunk(r + 16 * k, ck, jb + 32 * k, thr, thr_f, cl);
+        }
         if (cl.ovf) {
           active = false;
-          thr = INFINITY;
+          thr = __ushort_as_half(0x7C00);  // +inf
         }
       }
     }
@@ -604,8 +670,8 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
 template <int KP>
 __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
-                 const float* __restrict__ win_tc, ZSource zs, DictView dv, ProjOut out,
-                 int* ovf_count, int64_t* ovf_list) {
+                 const float* __restrict__ win_tc, DictView dv, int64_t n_pad,
+                 int2* __restrict__ cand, int2* __restrict__ meta) {
   using C = TcCfg<KP>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -649,12 +715,12 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------ producer (bulk copies of atom tiles)
     const uint64_t pol_b = policy_evict_last();
-    uint32_t k = 0;
+    int st = 0;
+    uint32_t ph = 0;
     for (int it = 0; it < my_vts; ++it) {
       int ba = rot;
-      for (int b = 0; b < nB; ++b, ++k) {
-        const int st = int(k % C::kStages);
-        mbar_wait(b_empty + st, ((k / C::kStages) & 1) ^ 1);
+      for (int b = 0; b < nB; ++b) {
+        mbar_wait(b_empty + st, ph ^ 1u);
         if (elect_one()) {
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
           bulk_g2s(smem + C::kOffB + st * C::kBBytes, dv.atoms_tc + size_t(ba) * C::kBBytes,
@@ -662,39 +728,50 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         }
         __syncwarp();
         if (++ba == nB) ba = 0;
+        if (++st == C::kStages) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
     }
   } else if (warp >= 1 && warp <= kParts) {
     // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
     const int me = warp - 1;
     const uint32_t b_base = smem_u32(smem + C::kOffB);
-    int a_ready = -1;
+    const uint32_t d_tm = tbase + uint32_t(me * C::kAccCols);  // stage me (kAcc == kParts)
+    int itk = -1;
+    uint32_t vt_end = 0;  // first tile index of the next voxel tile
+    int st = me;
+    uint32_t ph = 0;
     for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
-      const int itk = int(kk / uint32_t(nB));
-      const int buf = itk & 1;
-      if (itk > a_ready) {
-        mbar_wait(a_full + buf, (itk >> 1) & 1);
-        a_ready = itk;
+      if (kk >= vt_end) {  // first tile of this issuer in a new voxel tile: wait for its A
+        ++itk;
+        vt_end += uint32_t(nB);
+        mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
-      const int st = int(kk % C::kStages), s = int(kk % C::kAcc);
       if (lane == 0) CBB_STAMP(4, kk);
-      mbar_wait_sleep(b_full + st, (kk / C::kStages) & 1);
+      mbar_wait_sleep(b_full + st, ph);
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
         const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
-        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + buf * C::kACols);
+        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kACols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq)
-          tc_mma_bf16_ts(tbase + uint32_t(s * C::kAccCols), a_tm + uint32_t(kq * 8),
-                         bdesc + uint64_t(2 * kq), C::kIdesc, kq > 0 ? 1u : 0u);
+          tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * kq), C::kIdesc,
+                        kq > 0 ? 1u : 0u);
         tc_commit(b_empty + st);
-        tc_commit(t_full + s);
+        tc_commit(t_full + me);
         // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
-        if (kk + kParts >= uint32_t(itk + 1) * uint32_t(nB)) tc_commit(a_empty + buf);
+        if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
         CBB_STAMP(1, kk);
       }
       __syncwarp();
+      st += kParts;
+      if (st >= C::kStages) {
+        st -= C::kStages;
+        ph ^= 1u;
+      }
     }
   } else if (warp >= C::kFirstEpiWarp) {
     // -------------------------------------------------- epilogue parts
@@ -704,12 +781,9 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     const int slot = part * C::kVox + row;
     int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
     float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
-    float* xmax = reinterpret_cast<float*>(smem + C::kOffX);           // [slot] part runmax
-    int* xcnt = reinterpret_cast<int*>(smem + C::kOffX) + C::kSlots;   // [slot] count, -1 ovf
-    double* xbs = reinterpret_cast<double*>(smem + C::kOffX + 8 * C::kSlots);  // part best
-    int* xbest = reinterpret_cast<int*>(smem + C::kOffX + 16 * C::kSlots);     // part best atom
     const uint32_t lane_off = uint32_t(q * 32) << 16;
     const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
+    const uint32_t t_lane = tbase + lane_off + uint32_t(part * C::kAccCols);  // this part's stage
 
     // ---- A for the first voxel tile
     if (part == 0 && my_vts > 0) {
@@ -721,6 +795,10 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     }
 
     uint32_t kk = uint32_t(part);  // this part's next tile
+    uint32_t ph = 0;               // phase of t_full[part]
+    int rel = part + C::kAcc;      // release barrier (kk + kAcc) % kStages
+    int ba = rot + part;           // atom tile (rot + kk) % nB
+    if (ba >= nB) ba -= nB;
     for (int it = 0; it < my_vts; ++it) {
       const int vt = int(blockIdx.x) + it * int(gridDim.x);
       const int64_t v = int64_t(vt) * C::kVox + row;
@@ -736,88 +814,57 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full + nbuf);
       }
+      if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(0, it);
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
       CandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0, false};
-      float runmax = -INFINITY, thr = active ? -INFINITY : INFINITY;
+      __half runmax = __ushort_as_half(0xFC00);
+      __half thr = __ushort_as_half(active ? 0xFC00 : 0x7C00);
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
-      // incremental tile bookkeeping (no per-tile div/mod): stage s = kk % kAcc with phase
-      // (kk / kAcc) & 1, release barrier (kk + kAcc) % kStages, atom tile (rot + b) % nB
-      int s = int(kk % C::kAcc);
-      uint32_t ph = (kk / C::kAcc) & 1;
-      int rel = int((kk + C::kAcc) % C::kStages);
-      int ba = rot + int(kk - uint32_t(it) * uint32_t(nB));
-      if (ba >= nB) ba -= nB;
       for (; kk < kend; kk += kParts) {
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-        mbar_wait_sleep(t_full + s, ph);
+        mbar_wait_sleep(t_full + part, ph);
         tc_fence_after();
         if (q == 0 && lane == 0) CBB_STAMP(2, kk);
-        float ra[32], rb[32];
+        uint32_t r[64];
         __syncwarp();
-        const uint32_t taddr = tbase + lane_off + uint32_t(s * C::kAccCols);
-        tmem_ld32(taddr, ra);
-        tmem_ld32(taddr + 32, rb);
+        tmem_ld32_pack16(t_lane, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32_pack16(t_lane + 64u, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
         tc_wait_ld();
         if (q == 0 && lane == 0) CBB_STAMP(3, kk);
-        // early release: stage s may be overwritten by tile kk + kAcc while we screen
+        // early release: the stage may be overwritten by tile kk + kAcc while we screen
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(b_full + rel);
-        const bool tail = (ba == nB - 1) && (int64_t(nB) * BN > d);
-        screen64(ra, rb, int64_t(ba) * BN, tail, d, win, runmax, thr, active, cl);
+        screen128(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
         if (q == 0 && lane == 0) CBB_STAMP(6, kk);
-        s += kParts;
-        if (s >= C::kAcc) {
-          s -= C::kAcc;
-          ph ^= 1u;
-        }
+        ph ^= 1u;
         rel += kParts;
         if (rel >= C::kStages) rel -= C::kStages;
         ba += kParts;
         if (ba >= nB) ba -= nB;
       }
-      // ---- finalize: every part rescores its own surviving groups, part 0 merges
-      xmax[slot] = runmax;
-      xcnt[slot] = cl.ovf ? -1 : cl.cnt;
-      named_bar_sync(1, C::kEpiWarps * 32);
-      float gmax = -INFINITY;
-      bool ovf = false;
-#pragma unroll
-      for (int p2 = 0; p2 < kParts; ++p2) {
-        gmax = fmaxf(gmax, xmax[p2 * C::kVox + row]);
-        ovf |= xcnt[p2 * C::kVox + row] < 0;
-      }
-      int64_t best = -1;
-      double bs = -INFINITY;
-      if (live && win >= 0.f && !ovf)
-        rescore_entries(zs, dv, v, cj_base + slot, cs_base + slot, C::kSlots, cl.cnt, gmax - win,
-                        32, best, bs);
-      xbs[slot] = bs;
-      xbest[slot] = int(best);
-      named_bar_sync(1, C::kEpiWarps * 32);
-      if (part == 0 && live) {
-        if (win < 0.f) {
-          write_winner(out, dv, v, 0, 0.0);
-        } else {
-          for (int p2 = 1; p2 < kParts; ++p2) {
-            const double b2 = xbs[p2 * C::kVox + row];
-            const int64_t j2 = xbest[p2 * C::kVox + row];
-            if (j2 >= 0 && (best < 0 || b2 > bs || (b2 == bs && j2 < best))) {
-              bs = b2;
-              best = j2;
+      // ---- hand-off (no inter-part barrier): this part's surviving chunk entries and its
+      // running max go to the global candidate buffer; rescore_kernel merges the parts and
+      // rescans the flagged groups in fp64
+      if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(1, it);
+      if (live) {
+        int k = 0;
+        if (!cl.ovf && win >= 0.f) {
+          const float thr_f = __half2float(runmax) - win;
+          for (int c = 0; c < cl.cnt; ++c) {
+            const float x = cl.cs[c * C::kSlots];
+            if (x >= thr_f) {
+              cand[(int64_t(part) * kCandCap + k) * n_pad + v] =
+                  make_int2(cl.cj[c * C::kSlots], __float_as_int(x));
+              ++k;
             }
           }
-          if (ovf || best < 0) {
-            const int sl2 = atomicAdd(ovf_count, 1);
-            ovf_list[sl2] = v;
-          } else {
-            write_winner(out, dv, v, best, bs);
-          }
         }
+        meta[int64_t(part) * n_pad + v] =
+            make_int2(cl.ovf ? -1 : k, __float_as_int(__half2float(runmax)));
       }
-      // the exchange slots of this tile are rewritten only after every part has streamed the
-      // whole next tile, which needs part 0's stage releases: no third barrier is required
+      if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(2, it);
     }
   }
   __syncthreads();
@@ -827,7 +874,65 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   }
 }
 
-// Debug: raw bf16 tcgen05 scores (A = voxel rows staged into TMEM, B = swizzled atom tile in
+// ============================================================== fp64 rescoring of tcgen05 candidates
+// One thread per voxel.  Merges the parts' running maxima (gmax), keeps the entries whose
+// approximate chunk max lies inside the final window gmax - win, rescans their flagged groups
+// exactly in fp64 from the caller's atoms and voxel, and writes the winner (lowest index on
+// exact ties, projection.py:62).  Zero voxels -> index 0 / gamma 0; overflowed candidate lists
+// and non-finite voxels -> exhaustive list.
+__global__ void __launch_bounds__(256) rescore_kernel(ZSource zs, DictView dv, int64_t n,
+                                                      int64_t n_pad,
+                                                      const float* __restrict__ win_tc,
+                                                      const int2* __restrict__ cand,
+                                                      const int2* __restrict__ meta, ProjOut out,
+                                                      int* ovf_count, int64_t* ovf_list) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const float win = win_tc[v];
+  if (win < 0.f) {
+    write_winner(out, dv, v, 0, 0.0);
+    return;
+  }
+  float gmax = -INFINITY;
+  bool ovf = !(win >= 0.f);
+  int cnt[kParts];
+#pragma unroll
+  for (int p = 0; p < kParts; ++p) {
+    const int2 m = meta[int64_t(p) * n_pad + v];
+    cnt[p] = m.x;
+    ovf |= m.x < 0;
+    gmax = fmaxf(gmax, __int_as_float(m.y));
+  }
+  int64_t best = -1;
+  double bs = -INFINITY;
+  if (!ovf) {
+    const float thr = gmax - win;
+#pragma unroll
+    for (int p = 0; p < kParts; ++p) {
+      for (int c = 0; c < cnt[p]; ++c) {
+        const int2 e = cand[(int64_t(p) * kCandCap + c) * n_pad + v];
+        if (__int_as_float(e.y) < thr) continue;
+        const int64_t j0 = int64_t(uint32_t(e.x) & ((1u << kChunkShift) - 1)) << 5;
+        uint32_t mask = uint32_t(e.x) >> kChunkShift;
+        while (mask) {
+          const int b = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
+          for (int i = lo; i < hi; ++i)
+            if (j0 + i < dv.d) rescore_one(zs, dv, v, j0 + i, best, bs);
+        }
+      }
+    }
+  }
+  if (ovf || best < 0) {
+    const int slot = atomicAdd(ovf_count, 1);
+    ovf_list[slot] = v;
+    return;
+  }
+  write_winner(out, dv, v, best, bs);
+}
+
+// Debug: raw fp16 tcgen05 scores (A = voxel rows staged into TMEM, B = swizzled atom tile in
 // SMEM) of voxel rows [128 a_tile, +128) x atoms [128 b_tile, +128) -- validates descriptors,
 // the swizzled atom tiles and the TMEM A-operand layout against a host emulation.
 template <int KP>
@@ -863,18 +968,22 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     const uint64_t bd = umma_desc_kmajor(smem_u32(smem), KP);
     for (int k = 0; k < KP / 16; ++k)
-      tc_mma_bf16_ts(tbase, tbase + a_col + k * 8, bd + uint64_t(2 * k),
-                     idesc_bf16_f32(128, 128), k > 0);
+      tc_mma_f16_ts(tbase, tbase + a_col + k * 8, bd + uint64_t(2 * k),
+                    idesc_f16_f16(128, 128), k > 0);
     tc_commit(bar + 1);
   }
   __syncwarp();
   mbar_wait(bar + 1, 0);
   tc_fence_after();
-  for (int c = 0; c < 4; ++c) {
-    float r[32];
-    tmem_ld32(tbase + (uint32_t(warp * 32) << 16) + c * 32, r);
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tmem_ld32_pack16(tbase + (uint32_t(warp * 32) << 16) + c * 64, r);
     tc_wait_ld();
-    for (int i = 0; i < 32; ++i) out[(warp * 32 + lane) * 128 + c * 32 + i] = r[i];
+    for (int i = 0; i < 32; ++i) {
+      const float2 f = __half22float2(as_h2(r[i]));
+      out[(warp * 32 + lane) * 128 + c * 64 + 2 * i] = f.x;
+      out[(warp * 32 + lane) * 128 + c * 64 + 2 * i + 1] = f.y;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -994,18 +1103,29 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   v.bounds = reinterpret_cast<float*>(base + ob);
   const int threads = 256;
   const int blocks = int((d + threads - 1) / threads);
-  prep_dict_kernel<<<blocks, threads, 0, st>>>(atoms, in128, d, s, v.s_pad, v.kpad,
+  prep_dict_kernel<<<blocks, threads, 0, st>>>(atoms, in128, d, s, v.s_pad,
                                                 const_cast<double2*>(v.atoms64),
                                                 const_cast<float*>(v.atoms32),
-                                                const_cast<uint8_t*>(v.atoms_tc),
                                                 const_cast<float*>(v.bounds));
   CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  if (2 * s < 64) {  // tensor-core operand tiles (+ sentinel column)
+    const int64_t d_pad = int64_t(v.n_btiles) * kTileRows;
+    prep_tc_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
+        v.atoms64, d, d_pad, s, v.kpad, const_cast<uint8_t*>(v.atoms_tc),
+        const_cast<float*>(v.bounds));
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+  }
   *view = v;
   return kOk;
 }
 
 // Workspace carve-up for one projection call.
 struct ProjWs {
+  int64_t n_pad;
+  int2* cand;      // [kParts][kCandCap][n_pad] tcgen05 chunk entries (entry, approx max)
+  int2* meta;      // [kParts][n_pad] (entry count or -1 on overflow, part running max)
   uint8_t* ztiles;
   float* win_tc;
   float* win32;
@@ -1028,7 +1148,10 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
     return base ? base + r : nullptr;
   };
   ProjWs w{};
-  w.ztiles = take(size_t(n_vt) * kVoxPad * kp * 2);
+  w.n_pad = n_vt * kVoxPad;
+  w.ztiles = take(size_t(n_vt) * kVoxPad * kp * 2);  // first: cbb_debug_tc_scores reads it
+  w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * kCandCap * sizeof(int2)));
+  w.meta = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * sizeof(int2)));
   w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.ovf_count = reinterpret_cast<int*>(take(16));
@@ -1064,8 +1187,8 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
-  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, zs, dv, out,
-                                                        w.ovf_count, w.ovf_list);
+  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, dv,
+                                                        w.n_pad, w.cand, w.meta);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
@@ -1135,7 +1258,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   if (nd_sum && !o.nd_v) o.nd_v = w.nd_v;
   // tcgen05 path: K = 2s <= 64; chunk entries pack (atom / 32) into 20 bits; every epilogue
   // part needs >= 2 atom tiles of 64 per voxel tile (d > 320; smaller dictionaries use FFMA)
-  const bool tc_ok = (2 * dv.s <= 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
+  const bool tc_ok = (2 * dv.s < 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
   if (algo == 0) algo = tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
   if (algo == 1 && !tc_ok) return kErrUnsupported;
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
@@ -1154,6 +1277,12 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
                          : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
     timing_mark(1, st);
+    if (algo == 1) {
+      rescore_kernel<<<int((n + 255) / 256), 256, 0, st>>>(zr, dv, n, w.n_pad, w.win_tc, w.cand,
+                                                           w.meta, o, w.ovf_count, w.ovf_list);
+      CBB_CUDA_TRY(cudaGetLastError());
+      count_launches(1);
+    }
     count_launches(3);  // prologue, screening kernel, exhaustive rescan
     {
       rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
@@ -1212,6 +1341,10 @@ int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile
 
 #ifdef CBB_TRACE
 int trace_dump(long long* host, int count) {
+  if (count < 0) {  // per-voxel-tile stamps (256 x 4)
+    CBB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_trace_vt, sizeof(long long) * 4 * 256));
+    return kOk;
+  }
   CBB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 8 * count));
   return kOk;
 }

@@ -6,7 +6,7 @@
 //   P_v   = g_v * D_j*               (projection.py:64)
 //
 // B200 design: a screening pass scores every (voxel, atom) pair in low
-// precision (bf16 tcgen05 MMA, or fp32 FFMA) and keeps, per voxel, every atom
+// precision (fp16 tcgen05 MMA with fp16 accumulation, or fp32 FFMA) and keeps, per voxel, every atom
 // whose approximate score lies inside a CERTIFIED window below the running
 // maximum (window = 2 * rigorous bound on |approx - exact|).  The surviving
 // candidates are rescored in fp64 from the caller's own atoms and voxels, so
@@ -28,12 +28,21 @@ struct DictView {
   int32_t n_btiles;    // ceil(d / 128)
   const double2* atoms64;      // d x s   complex128 (exact rescoring)
   const float* atoms32;        // d x 2*s_pad planar fp32 [re.., im..]
-  const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad bf16, swizzled tiles
-  const float* bounds;         // [0]=delta_bf16 [1]=dmax [2]=dbf_max [3]=delta32 [4]=d32max
+  const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad fp16 (atoms * scale), swizzled
+  const float* bounds;         // kB* slots below
 };
 
-// Bounds slots.
-enum { kBDeltaBf16 = 0, kBDmax = 1, kBDbfMax = 2, kBDelta32 = 3, kBD32Max = 4, kBCount = 8 };
+// Bounds slots (all rounded up).  The fp16 tiles hold d~ = fp16(scale_d * d) with scale_d a
+// power of two putting max||scale_d d|| in [0.5, 1).
+enum {
+  kBDeltaH = 0,    // max_j ||scale_d d_j - d~_j||
+  kBDmax = 1,      // max_j ||d_j||
+  kBDhMax = 2,     // max_j ||d~_j||
+  kBDelta32 = 3,   // max_j ||d_j - fp32(d_j)||
+  kBD32Max = 4,    // max_j ||fp32(d_j)||
+  kBScaleD = 5,    // scale_d
+  kBCount = 8
+};
 
 // Where the projection input Z comes from.
 struct ZSource {

@@ -9,8 +9,8 @@ host setup: they run in numpy exactly like the reference so the
 GPU path consumes the same basis.
 
 ``DeviceDictionary`` is the B200 form: fp64 atoms for exact rescoring, fp32
-planar atoms for FFMA screening, bf16 UMMA tiles for tcgen05 screening and the
-certified rounding bounds, built by one kernel (``cbb_dict_prepare``).  Any
+planar atoms for FFMA screening, power-of-two scaled fp16 UMMA tiles for tcgen05
+screening and the certified rounding bounds (``cbb_dict_prepare``).  Any
 object exposing ``.atoms`` or ``.atoms_compressed`` (the reference's duck
 typing, ``projection.py:26-29``) can be prepared.
 """
@@ -219,6 +219,14 @@ class DeviceDictionary:
         n = self.d * self.s * 16
         raw = self.storage[:n]
         return raw.view(torch.complex128).view(self.d, self.s)
+
+    BOUND_SLOTS = ("delta_h", "dmax", "dh_max", "delta32", "d32max", "scale_d")
+
+    def bounds(self) -> dict:
+        """Certified rounding bounds of the prepared copies (``cbb_project.cuh`` kB* slots)."""
+        off = int(self.view.bounds) - self.storage.data_ptr()
+        vals = self.storage[off:off + 32].view(torch.float32).cpu().tolist()
+        return dict(zip(self.BOUND_SLOTS, vals))
 
 
 _cache_lock = __import__("threading").Lock()

@@ -31,5 +31,15 @@ print("epi: screen (3->6)                  ", med(t[ks, 6] - t[ks, 3]))
 print("epi: loop overhead (6 -> next 5)    ", med(t[ks + 3, 5] - t[ks, 6]))
 print("epi: part period (2 -> next 2)      ", med(t[ks + 3, 2] - t[ks, 2]))
 print("commit -> t_full ready (1->2)       ", med(t[ks, 2] - t[ks, 1]))
-print("release(k-6) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 6, 3]))
+print("release(k-3) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 3, 3]))
 print("frac of part time waiting           ", med((t[ks, 2] - t[ks, 5]) / (t[ks + 3, 2] - t[ks, 2])))
+vt = np.zeros(256 * 4, dtype=np.int64)
+assert fn(vt.ctypes.data, -1) == 0
+vt = vt.reshape(256, 4).astype(np.float64)
+nv = int((vt[:, 0] > 0).sum())
+its = np.arange(1, nv - 1)
+print("voxel tiles traced                  ", nv)
+print("voxel tile: atom loop (0->1)        ", med(vt[its, 1] - vt[its, 0]))
+print("voxel tile: finalize (1->2)         ", med(vt[its, 2] - vt[its, 1]))
+print("voxel tile: total (0 -> next 0)     ", med(vt[its + 1, 0] - vt[its, 0]))
+print("voxel tile 0: loop / finalize       ", vt[0, 1] - vt[0, 0], vt[0, 2] - vt[0, 1])

@@ -11,15 +11,19 @@ __global__ void k2(float* out, int iters, float seed) {
   __half2 h[8];
   float a[8];
   for (int i = 0; i < 8; ++i) { a[i] = seed * (threadIdx.x + i); h[i] = __floats2half2_rn(a[i], a[i] + 1); }
-  __half2 hb = __floats2half2_rn(seed, seed * 2);
+  __half2 hb = __floats2half2_rn(seed, seed * 2), hc = __floats2half2_rn(seed * 3, seed);
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (MODE == 0) { a[i] = fmaxf(a[i], __uint_as_float(__float_as_uint(a[i]) ^ 1u)); h[i] = __floats2half2_rn(a[i], a[i]); }
       else if (MODE == 1) { h[i] = __hmax2(h[i], hb); }
+      else if (MODE == 3) { h[i] = __hmax2(__hmax2(h[i], hb), hc); }
+      else if (MODE == 4) { if (i & 1) h[i] = __hmax2(__hmax2(h[i], hb), hc); else h[i] = __hmax2(h[i], hb); }
+      else if (MODE == 5) { if (i & 1) h[i] = __hmax2(__hmax2(h[i], hb), hc); else a[i] = fmaxf(a[i], seed); }
       else { if (i & 1) h[i] = __hmax2(h[i], hb); else a[i] = fmaxf(a[i], seed); }
     }
     hb = __hadd2(hb, hb);
+    hc = __hadd2(hc, hb);
   }
   float s = 0; for (int i = 0; i < 8; ++i) s += __half2float(h[i].x) + __half2float(h[i].y);
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
@@ -71,14 +75,18 @@ int main() {
     printf("%s: %.3f ms  %.1f lane-ops/clk/SM (at %.0f MHz)\n", names[mode], ms,
            ops / (ms * 1e-3) / 148 / (clk * 1e3), clk / 1e3);
   }
-  const char* n2[3] = {"F2FP pack + FMNMX", "HMNMX2", "HMNMX2+FMNMX interleaved"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* n2[6] = {"F2FP pack + FMNMX", "HMNMX2", "HMNMX2+FMNMX interleaved",
+                       "VHMNMX (3-input half2)", "VHMNMX+HMNMX2 interleaved", "VHMNMX+FMNMX interleaved"};
+  for (int mode = 0; mode < 6; ++mode) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
       if (mode == 0) k2<0><<<148 * 8, 1024>>>(out, iters, 1.0f);
       if (mode == 1) k2<1><<<148 * 8, 1024>>>(out, iters, 1.0f);
       if (mode == 2) k2<2><<<148 * 8, 1024>>>(out, iters, 1.0f);
+      if (mode == 3) k2<3><<<148 * 8, 1024>>>(out, iters, 1.0f);
+      if (mode == 4) k2<4><<<148 * 8, 1024>>>(out, iters, 1.0f);
+      if (mode == 5) k2<5><<<148 * 8, 1024>>>(out, iters, 1.0f);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
     }
     float ms; cudaEventElapsedTime(&ms, e0, e1);

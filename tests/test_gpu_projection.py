@@ -47,17 +47,35 @@ def assert_parity(Z, atoms, res, gamma_rtol=1e-12, allow_ties=True):
     return diff.sum()
 
 
-def test_tc_debug_scores_match_bf16_emulation():
-    """Raw tcgen05 scores == fp64 dot of the bf16-rounded operands (descriptor / swizzle check)."""
+def _f16_mma_emulation(zh, ah, kp):
+    """fp16 tcgen05 accumulation model: each K=16 block's sum is added to the fp16 accumulator
+    with ONE round-to-nearest-even (scripts/probe_f16acc.cu); the hardware's internal sum is
+    exact up to a finite-width alignment (covered by the 2^-19 slack of the window)."""
+    acc = np.zeros((zh.shape[0], ah.shape[0]), dtype=np.float16)
+    peak = np.zeros(acc.shape)
+    for k0 in range(0, kp, 16):
+        part = zh[:, k0:k0 + 16].astype(np.float64) @ ah[:, k0:k0 + 16].astype(np.float64).T
+        acc = (acc.astype(np.float64) + part).astype(np.float16)
+        peak = np.maximum(peak, np.abs(acc.astype(np.float64)))
+    return acc.astype(np.float64), peak
+
+
+def test_tc_debug_scores_match_f16_emulation():
+    """Raw tcgen05 scores == bit-exact emulation of the fp16 MMA on the scaled fp16 operands
+    (descriptors, swizzled tiles, TMEM A layout, .pack::16b read-back, accumulation model)."""
     import ctypes
     p = _pkg()
     from paper_1810_01967_b200 import _lib
     from paper_1810_01967_b200.device import workspace
     rng = np.random.default_rng(5)
-    for s in (10, 20):
+    for s in (10, 16, 20):
+        kp = 32 if 2 * s < 32 else 64
         atoms = random_atoms(rng, 300, s)
         Z = rng.standard_normal((300, s)) + 1j * rng.standard_normal((300, s))
+        Z[:40] *= np.exp(rng.uniform(-30, 30, size=(40, 1)))   # wide dynamic range of voxels
         dd = p.device_dictionary(atoms)
+        sd = dd.bounds()["scale_d"]
+        assert sd == 2.0 ** -np.frexp(dd.bounds()["dmax"])[1]
         lib = _lib.load()
         zt = torch.from_numpy(Z).cuda()
         wsb = lib.cbb_project_workspace_bytes(300, s)
@@ -65,21 +83,34 @@ def test_tc_debug_scores_match_bf16_emulation():
         _lib.check(lib.cbb_project_prologue(zt.data_ptr(), 1, 300, ctypes.byref(dd.view),
                                             ws.data_ptr(), wsb, _lib.stream_ptr()), "prologue")
         out = torch.empty((128, 128), dtype=torch.float32, device="cuda")
+        sv = 2.0 ** (13 - np.frexp(np.linalg.norm(Z, axis=1))[1])
+        zr = np.zeros((384, kp))
+        zr[:300, :2 * s] = np.concatenate([Z.real, Z.imag], 1) * sv[:, None]
+        ar = np.zeros((384, kp))
+        ar[:300, :2 * s] = np.concatenate([atoms.real, atoms.imag], 1) * sd
+        zr[:300, kp - 1] = 1.0        # sentinel column: voxel rows 1,
+        ar[300:, kp - 1] = -65504.0   # zero-padded atom rows of the last tile -65504
+        zh, ah = zr.astype(np.float16), ar.astype(np.float16)
+        assert np.all(np.isfinite(zh)) and np.abs(zh).max() < 2.0 ** 13
         for at, bt in ((0, 0), (1, 2), (2, 1)):
             _lib.check(lib.cbb_debug_tc_scores(ws.data_ptr(), ctypes.byref(dd.view), at, bt,
                                                out.data_ptr(), _lib.stream_ptr()), "dbg")
             got = out.cpu().numpy().astype(np.float64)
-
-            def bf(x):
-                return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(
-                    torch.bfloat16).to(torch.float64).numpy()
-            zr = np.zeros((384, 2 * s))
-            zr[:300] = np.concatenate([Z.real, Z.imag], 1)
-            ar = np.zeros((384, 2 * s))
-            ar[:300] = np.concatenate([atoms.real, atoms.imag], 1)
-            exp = bf(zr[at * 128:(at + 1) * 128]) @ bf(ar[bt * 128:(bt + 1) * 128]).T
-            err = np.abs(got - exp).max()
-            assert err <= 1e-5 * max(1.0, np.abs(exp).max()), (s, at, bt, err)
+            exp, peak = _f16_mma_emulation(zh[at * 128:(at + 1) * 128],
+                                           ah[bt * 128:(bt + 1) * 128], kp)
+            # bit-exact except rare 1-ulp flips where the tensor core's internal (aligned,
+            # finite-width) K=16 sum is not exact under heavy cancellation
+            # (a flip in an intermediate accumulator propagates: compare with its ulp)
+            ulp = (kp // 16) * np.spacing(peak.astype(np.float16)).astype(np.float64)
+            flips = got != exp
+            assert flips.mean() < 1e-3, (s, at, bt, flips.sum())
+            assert np.all(np.abs(got - exp)[flips] <= ulp[flips]), (s, at, bt)
+            # and the accumulation error stays inside the certified acc term
+            z64 = zh[at * 128:(at + 1) * 128].astype(np.float64)
+            a64 = ah[bt * 128:(bt + 1) * 128].astype(np.float64)
+            bound = (kp // 16) * 2.0 ** -11 * 1.002 * np.outer(np.linalg.norm(z64, axis=1),
+                                                             np.linalg.norm(a64, axis=1))
+            assert np.all(np.abs(got - z64 @ a64.T) <= bound + 2.0 ** -24)
 
 
 @pytest.mark.parametrize("algo", ["tcgen05", "ffma", "exhaustive"])
@@ -89,6 +120,11 @@ def test_random_parity(algo, s):
     rng = np.random.default_rng(100 + s)
     atoms = random_atoms(rng, 1000, s)
     Z = rng.standard_normal((777, s)) + 1j * rng.standard_normal((777, s))
+    if algo == "tcgen05" and 2 * s >= 64:   # no spare sentinel column in K = 64
+        from paper_1810_01967_b200._lib import NativeError
+        with pytest.raises(NativeError, match="status 3"):
+            p.project_cone_exact(Z, atoms, algo=algo)
+        return
     res = p.project_cone_exact(Z, atoms, algo=algo)
     assert res.indices.dtype == np.int64 and res.gammas.dtype == np.float64
     assert res.projected.dtype == np.complex128 and res.cost == 777 * 1000
@@ -148,7 +184,7 @@ def test_cfg1_subsample_parity_and_complex64():
 
 
 def test_coherent_dictionary_overflow_path():
-    """MRF-like coherent atoms: many candidates inside the bf16 window -> exhaustive rescans."""
+    """MRF-like coherent atoms: many candidates inside the fp16 window -> exhaustive rescans."""
     p = _pkg()
     from paper_1810_01967_b200.workloads import cfg0_dictionary
     from paper_1810_01967_b200 import svd_compress
