@@ -3,8 +3,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one exact cone projection (``project_cone_exact``: tcgen05 bf16 screening,
-certified window, fp64 rescoring, write-back) of N = 2^20 voxels x D = 2^17 random unit
+One step = one exact cone projection (``project_cone_exact``: tcgen05 fp16 screening with
+fp16 accumulators, certified window, fp64 rescoring, write-back) of N = 2^20 voxels x D = 2^17 random unit
 atoms, s = 10, per GPU (voxel-sharded, weak scaling: every rank projects its own 2^20
 voxels against the replicated dictionary; there is no data-path collective).  Inputs are
 seeded synthetic data with the config's shapes and distributions (no dataset exists).
@@ -13,7 +13,8 @@ The JSON line carries: value = whole-job algorithmic MAC/s (N D 2s real MACs per
 step, inputs resident in HBM, L2 flushed between timed steps), e2e = the same metric
 through the public numpy API with pinned host buffers (H2D of Z and D2H of indices /
 gammas / projected inside the timed region), the roofline of the matched-filter kernel
-against the measured bf16 peak, the CPU baseline (the numpy port of the reference path on
+against the measured dense 16-bit tensor peak (MEASURED_PEAKS bf16; fp16 runs at the same
+tcgen05 rate), the CPU baseline (the numpy port of the reference path on
 this box's host cores, bounded sample), the cfg0 IPG iteration rate, clocks sampled during
 the timed region, and the number of kernels this library launched.
 
@@ -286,14 +287,16 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "precision": "bf16 tcgen05 screening inside a certified error window, fp64 exact "
-                     "rescoring of the surviving atoms (indices = fp64 argmax)",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "precision": "fp16 tcgen05 screening (fp16 operands, fp16 accumulators) inside a "
+                     "certified error window, fp64 exact rescoring of the surviving atoms "
+                     "(indices = fp64 argmax)",
         "data": "synthetic (seeded; no dataset is named by the benchmark)",
         "config": workload_config(world),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak,
-                     "peak_source": f"{peak_kind} bf16_tflops (burst; kernel timed alone)",
+                     "peak_source": f"{peak_kind} bf16_tflops (burst; kernel timed alone; "
+                                    "dense fp16 has the same tcgen05 rate)",
                      "kernel": "mf_tc_kernel<32>",
                      "algorithmic": "4 s flops per (voxel, atom) pair = 2s real MACs "
                                     f"(Re<z,d> only); {flops:.3e} flops per launch",

@@ -513,34 +513,42 @@ __device__ long long g_trace_vt[256 * 4];  // per voxel tile of CTA 0: loop star
 // One CTA per SM (persistent).  Per voxel tile (128 voxels):
 //   * the voxel operand A (fp16, K = KP) lives in TENSOR MEMORY (double buffered): part-0
 //     epilogue threads tcgen05.st their own voxel row into their TMEM lane one tile ahead;
-//   * warp 0 streams atom tiles (BN = 128 rows, pre-swizzled fp16) through a bulk-copy ring;
-//   * warps 1..kParts issue the MMAs: issuer i owns the CTA's atom tiles k = i (mod kParts),
-//     i.e. accumulator stage i (kAcc = kParts stages of 128 fp16 accumulator columns) and the
-//     B-ring stages st = i (mod kParts); per tile it waits ONE barrier, b_full[st], whose phase
-//     completes when the tile's bytes have landed AND the epilogue released the accumulator
-//     stage (the epilogue arrives on the b_full of the tile that will reuse its stage), then
-//     issues KP/16 MMAs (M=128, N=128, K=16, A from TMEM, B from SMEM) and commits;
+//   * warp 0 streams atom tiles (BN = 96 rows = 8-row aligned windows of the pre-swizzled
+//     fp16 128-row tiles) through a bulk-copy ring;
+//   * tile k accumulates in TMEM stage k % kAcc (kAcc = 5 stages x 96 fp16 accumulator
+//     columns + the 32-column A double buffer = all 512 columns); warps 1..kParts issue the
+//     MMAs: issuer i owns the CTA's atom tiles k = i (mod kParts) and the B-ring stages
+//     st = i (mod kParts); per tile it waits ONE barrier, b_full[st], whose phase completes
+//     when the tile's bytes have landed AND the epilogue released the accumulator stage (the
+//     epilogue arrives on the b_full of the tile that will reuse its stage), then issues KP/16
+//     MMAs (M=128, N=96, K=16, A from TMEM, B from SMEM) and commits;
 //   * epilogue part p (4 warps, one per TMEM lane quarter) consumes tiles k = p (mod kParts):
-//     it copies the 128 packed scores per lane into registers and releases the stage at once,
-//     so the screening runs while the tensor core refills it.
-// Every mbarrier has a single waiter role that consumes its phases in order (no parity
-// aliasing): b_full[st] -> issuer st % kParts (kStages % kParts == 0), t_full[s] -> part s,
-// b_empty -> producer, a_full -> issuers, a_empty -> part 0.  An epilogue arrival for tile
-// k + kAcc lands on b_full[(k + kAcc) % kStages] only after that barrier's previous phase
-// (tile k + kAcc - kStages) completed: the same issuer issued that tile before tile k.
+//     it copies the 96 packed scores per lane into registers and releases the stage at once.
+//     With 5 stages rotating over 3 parts a stage's refill (release -> issuer -> MMA -> commit)
+//     overlaps 5/3 screening iterations instead of one.
+// Barrier phases: b_full[st] -> issuer st % kParts (kStages % kParts == 0) consumes its phases
+// in order; an epilogue arrival for tile k + kAcc lands on b_full[(k + kAcc) % kStages] only
+// after that barrier's previous phase (tile k + kAcc - kStages) completed (issued before tile
+// k, whose stage is being released).  t_full[s] is waited by the parts of tiles s, s + kAcc,
+// ... in turn, so their completions go to t_full[k % kTBars] (kTBars = kAcc * kParts): each
+// of those barriers serves one stage and one part, which consumes its phases in order.
+// b_empty -> producer, a_full -> issuers, a_empty -> part 0.
 // Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
 constexpr int kParts = 3;
 
 template <int KP>
 struct TcCfg {
-  static constexpr int BN = 128;
+  static constexpr int kChunks = KP == 32 ? 5 : 4;           // 32-atom chunks per tile
+  static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 atoms per tile
   static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
-  static constexpr int kAcc = kParts;                        // one 128-column stage per part
+  static constexpr int kAcc = 3;                             // x BN accumulator columns
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
   static constexpr int kBBytes = BN * KP * 2;
-  static constexpr int kStagesRaw = (96 * 1024) / kBBytes > 24 ? 24 : (96 * 1024) / kBBytes;
+  static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
+  static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
+  static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
   static constexpr int kStages = (kStagesRaw / kParts) * kParts;
   static_assert(kStages >= 2 * kAcc, "B ring too shallow");
   static constexpr int kEpiWarps = 4 * kParts;
@@ -552,13 +560,16 @@ struct TcCfg {
   static constexpr int kOffCj = kOffB + kStages * kBBytes;
   static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
   static constexpr int kOffBar = kOffCs + kCandCap * kSlots * 4;
-  static constexpr int kNumBars = 4 + 2 * kStages + kAcc;
-  static_assert(kStages % kParts == 0 && kAcc % kParts == 0, "barrier ownership");
+  // completion barriers per tile slot k % kTBars (lcm(kAcc, kParts)): every barrier belongs to
+  // one stage AND one part, whose waits consume its phases in order (no parity aliasing)
+  static constexpr int kTBars = (kAcc % kParts == 0) ? kAcc : kAcc * kParts;
+  static constexpr int kNumBars = 4 + 2 * kStages + kTBars;
+  static_assert(kStages % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
   static constexpr uint32_t kIdesc = idesc_f16_f16(128, BN);
-  static constexpr int kMinTiles = kAcc;  // nB >= kAcc: every part owns >= 1 tile per voxel tile
+  static constexpr int kMinTiles = kParts;  // every part owns >= 1 tile per voxel tile
 };
 
 __device__ __forceinline__ uint8_t* align1024_smem(uint8_t* raw) {
@@ -578,9 +589,9 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // Screen approximate scores of one voxel (one thread): running max + certified window.
-// The fp16 accumulators arrive packed (register m = atoms 2m, 2m+1).  Fast path per 128
-// scores: four 3-input packed max chains (VHMNMX, 35 instructions, one chain per 32-atom
-// chunk) + one compare + a warp vote.
+// The fp16 accumulators arrive packed (register m = atoms 2m, 2m+1).  Fast path per
+// tile: one 3-input packed max chain per 32-atom chunk (VHMNMX, ~9 instructions per chunk)
+// + one compare + a warp vote.
 // Only when some lane's max reaches its threshold (rare after the first tiles) the chunks are
 // examined: a 32-atom chunk whose max enters the window is recorded (first atom, mask of
 // 6-atom groups inside the window, chunk max) -- no per-value inserts; the finalize rescans
@@ -611,20 +622,24 @@ __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64
   cl.insert(pack_chunk(jb, mask), __half2float(cm), thr_f);
 }
 
-__device__ __forceinline__ void screen128(const uint32_t (&r)[64], int64_t jb, float win,
-                                          __half& runmax, __half& thr, bool& active,
-                                          CandList& cl) {
-  // four independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
-  __half2 c[4];
+template <int NC>
+__device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_t jb, float win,
+                                            __half& runmax, __half& thr, bool& active,
+                                            CandList& cl) {
+  // NC independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
+  __half2 c[NC];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < NC; ++k) {
     const uint32_t* q = r + 16 * k;
     __half2 a = hmax3(as_h2(q[0]), as_h2(q[1]), as_h2(q[2]));
 #pragma unroll
     for (int i = 3; i < 15; i += 2) a = hmax3(a, as_h2(q[i]), as_h2(q[i + 1]));
     c[k] = __hmax2(a, as_h2(q[15]));
   }
-  const __half cm = hmax_halves(__hmax2(hmax3(c[0], c[1], c[2]), c[3]));
+  __half2 m = c[0];
+#pragma unroll
+  for (int k = 1; k < NC; ++k) m = __hmax2(m, c[k]);
+  const __half cm = hmax_halves(m);
   // warp-uniform test: the fast path carries no divergent branch / reconvergence
   if (__any_sync(0xffffffffu, __hge(cm, thr))) {
     if (__hge(cm, thr)) {
@@ -633,7 +648,7 @@ __device__ __forceinline__ void screen128(const uint32_t (&r)[64], int64_t jb, f
         thr = __float2half_rd(__half2float(runmax) - win);
         const float thr_f = __half2float(thr);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < NC; ++k) {
           const __half ck = hmax_halves(c[k]);
           if (__hge(ck, thr) && !cl.ovf) record_chunk(r + 16 * k, ck, jb + 32 * k, thr, thr_f, cl);
         }
@@ -696,7 +711,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       mbar_init(a_full + i, 4);         // the 4 part-0 warps stage A
       mbar_init(a_empty + i, kParts);   // each issuer commits after its last tile of a voxel tile
     }
-    for (int i = 0; i < C::kAcc; ++i) mbar_init(t_full + i, 1);
+    for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full + i, 1);
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(b_full + i, 1 + 4);     // producer (with tx) + the 4 warps releasing the stage
       mbar_init(b_empty + i, 1);
@@ -738,7 +753,8 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
     const int me = warp - 1;
     const uint32_t b_base = smem_u32(smem + C::kOffB);
-    const uint32_t d_tm = tbase + uint32_t(me * C::kAccCols);  // stage me (kAcc == kParts)
+    int sacc = me;  // accumulator stage kk % kAcc
+    int tb = me;    // completion barrier kk % kTBars
     int itk = -1;
     uint32_t vt_end = 0;  // first tile index of the next voxel tile
     int st = me;
@@ -756,17 +772,22 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       if (elect_one()) {
         const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
         const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kACols);
+        const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq)
           tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * kq), C::kIdesc,
                         kq > 0 ? 1u : 0u);
         tc_commit(b_empty + st);
-        tc_commit(t_full + me);
+        tc_commit(t_full + tb);
         // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
         if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
         CBB_STAMP(1, kk);
       }
       __syncwarp();
+      sacc += kParts;
+      if (sacc >= C::kAcc) sacc -= C::kAcc;
+      tb += kParts;
+      if (tb >= C::kTBars) tb -= C::kTBars;
       st += kParts;
       if (st >= C::kStages) {
         st -= C::kStages;
@@ -783,7 +804,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
     const uint32_t lane_off = uint32_t(q * 32) << 16;
     const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
-    const uint32_t t_lane = tbase + lane_off + uint32_t(part * C::kAccCols);  // this part's stage
+    const uint32_t t_lane = tbase + lane_off;
 
     // ---- A for the first voxel tile
     if (part == 0 && my_vts > 0) {
@@ -795,7 +816,9 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     }
 
     uint32_t kk = uint32_t(part);  // this part's next tile
-    uint32_t ph = 0;               // phase of t_full[part]
+    int sacc = part;               // its accumulator stage kk % kAcc
+    int tb = part;                 // its completion barrier kk % kTBars, phase (kk / kTBars) & 1
+    uint32_t ph = 0;
     int rel = part + C::kAcc;      // release barrier (kk + kAcc) % kStages
     int ba = rot + part;           // atom tile (rot + kk) % nB
     if (ba >= nB) ba -= nB;
@@ -823,22 +846,33 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
       for (; kk < kend; kk += kParts) {
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-        mbar_wait_sleep(t_full + part, ph);
+        mbar_wait_sleep(t_full + tb, ph);
         tc_fence_after();
         if (q == 0 && lane == 0) CBB_STAMP(2, kk);
-        uint32_t r[64];
+        uint32_t r[16 * C::kChunks];
         __syncwarp();
-        tmem_ld32_pack16(t_lane, *reinterpret_cast<uint32_t(*)[32]>(r));
-        tmem_ld32_pack16(t_lane + 64u, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
+#pragma unroll
+        for (int c = 0; c + 2 <= C::kChunks; c += 2)
+          tmem_ld32_pack16(ta + uint32_t(32 * c), *reinterpret_cast<uint32_t(*)[32]>(r + 16 * c));
+        if (C::kChunks & 1)
+          tmem_ld16_pack16(ta + uint32_t(32 * (C::kChunks - 1)),
+                           *reinterpret_cast<uint32_t(*)[16]>(r + 16 * (C::kChunks - 1)));
         tc_wait_ld();
         if (q == 0 && lane == 0) CBB_STAMP(3, kk);
         // early release: the stage may be overwritten by tile kk + kAcc while we screen
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(b_full + rel);
-        screen128(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
+        screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
         if (q == 0 && lane == 0) CBB_STAMP(6, kk);
-        ph ^= 1u;
+        sacc += kParts;
+        if (sacc >= C::kAcc) sacc -= C::kAcc;
+        tb += kParts;
+        if (tb >= C::kTBars) {
+          tb -= C::kTBars;
+          ph ^= 1u;
+        }
         rel += kParts;
         if (rel >= C::kStages) rel -= C::kStages;
         ba += kParts;
@@ -1075,7 +1109,9 @@ size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc,
   };
   size_t a = take(size_t(d) * s * 16);
   size_t b = take(size_t(d) * 2 * sp * 4);
-  size_t c = take(size_t(nbt) * kTileRows * kp * 2);
+  // + two extra 128-row sentinel tiles: the screening reads BN-row (BN <= 256) windows that
+  // may run past the last 128-row tile
+  size_t c = take(size_t(nbt + 2) * kTileRows * kp * 2);
   size_t e = take(kBCount * sizeof(float));
   if (off64) *off64 = a;
   if (off32) *off32 = b;
@@ -1110,7 +1146,7 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   CBB_CUDA_TRY(cudaGetLastError());
   count_launches(1);
   if (2 * s < 64) {  // tensor-core operand tiles (+ sentinel column)
-    const int64_t d_pad = int64_t(v.n_btiles) * kTileRows;
+    const int64_t d_pad = int64_t(v.n_btiles + 2) * kTileRows;
     prep_tc_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
         v.atoms64, d, d_pad, s, v.kpad, const_cast<uint8_t*>(v.atoms_tc),
         const_cast<float*>(v.bounds));
