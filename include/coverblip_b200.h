@@ -116,6 +116,10 @@ typedef struct cbb_op cbb_op;
  * flat C-order index per sample).  flags bit 0: identity_transform hook (no DFT). */
 int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const int32_t* pattern,
                   int32_t flags, cbb_op** out);
+/* Coil sensitivity maps S (forward_model.py:82-113,132-167): c x n complex64 device array
+ * (caller-owned, must outlive the operator; NULL with c = 1 = all ones).  Measurements become
+ * (L, c*m) frame-major: column ci*m + i of frame t = coil ci, sample Omega_t(i). */
+int cbb_op_set_coils(cbb_op* op, int32_t c, const void* coil_maps);
 int cbb_op_destroy(cbb_op* op);
 size_t cbb_op_workspace_bytes(const cbb_op* op);
 /* Y = A X.  X: n x L complex64 voxel-major (reference layout); Y: L x m complex64

@@ -42,6 +42,7 @@ int scaled_rows(const DictView& dv, int64_t offset, const int64_t* idx, const do
 struct Op;
 int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int flags, Op** out);
 int op_destroy(Op* op);
+int op_set_coils(Op* op, int c, const float2* coils);
 size_t op_ws_bytes(const Op* op);
 int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st);
 int op_adjoint(Op* op, const float2* Y, float2* X, void* ws, cudaStream_t st);
@@ -236,6 +237,16 @@ int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const
   if (rc) return rc;
   *out = new cbb_op{impl};
   return kOk;
+}
+
+int cbb_op_set_coils(cbb_op* op, int32_t c, const void* coil_maps) {
+  if (!op) {
+    set_last_error("cbb_op_set_coils: null operator");
+    return kErrArgument;
+  }
+  int rc = op_set_coils(op->impl, c, static_cast<const float2*>(coil_maps));
+  if (rc) set_last_error("cbb_op_set_coils: need c >= 1 and a c x n map array for c > 1");
+  return rc;
 }
 
 int cbb_op_destroy(cbb_op* op) {

@@ -1,17 +1,33 @@
-// Cartesian acquisition operator A = P_Omega F (unitary DFT per frame) on B200,
-// plus the SVD-subspace maps and the fused reductions that drive the IPG step rule.
+// Cartesian acquisition operator A = P_Omega F S_c (unitary DFT per frame, c coil maps) on
+// B200, plus the SVD-subspace maps and the fused reductions that drive the IPG step rule.
 //
-// Reference: coverblip/forward_model.py:123-167 (apply/adjoint, cartesian_dft, c = 1),
+// Reference: coverblip/forward_model.py:123-167 (apply/adjoint, cartesian_dft),
 //            coverblip/dictionary.py:116-122 (compress = rows @ V, decompress = rows @ V^H),
 //            coverblip/solver.py:130,135,180-190 (squared norms, residual, weighted residual).
 //
 // Internal layout: frame-major.  A frame stack is (L, n) complex64 with n = prod(dims) in C
 // order (v = row*w + col, forward_model.py:138), so cuFFT runs one batched C2C over L
-// contiguous frames; measurements are (L, m) complex64 (frame t, sample i -> Omega_t(i)).
+// contiguous frames; measurements are (L, c*m) complex64 (frame t, coil ci, sample i ->
+// column ci*m + i, k-space index Omega_t(i); the reference's (c*m, L) transposed).
 // The unitary 1/sqrt(n) is folded into the gather / compress kernels.
+//
+// Compressed operator ("s-channel"): A(Xc V^H) and (A^H R) V never materialise
+// the (L, n) frame stack.  By linearity, FFT(sum_k Xc[:,k] conj(V[t,k])) = sum_k FFT(Xc[:,k])
+// conj(V[t,k]), so the forward map FFTs the c*s channel images S_ci Xc[:,k] (c*s transforms
+// instead of c*L) and the gather forms y[t, ci*m+i] = sum_k K[ci,k][Omega_t(i)] conj(V[t,k]).
+// The adjoint builds each channel's k-space K[ci,k][w] = sum_{(t,i): Omega_t(i)=w} R[t,ci*m+i]
+// V[t,k] deterministically from a CSR of the (fixed) pattern, inverse-FFTs c*s channels and
+// combines G[v,k] = sum_ci conj(S_ci[v]) IFFT(K[ci,k])[v].  Same result as decompress -> per-
+// frame FFT -> gather (compress) up to fp32 summation order.
 #include "cbb_common.cuh"
 
 #include <cufft.h>
+#include <thrust/binary_search.h>
+#include <thrust/execution_policy.h>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/sequence.h>
+#include <thrust/sort.h>
+
 #include <cmath>
 #include <new>
 
@@ -41,102 +57,14 @@ __global__ void __launch_bounds__(256) finish_sum(const double* __restrict__ par
   if (threadIdx.x == 0) *out = r;
 }
 
-// ---------------------------------------------------------------- subspace maps
-// F[t][v] = sum_k Xc[v][k] * conj(V[t][k])    (decompress, dictionary.py:122)
-__global__ void __launch_bounds__(256) decompress_frames_kernel(const float2* __restrict__ Xc,
-                                                                const float2* __restrict__ V,
-                                                                int s, int64_t n, int L,
-                                                                int t_per_block,
-                                                                float2* __restrict__ F) {
-  extern __shared__ float2 sV[];  // t_per_block x s
-  const int t0 = blockIdx.y * t_per_block;
-  const int tn = min(t_per_block, L - t0);
-  for (int i = threadIdx.x; i < tn * s; i += blockDim.x) sV[i] = V[size_t(t0) * s + i];
-  __syncthreads();
-  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= n) return;
-  float2 x[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) x[k] = (k < s) ? Xc[v * s + k] : make_float2(0.f, 0.f);
-  for (int tt = 0; tt < tn; ++tt) {
-    float re = 0.f, im = 0.f;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k < s) {
-        const float2 b = sV[tt * s + k];
-        // x * conj(b)
-        re = fmaf(x[k].x, b.x, fmaf(x[k].y, b.y, re));
-        im = fmaf(x[k].y, b.x, fmaf(-x[k].x, b.y, im));
-      }
-    }
-    F[size_t(t0 + tt) * n + v] = make_float2(re, im);
-  }
-}
-
-// Gc[v][k] = scale * sum_t F[t][v] * V[t][k]    (compress, dictionary.py:118)
-__global__ void __launch_bounds__(256) compress_frames_kernel(const float2* __restrict__ F,
-                                                              const float2* __restrict__ V,
-                                                              int s, int64_t n, int L,
-                                                              float scale,
-                                                              float2* __restrict__ Gc) {
-  constexpr int TB = 64;
-  __shared__ float2 sV[TB * 32];
-  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  float2 acc[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) acc[k] = make_float2(0.f, 0.f);
-  for (int t0 = 0; t0 < L; t0 += TB) {
-    const int tn = min(TB, L - t0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < tn * s; i += blockDim.x) sV[i] = V[size_t(t0) * s + i];
-    __syncthreads();
-    if (v < n) {
-      for (int tt = 0; tt < tn; ++tt) {
-        const float2 f = F[size_t(t0 + tt) * n + v];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          if (k < s) {
-            const float2 b = sV[tt * s + k];
-            acc[k].x = fmaf(f.x, b.x, fmaf(-f.y, b.y, acc[k].x));
-            acc[k].y = fmaf(f.x, b.y, fmaf(f.y, b.x, acc[k].y));
-          }
-        }
-      }
-    }
-  }
-  if (v < n) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      if (k < s) Gc[v * s + k] = make_float2(acc[k].x * scale, acc[k].y * scale);
-  }
-}
-
-// Voxel-major (n, L) <-> frame-major (L, n) transposes with scaling.
-__global__ void transpose_kernel(const float2* __restrict__ in, int64_t rows, int64_t cols,
-                                 float scale, float2* __restrict__ out) {
-  __shared__ float2 tile[32][33];
-  const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int64_t r = r0 + i, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += 8) {
-    const int64_t c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) {
-      float2 x = tile[threadIdx.x][i];
-      out[c * rows + r] = make_float2(x.x * scale, x.y * scale);
-    }
-  }
-}
-
 // ---------------------------------------------------------------- sampling
 // mode 0: Y[t][i] = scale * F[t][Omega_t(i)]
 // mode 1: partial ||scale * F[Omega]||^2 only (apply_diff denominator, solver.py:135)
 // mode 2: R[t][i] = scale * F[t][Omega] - Ymeas[t][i] (+ partial of w*|R|^2), R stored as w*R
 __global__ void __launch_bounds__(256) gather_kernel(const float2* __restrict__ F,
                                                      const int* __restrict__ pat, int64_t n,
-                                                     int L, int m, float scale, int mode,
+                                                     int L, int m, int64_t ystride, int yoff,
+                                                     float scale, int mode,
                                                      const float2* __restrict__ Ymeas,
                                                      const float* __restrict__ w,
                                                      float2* __restrict__ Y,
@@ -147,8 +75,88 @@ __global__ void __launch_bounds__(256) gather_kernel(const float2* __restrict__ 
   for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * 256) {
     const int64_t t = e / m;
+    const int64_t ye = t * ystride + yoff + (e - t * m);  // column ci*m + i of frame t
     const float2 f = F[t * n + pat[e]];
     float2 y = make_float2(f.x * scale, f.y * scale);
+    if (mode == 2) {
+      const float2 ym = Ymeas[ye];
+      y.x -= ym.x;
+      y.y -= ym.y;
+      const float ww = w ? w[ye] : 1.f;
+      acc += double(ww) * (double(y.x) * y.x + double(y.y) * y.y);
+      Y[ye] = make_float2(ww * y.x, ww * y.y);
+    } else {
+      if (mode == 0) Y[ye] = y;
+      acc += double(y.x) * y.x + double(y.y) * y.y;
+    }
+  }
+  if (partial) {
+    double r = block_sum_256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+  }
+}
+
+// K[t][Omega_t(i)] = R[t][i]   (put_along_axis zero-fill, forward_model.py:160-162); K zeroed first
+__global__ void __launch_bounds__(256) scatter_kernel(const float2* __restrict__ R,
+                                                      const int* __restrict__ pat, int64_t n,
+                                                      int L, int m, int64_t rstride, int roff,
+                                                      float2* __restrict__ K) {
+  const int64_t total = int64_t(L) * m;
+  for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * 256) {
+    const int64_t t = e / m;
+    K[t * n + pat[e]] = R[t * rstride + roff + (e - t * m)];
+  }
+}
+
+// ---------------------------------------------------------------- s-channel compressed operator
+// C[(ci*s + k)*n + v] = S_ci[v] * Xc[v*s + k]   (coils == nullptr -> S = 1)
+__global__ void __launch_bounds__(256) channels_kernel(const float2* __restrict__ Xc,
+                                                       const float2* __restrict__ coils, int c,
+                                                       int s, int64_t n,
+                                                       float2* __restrict__ C) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  for (int ci = 0; ci < c; ++ci) {
+    const float2 sc = coils ? coils[int64_t(ci) * n + v] : make_float2(1.f, 0.f);
+    for (int k = 0; k < s; ++k) {
+      const float2 x = Xc[v * s + k];
+      C[(int64_t(ci) * s + k) * n + v] =
+          make_float2(sc.x * x.x - sc.y * x.y, sc.x * x.y + sc.y * x.x);
+    }
+  }
+}
+
+// y[t][ci*m + i] = scale * sum_k K[(ci*s + k)*n + Omega_t(i)] * conj(V[t*s + k]);
+// modes as gather_kernel (0 write, 1 norm only, 2 weighted residual y - Ymeas).
+__global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict__ K,
+                                                       const int* __restrict__ pat, int64_t n,
+                                                       int L, int m, int c, int s,
+                                                       const float2* __restrict__ V, float scale,
+                                                       int mode,
+                                                       const float2* __restrict__ Ymeas,
+                                                       const float* __restrict__ w,
+                                                       float2* __restrict__ Y,
+                                                       double* __restrict__ partial) {
+  __shared__ double sh[256];
+  const int64_t cm = int64_t(c) * m;
+  const int64_t total = int64_t(L) * cm;
+  double acc = 0.0;
+  for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * 256) {
+    const int64_t t = e / cm;
+    const int r = int(e - t * cm);
+    const int ci = r / m, i = r - ci * m;
+    const int64_t wloc = pat[t * m + i];
+    const float2* kb = K + int64_t(ci) * s * n + wloc;
+    const float2* vt = V + t * s;
+    float yr = 0.f, yi = 0.f;
+    for (int k = 0; k < s; ++k) {
+      const float2 a = kb[int64_t(k) * n], b = vt[k];
+      yr = fmaf(a.x, b.x, fmaf(a.y, b.y, yr));   // a * conj(b)
+      yi = fmaf(a.y, b.x, fmaf(-a.x, b.y, yi));
+    }
+    float2 y = make_float2(yr * scale, yi * scale);
     if (mode == 2) {
       const float2 ym = Ymeas[e];
       y.x -= ym.x;
@@ -167,15 +175,94 @@ __global__ void __launch_bounds__(256) gather_kernel(const float2* __restrict__ 
   }
 }
 
-// K[t][Omega_t(i)] = R[t][i]   (put_along_axis zero-fill, forward_model.py:160-162); K zeroed first
-__global__ void __launch_bounds__(256) scatter_kernel(const float2* __restrict__ R,
-                                                      const int* __restrict__ pat, int64_t n,
-                                                      int L, int m, float2* __restrict__ K) {
-  const int64_t total = int64_t(L) * m;
-  for (int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * 256) {
-    const int64_t t = e / m;
-    K[t * n + pat[e]] = R[e];
+// K[(ci*s + k)*n + w] = sum over the pattern entries e = t*m + i with Omega_t(i) = w (CSR,
+// ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per k-space location; unsampled
+// locations get 0 (the zero-fill of forward_model.py:160-162).
+template <int SMAX>
+__global__ void __launch_bounds__(128) kspace_s_kernel(const float2* __restrict__ R,
+                                                       const int* __restrict__ csr_off,
+                                                       const int64_t* __restrict__ csr_e,
+                                                       int64_t n, int m, int c, int s,
+                                                       const float2* __restrict__ V,
+                                                       float2* __restrict__ K) {
+  const int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (wloc >= n) return;
+  const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
+  const int64_t cm = int64_t(c) * m;
+  for (int ci = 0; ci < c; ++ci) {
+    float2 acc[SMAX];
+#pragma unroll
+    for (int k = 0; k < SMAX; ++k) acc[k] = make_float2(0.f, 0.f);
+    for (int j = b; j < e_end; ++j) {
+      const int64_t e = csr_e[j];
+      const int64_t t = e / m, i = e - t * m;
+      const float2 r = R[t * cm + int64_t(ci) * m + i];
+      const float2* vt = V + t * s;
+#pragma unroll
+      for (int k = 0; k < SMAX; ++k) {
+        if (k < s) {
+          const float2 v = vt[k];
+          acc[k].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[k].x));
+          acc[k].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[k].y));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SMAX; ++k)
+      if (k < s) K[(int64_t(ci) * s + k) * n + wloc] = acc[k];
+  }
+}
+
+// G[v*s + k] = scale * sum_ci conj(S_ci[v]) * K[(ci*s + k)*n + v]
+__global__ void __launch_bounds__(256) combine_s_kernel(const float2* __restrict__ K,
+                                                        const float2* __restrict__ coils, int c,
+                                                        int s, int64_t n, float scale,
+                                                        float2* __restrict__ G) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  for (int k = 0; k < s; ++k) {
+    float gr = 0.f, gi = 0.f;
+    for (int ci = 0; ci < c; ++ci) {
+      const float2 a = K[(int64_t(ci) * s + k) * n + v];
+      const float2 sc = coils ? coils[int64_t(ci) * n + v] : make_float2(1.f, 0.f);
+      gr += sc.x * a.x + sc.y * a.y;   // conj(sc) * a
+      gi += sc.x * a.y - sc.y * a.x;
+    }
+    G[v * s + k] = make_float2(gr * scale, gi * scale);
+  }
+}
+
+// Coil-weighted transposes of the uncompressed path:
+//   fwd: F[t][v] = S[v] * X[v][t];   adj: X[v][t] (+)= scale * conj(S[v]) * F[t][v]
+__global__ void coil_transpose_kernel(const float2* __restrict__ in, int64_t rows, int64_t cols,
+                                      const float2* __restrict__ coil, int coil_on_rows,
+                                      int conj_coil, float scale, int accumulate,
+                                      float2* __restrict__ out) {
+  __shared__ float2 tile[32][33];
+  const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      float2 x = tile[threadIdx.x][i];
+      if (coil) {
+        float2 sc = coil[coil_on_rows ? r : c];
+        if (conj_coil) sc.y = -sc.y;
+        x = make_float2(sc.x * x.x - sc.y * x.y, sc.x * x.y + sc.y * x.x);
+      }
+      x.x *= scale;
+      x.y *= scale;
+      if (accumulate) {
+        const float2 o = out[c * rows + r];
+        x.x += o.x;
+        x.y += o.y;
+      }
+      out[c * rows + r] = x;
+    }
   }
 }
 
@@ -241,10 +328,16 @@ struct Op {
   int dims[3];
   int64_t n;
   int L, m;
+  int c;                 // coils (measurement columns per frame: c * m)
+  const float2* coils;   // c x n device coil maps (caller-owned), nullptr = all ones
   const int* pattern;
-  cufftHandle plan;
-  float scale;     // 1/sqrt(n) (1 for the identity hook)
-  bool identity;   // forward_model.py:95,137,163 identity_transform test hook: skip the DFT
+  cufftHandle plan;      // batch L (uncompressed frame stacks)
+  int chan_batch[4];     // cached plans for batches of c*s channel images
+  cufftHandle chan_plan[4];
+  int* csr_off;          // n + 1 offsets into csr_e (s-channel adjoint)
+  int64_t* csr_e;        // pattern entries t*m + i sorted by k-space location (stable)
+  float scale;           // 1/sqrt(n) (1 for the identity hook)
+  bool identity;         // forward_model.py:95,137,163 identity_transform test hook: skip the DFT
 };
 
 static int grid_for(int64_t work, int per_block = 256) {
@@ -253,15 +346,53 @@ static int grid_for(int64_t work, int per_block = 256) {
   return int(g > 0 ? g : 1);
 }
 
+// workspace: max(frame stack L*n, c*32 channel images) + per-coil reduction partials
+static size_t ws_main_bytes(const Op* op) {
+  const size_t frames = size_t(op->L) * op->n * sizeof(float2);
+  const size_t chans = size_t(op->c) * 32 * op->n * sizeof(float2);
+  return ((frames > chans ? frames : chans) + 255) & ~size_t(255);
+}
 size_t op_ws_bytes(const Op* op) {
-  const size_t frames = (size_t(op->L) * op->n * sizeof(float2) + 255) & ~size_t(255);
-  return frames + kRedBlocks * sizeof(double) + 256;
+  return ws_main_bytes(op) + size_t(op->c) * kRedBlocks * sizeof(double) + 256;
 }
 static float2* ws_frames(void* ws) { return static_cast<float2*>(ws); }
 static double* ws_partial(const Op* op, void* ws) {
-  const size_t frames = (size_t(op->L) * op->n * sizeof(float2) + 255) & ~size_t(255);
-  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + frames);
+  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + ws_main_bytes(op));
 }
+
+static int make_plan(const Op* op, int batch, cufftHandle* plan) {
+  int nd[3] = {op->dims[0], op->dims[1], op->ndim == 3 ? op->dims[2] : 1};
+  if (cufftPlanMany(plan, op->ndim, nd, nullptr, 1, int(op->n), nullptr, 1, int(op->n),
+                    CUFFT_C2C, batch) != CUFFT_SUCCESS) {
+    set_last_error("cufftPlanMany failed");
+    return kErrCufft;
+  }
+  return kOk;
+}
+
+// CSR of the pattern by k-space location: stable sort of the L*m flat entries by Omega value.
+static int build_csr(Op* op) {
+  const int64_t total = int64_t(op->L) * op->m;
+  int* keys = nullptr;
+  CBB_CUDA_TRY(cudaMalloc(&op->csr_off, sizeof(int) * size_t(op->n + 1)));
+  CBB_CUDA_TRY(cudaMalloc(&op->csr_e, sizeof(int64_t) * size_t(total)));
+  CBB_CUDA_TRY(cudaMalloc(&keys, sizeof(int) * size_t(total)));
+  CBB_CUDA_TRY(cudaMemcpy(keys, op->pattern, sizeof(int) * size_t(total),
+                          cudaMemcpyDeviceToDevice));
+  thrust::sequence(thrust::device, op->csr_e, op->csr_e + total);
+  thrust::stable_sort_by_key(thrust::device, keys, keys + total, op->csr_e);
+  thrust::lower_bound(thrust::device, keys, keys + total, thrust::counting_iterator<int>(0),
+                      thrust::counting_iterator<int>(int(op->n) + 1), op->csr_off);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(keys);
+  if (e != cudaSuccess) {
+    set_last_error(cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+int op_destroy(Op* op);
 
 int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int flags, Op** out) {
   if ((ndim != 2 && ndim != 3) || L <= 0 || m <= 0) return kErrArgument;
@@ -276,41 +407,72 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int f
   }
   op->L = L;
   op->m = m;
+  op->c = 1;
   op->pattern = pattern;
   op->identity = (flags & 1) != 0;
   op->scale = op->identity ? 1.f : float(1.0 / std::sqrt(double(op->n)));
-  if (op->identity) {
-    op->plan = 0;
-    *out = op;
-    return kOk;
+  if (!op->identity) {
+    if (int rc = make_plan(op, L, &op->plan)) {
+      delete op;
+      return rc;
+    }
   }
-  int nd[3] = {dims[0], dims[1], ndim == 3 ? dims[2] : 1};
-  if (cufftPlanMany(&op->plan, ndim, nd, nullptr, 1, int(op->n), nullptr, 1, int(op->n), CUFFT_C2C,
-                    L) != CUFFT_SUCCESS) {
-    delete op;
-    set_last_error("cufftPlanMany failed");
-    return kErrCufft;
+  if (int rc = build_csr(op)) {
+    op_destroy(op);
+    return rc;
   }
   *out = op;
   return kOk;
 }
 
+int op_set_coils(Op* op, int c, const float2* coils) {
+  if (!op || c < 1 || (c > 1 && !coils)) return kErrArgument;
+  op->c = c;
+  op->coils = coils;
+  return kOk;
+}
+
 int op_destroy(Op* op) {
   if (!op) return kOk;
-  if (!op->identity) cufftDestroy(op->plan);
+  if (!op->identity) {
+    if (op->plan) cufftDestroy(op->plan);
+    for (int i = 0; i < 4; ++i)
+      if (op->chan_batch[i]) cufftDestroy(op->chan_plan[i]);
+  }
+  if (op->csr_off) cudaFree(op->csr_off);
+  if (op->csr_e) cudaFree(op->csr_e);
   delete op;
   return kOk;
 }
 
-static int fft(Op* op, float2* F, int dir, cudaStream_t st) {
-  if (op->identity) return kOk;
-  if (cufftSetStream(op->plan, st) != CUFFT_SUCCESS) return kErrCufft;
-  if (cufftExecC2C(op->plan, reinterpret_cast<cufftComplex*>(F), reinterpret_cast<cufftComplex*>(F),
+static int exec_fft(cufftHandle plan, float2* F, int dir, cudaStream_t st) {
+  if (cufftSetStream(plan, st) != CUFFT_SUCCESS) return kErrCufft;
+  if (cufftExecC2C(plan, reinterpret_cast<cufftComplex*>(F), reinterpret_cast<cufftComplex*>(F),
                    dir) != CUFFT_SUCCESS) {
     set_last_error("cufftExecC2C failed");
     return kErrCufft;
   }
   return kOk;
+}
+
+static int fft(Op* op, float2* F, int dir, cudaStream_t st) {
+  if (op->identity) return kOk;
+  return exec_fft(op->plan, F, dir, st);
+}
+
+// batched FFT of `batch` channel images (plans cached per batch size)
+static int fft_channels(Op* op, float2* C, int batch, int dir, cudaStream_t st) {
+  if (op->identity) return kOk;
+  for (int i = 0; i < 4; ++i) {
+    if (op->chan_batch[i] == batch) return exec_fft(op->chan_plan[i], C, dir, st);
+    if (op->chan_batch[i] == 0) {
+      if (int rc = make_plan(op, batch, &op->chan_plan[i])) return rc;
+      op->chan_batch[i] = batch;
+      return exec_fft(op->chan_plan[i], C, dir, st);
+    }
+  }
+  set_last_error("too many distinct channel batch sizes");
+  return kErrUnsupported;
 }
 
 static int finish(const double* partial, int np, double* out, cudaStream_t st) {
@@ -319,84 +481,87 @@ static int finish(const double* partial, int np, double* out, cudaStream_t st) {
   return kOk;
 }
 
-static int decompress(const Op* op, const float2* Xc, const float2* V, int s, float2* F,
-                      cudaStream_t st) {
-  if (s < 1 || s > 32) return kErrUnsupported;
-  const int tpb = 32;
-  dim3 grid(unsigned((op->n + 255) / 256), unsigned((op->L + tpb - 1) / tpb));
-  decompress_frames_kernel<<<grid, 256, tpb * s * sizeof(float2), st>>>(Xc, V, s, op->n, op->L,
-                                                                         tpb, F);
-  CBB_CUDA_TRY(cudaGetLastError());
-  return kOk;
-}
-
-static int gather(const Op* op, const float2* F, int mode, const float2* Ymeas, const float* w,
-                  float2* Y, double* partial, cudaStream_t st) {
-  gather_kernel<<<kRedBlocks, 256, 0, st>>>(F, op->pattern, op->n, op->L, op->m, op->scale, mode,
-                                            Ymeas, w, Y, partial);
-  CBB_CUDA_TRY(cudaGetLastError());
-  return kOk;
-}
-
 int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st) {
   float2* F = ws_frames(ws);
-  dim3 grid(unsigned((op->L + 31) / 32), unsigned((op->n + 31) / 32));
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(X, op->n, op->L, 1.f, F);
-  CBB_CUDA_TRY(cudaGetLastError());
-  int rc = fft(op, F, CUFFT_FORWARD, st);
-  if (rc) return rc;
-  count_launches(2);
-  return gather(op, F, 0, nullptr, nullptr, Y, nullptr, st);
+  const int64_t cm = int64_t(op->c) * op->m;
+  for (int ci = 0; ci < op->c; ++ci) {
+    dim3 grid(unsigned((op->L + 31) / 32), unsigned((op->n + 31) / 32));
+    coil_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(
+        X, op->n, op->L, op->coils ? op->coils + int64_t(ci) * op->n : nullptr, 1, 0, 1.f, 0, F);
+    CBB_CUDA_TRY(cudaGetLastError());
+    int rc = fft(op, F, CUFFT_FORWARD, st);
+    if (rc) return rc;
+    gather_kernel<<<kRedBlocks, 256, 0, st>>>(F, op->pattern, op->n, op->L, op->m, cm,
+                                              ci * op->m, op->scale, 0, nullptr, nullptr, Y,
+                                              nullptr);
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(3);
+  }
+  return kOk;
 }
 
 int op_adjoint(Op* op, const float2* Y, float2* X, void* ws, cudaStream_t st) {
   float2* F = ws_frames(ws);
-  CBB_CUDA_TRY(cudaMemsetAsync(F, 0, size_t(op->L) * op->n * sizeof(float2), st));
-  scatter_kernel<<<grid_for(int64_t(op->L) * op->m), 256, 0, st>>>(Y, op->pattern, op->n, op->L,
-                                                                     op->m, F);
-  CBB_CUDA_TRY(cudaGetLastError());
-  int rc = fft(op, F, CUFFT_INVERSE, st);
-  if (rc) return rc;
-  dim3 grid(unsigned((op->n + 31) / 32), unsigned((op->L + 31) / 32));
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(F, op->L, op->n, op->scale, X);
-  CBB_CUDA_TRY(cudaGetLastError());
-  count_launches(2);
+  const int64_t cm = int64_t(op->c) * op->m;
+  for (int ci = 0; ci < op->c; ++ci) {
+    CBB_CUDA_TRY(cudaMemsetAsync(F, 0, size_t(op->L) * op->n * sizeof(float2), st));
+    scatter_kernel<<<grid_for(int64_t(op->L) * op->m), 256, 0, st>>>(
+        Y, op->pattern, op->n, op->L, op->m, cm, ci * op->m, F);
+    CBB_CUDA_TRY(cudaGetLastError());
+    int rc = fft(op, F, CUFFT_INVERSE, st);
+    if (rc) return rc;
+    dim3 grid(unsigned((op->n + 31) / 32), unsigned((op->L + 31) / 32));
+    coil_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(
+        F, op->L, op->n, op->coils ? op->coils + int64_t(ci) * op->n : nullptr, 0, 1, op->scale,
+        ci > 0 ? 1 : 0, X);
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(2);
+  }
   return kOk;
 }
 
+// s-channel forward: channels -> c*s FFTs -> gather (mode 0 write / 1 norm / 2 residual)
 int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2* Y, void* ws,
                         const float2* Ymeas, const float* w, double* norm_out, cudaStream_t st) {
-  float2* F = ws_frames(ws);
-  int rc = decompress(op, Xc, V, s, F, st);
-  if (rc) return rc;
-  rc = fft(op, F, CUFFT_FORWARD, st);
+  if (s < 1 || s > 32) return kErrUnsupported;
+  float2* C = ws_frames(ws);
+  channels_kernel<<<unsigned((op->n + 255) / 256), 256, 0, st>>>(Xc, op->coils, op->c, s,
+                                                                   op->n, C);
+  CBB_CUDA_TRY(cudaGetLastError());
+  int rc = fft_channels(op, C, op->c * s, CUFFT_FORWARD, st);
   if (rc) return rc;
   double* part = ws_partial(op, ws);
-  if (Y == nullptr) {  // norm only
-    rc = gather(op, F, 1, nullptr, nullptr, nullptr, part, st);
-  } else if (Ymeas != nullptr) {
-    rc = gather(op, F, 2, Ymeas, w, Y, part, st);
-  } else {
-    rc = gather(op, F, 0, nullptr, nullptr, Y, norm_out ? part : nullptr, st);
-  }
-  if (rc) return rc;
+  int mode = 0;
+  if (Y == nullptr) mode = 1;
+  else if (Ymeas != nullptr) mode = 2;
+  gather_s_kernel<<<kRedBlocks, 256, 0, st>>>(C, op->pattern, op->n, op->L, op->m, op->c, s, V,
+                                              op->scale, mode, Ymeas, w, Y,
+                                              (mode != 0 || norm_out) ? part : nullptr);
+  CBB_CUDA_TRY(cudaGetLastError());
   count_launches(norm_out ? 3 : 2);
   if (norm_out) return finish(part, kRedBlocks, norm_out, st);
   return kOk;
 }
 
+// s-channel adjoint: deterministic k-space build per channel -> c*s IFFTs -> coil combine
 int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float2* Gc, void* ws,
                           cudaStream_t st) {
   if (s < 1 || s > 32) return kErrUnsupported;
-  float2* F = ws_frames(ws);
-  CBB_CUDA_TRY(cudaMemsetAsync(F, 0, size_t(op->L) * op->n * sizeof(float2), st));
-  scatter_kernel<<<grid_for(int64_t(op->L) * op->m), 256, 0, st>>>(R, op->pattern, op->n, op->L,
-                                                                     op->m, F);
+  float2* K = ws_frames(ws);
+  const unsigned g = unsigned((op->n + 127) / 128);
+  if (s <= 8)
+    kspace_s_kernel<8><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V, K);
+  else if (s <= 16)
+    kspace_s_kernel<16><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V,
+                                            K);
+  else
+    kspace_s_kernel<32><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V,
+                                            K);
   CBB_CUDA_TRY(cudaGetLastError());
-  int rc = fft(op, F, CUFFT_INVERSE, st);
+  int rc = fft_channels(op, K, op->c * s, CUFFT_INVERSE, st);
   if (rc) return rc;
-  compress_frames_kernel<<<unsigned((op->n + 255) / 256), 256, 0, st>>>(F, V, s, op->n, op->L,
-                                                                        op->scale, Gc);
+  combine_s_kernel<<<unsigned((op->n + 255) / 256), 256, 0, st>>>(K, op->coils, op->c, s, op->n,
+                                                                   op->scale, Gc);
   CBB_CUDA_TRY(cudaGetLastError());
   count_launches(2);
   return kOk;

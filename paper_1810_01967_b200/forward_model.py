@@ -112,9 +112,11 @@ class ForwardOperator:
             if pattern is None:
                 raise ValueError("cartesian operator needs a pattern")
             self.spatial_shape = _dims_of(pattern.spatial_shape)
-            if coil_maps is not None and (self.c != 1 or not np.allclose(coil_maps, 1.0)):
-                raise NotImplementedError(
-                    "coil sensitivity maps (c > 1) are not on the B200 path yet")
+            if coil_maps is None:
+                coil_maps = np.ones((self.c, self.n), dtype=complex)   # forward_model.py:104-105
+            elif tuple(np.shape(coil_maps)) != (self.c, self.n):
+                raise ValueError("coil map shape mismatch")
+            self.coil_maps = coil_maps
             lib = _lib.load()
             pat = np.asarray(pattern.indices)
             if pat.shape != (self.L, self.m):
@@ -127,6 +129,14 @@ class ForwardOperator:
                                          1 if self.identity_transform else 0,
                                          ctypes.byref(handle)), "cbb_op_create")
             self._op = handle
+            # unit maps stay implicit (no multiply); otherwise a device copy the op points to
+            self._coils_dev = None
+            if self.c > 1 or not np.allclose(np.asarray(coil_maps), 1.0):
+                self._coils_dev = torch.from_numpy(
+                    np.ascontiguousarray(coil_maps, dtype=np.complex64)).to(self.device)
+            _lib.check(lib.cbb_op_set_coils(
+                handle, self.c, None if self._coils_dev is None else self._coils_dev.data_ptr()),
+                "cbb_op_set_coils")
             self._ws_bytes = int(lib.cbb_op_workspace_bytes(handle))
         else:
             if matrix is None:
@@ -163,7 +173,7 @@ class ForwardOperator:
         X = self._check_image(X)
         host = not isinstance(X, torch.Tensor)
         Xd = self._to_dev(X)
-        Yfm = self.fm_apply(Xd)                       # (L, m) frame-major complex64
+        Yfm = self.fm_apply(Xd)                       # (L, c*m) frame-major complex64
         Y = Yfm.transpose(0, 1)
         return Y.contiguous().cpu().numpy().astype(np.complex128) if host else Y
 
@@ -189,19 +199,24 @@ class ForwardOperator:
     def _ws(self):
         return workspace(self._ws_bytes, self.device, f"op{id(self)}")
 
+    @property
+    def cm(self) -> int:
+        """Measurement columns per frame (c coils x m samples)."""
+        return self.c * self.m
+
     def fm_apply(self, X: torch.Tensor) -> torch.Tensor:
-        """(n, L) complex64 -> (L, m) complex64 frame-major."""
+        """(n, L) complex64 -> (L, c*m) complex64 frame-major."""
         X = X.contiguous()
         if self.kind == "dense_gaussian":
             return self._dense_apply(X)
-        Y = torch.empty((self.L, self.m), dtype=torch.complex64, device=self.device)
+        Y = torch.empty((self.L, self.cm), dtype=torch.complex64, device=self.device)
         _lib.check(_lib.load().cbb_op_apply(self._op, X.data_ptr(), Y.data_ptr(),
                                             self._ws().data_ptr(), _lib.stream_ptr()),
                    "cbb_op_apply")
         return Y
 
     def fm_adjoint(self, Yfm: torch.Tensor) -> torch.Tensor:
-        """(L, m) complex64 frame-major -> (n, L) complex64."""
+        """(L, c*m) complex64 frame-major -> (n, L) complex64."""
         Yfm = Yfm.contiguous()
         if self.kind == "dense_gaussian":
             return self._dense_adjoint(Yfm)
@@ -212,12 +227,13 @@ class ForwardOperator:
         return X
 
     def fm_apply_compressed(self, Xc, V, out=None):
-        """A(Xc V^H): (n, s) c64 coordinates -> (L, m) frame-major (decompress fused)."""
+        """A(Xc V^H): (n, s) c64 coordinates -> (L, c*m) frame-major (s-channel operator:
+        c*s FFTs of the subspace channel images, no (L, n) frame stack)."""
         Xc, V = Xc.contiguous(), V.contiguous()
         s = int(Xc.shape[1])
         if self.kind == "dense_gaussian" or s > 32:
             return self.fm_apply(Xc @ V.conj().transpose(0, 1))
-        Y = out if out is not None else torch.empty((self.L, self.m), dtype=torch.complex64,
+        Y = out if out is not None else torch.empty((self.L, self.cm), dtype=torch.complex64,
                                                     device=self.device)
         _lib.check(_lib.load().cbb_op_apply_compressed(self._op, Xc.data_ptr(), V.data_ptr(), s,
                                                        Y.data_ptr(), self._ws().data_ptr(),
@@ -240,7 +256,8 @@ class ForwardOperator:
         return out
 
     def fm_adjoint_compressed(self, R, V, out=None):
-        """(A^H R) V: (L, m) frame-major residual -> (n, s) coordinates (compress fused)."""
+        """(A^H R) V: (L, c*m) frame-major residual -> (n, s) coordinates (s-channel adjoint:
+        deterministic per-channel k-space build, c*s inverse FFTs, coil combine)."""
         R, V = R.contiguous(), V.contiguous()
         s = int(V.shape[1])
         if self.kind == "dense_gaussian" or s > 32:

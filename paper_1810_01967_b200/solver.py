@@ -152,11 +152,12 @@ class IpgState:
         self.dev = device
         self.dd = device_dictionary(dictionary, device)
         self.n, self.m, self.L = A.n, A.m, A.L
+        self.cm = getattr(A, "c", 1) * A.m                            # measurement columns
         self.dim = self.dd.s
         self.V = (None if basis is None else
                   torch.from_numpy(np.ascontiguousarray(basis, dtype=np.complex64)).to(device))
         Yfm = np.ascontiguousarray(np.asarray(Y).T, dtype=np.complex64)
-        self.Y = torch.from_numpy(Yfm).to(device)                      # (L, m)
+        self.Y = torch.from_numpy(Yfm).to(device)                      # (L, c*m)
         self.w = (None if weights is None else torch.from_numpy(np.ascontiguousarray(
             np.broadcast_to(weights, np.asarray(Y).shape).T, dtype=np.float32)).to(device))
         c64 = dict(dtype=torch.complex64, device=device)
@@ -166,8 +167,8 @@ class IpgState:
         self.G = torch.empty((n, dim), **c64)
         self.Z = torch.empty((n, dim), **c64)
         self.dX = torch.empty((n, dim), **c64)
-        self.AX = torch.zeros((self.L, self.m), **c64)
-        self.R = torch.empty((self.L, self.m), **c64)
+        self.AX = torch.zeros((self.L, self.cm), **c64)
+        self.R = torch.empty((self.L, self.cm), **c64)
         self.idx = torch.zeros(n, dtype=torch.int32, device=device)
         self.idx_n = torch.empty(n, dtype=torch.int32, device=device)
         self.gam = torch.zeros(n, dtype=torch.float64, device=device)

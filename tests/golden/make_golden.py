@@ -127,6 +127,63 @@ def solver_small():
                 nmse=np.array([r["nmse"] for r in rec]))
 
 
+def coil_maps(shape, c, seed):
+    """Smooth complex receive profiles (Gaussian magnitude around c centres, linear phase)."""
+    rng = np.random.default_rng(seed)
+    h, w = shape
+    yy, xx = np.meshgrid(np.arange(h) / h, np.arange(w) / w, indexing="ij")
+    maps = []
+    for _ in range(c):
+        cy, cx = rng.uniform(0, 1, size=2)
+        mag = np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 0.3)
+        ph = 2 * np.pi * (rng.uniform(-1, 1) * yy + rng.uniform(-1, 1) * xx)
+        maps.append((mag * np.exp(1j * ph)).ravel())
+    return np.array(maps)
+
+
+def coil_cases():
+    """Multi-coil operator (forward_model.py:123-167 with c > 1), its compressed chain, and a
+    small compressed IPG solve with coils through the reference."""
+    out = {}
+    rng = np.random.default_rng(40)
+    shape, c, L, s = (16, 16), 3, 6, 3
+    pat = ref_fm.make_epi_pattern(shape, 4, L).indices
+    S = coil_maps(shape, c, 41)
+    P = ref_fm.SamplingPattern(indices=pat, spatial_shape=shape)
+    A = ref_fm.make_cartesian_operator(P, coil_maps=S)
+    n = A.n
+    X = rng.standard_normal((n, L)) + 1j * rng.standard_normal((n, L))
+    Y = rng.standard_normal((c * A.m, L)) + 1j * rng.standard_normal((c * A.m, L))
+    V, _ = np.linalg.qr(rng.standard_normal((L, s)) + 1j * rng.standard_normal((L, s)))
+    Xc = rng.standard_normal((n, s)) + 1j * rng.standard_normal((n, s))
+    out.update(op_pattern=pat, op_shape=np.array(shape), op_coils=S, op_X=X, op_Y=Y,
+               op_AX=A.apply(X), op_AHY=A.adjoint(Y), op_V=V, op_Xc=Xc,
+               op_AXc=A.apply(Xc @ V.conj().T), op_AHYV=A.adjoint(Y) @ V)
+    # small IPG with 2 coils
+    cfg = workloads.make_cfg0(h=32, w=32, L=60, s=8, lines=6, snr_db=30.0, n_t1=20, n_t2=20)
+    dct = cfg.dictionary
+    rdict = ref_dict.Dictionary(atoms=dct.atoms, norms=dct.norms, lookup_table=dct.lookup_table,
+                                tr_ms=dct.tr_ms, L=dct.L)
+    cd = ref_dict.svd_compress(rdict, 8)
+    S2 = coil_maps(cfg.spatial_shape, 2, 42)
+    P2 = ref_fm.SamplingPattern(indices=cfg.pattern, spatial_shape=cfg.spatial_shape)
+    A2 = ref_fm.make_cartesian_operator(P2, coil_maps=S2)
+    clean = A2.apply(cfg.gt)
+    noise = rng.standard_normal(clean.shape) + 1j * rng.standard_normal(clean.shape)
+    noise *= np.linalg.norm(clean) * 10 ** (-30 / 20) / np.linalg.norm(noise)
+    Yc = clean + noise
+    conf = ref_solver.SolverConfig(mode="blip_exact", max_iters=8, zeta=2.0, compressed=8)
+    Xs, maps, gam, trace = ref_solver.solve_compressed(Yc, A2, cd, None, conf, gt=cfg.gt)
+    rec = trace.records
+    out.update(ipg_Y=Yc, ipg_pattern=cfg.pattern, ipg_shape=np.array(cfg.spatial_shape),
+               ipg_coils=S2, ipg_basis=cd.basis, ipg_atoms_c=cd.atoms_compressed,
+               ipg_lookup=dct.lookup_table, ipg_X=Xs, ipg_gammas=gam, ipg_t1=maps.t1,
+               ipg_t2=maps.t2, ipg_fidelity=np.array([r["fidelity"] for r in rec]),
+               ipg_mu=np.array([r["mu"] for r in rec]),
+               ipg_shrinks=np.array([r["shrinks"] for r in rec]))
+    return out
+
+
 def cfg0_reference():
     """BASELINE configs[0] through the reference (20 iterations, s = 10)."""
     cfg = workloads.make_cfg0()
@@ -156,11 +213,18 @@ def cfg0_reference():
 def main():
     meta = dict(reference_version=coverblip.__version__, numpy=np.__version__)
     print(meta)
+    only = sys.argv[1:]   # e.g. "coils": regenerate just that fixture
+    if only:
+        if "coils" in only:
+            np.savez_compressed(os.path.join(HERE, "coils.npz"), **coil_cases())
+        print("golden fixtures written to", HERE, only)
+        return
     np.savez_compressed(os.path.join(HERE, "projection.npz"), **projection_cases())
     np.savez_compressed(os.path.join(HERE, "operator.npz"), **operator_cases())
     np.savez_compressed(os.path.join(HERE, "solver_small.npz"), **solver_small())
     np.savez_compressed(os.path.join(HERE, "cfg0_reference.npz"), **cfg0_reference(),
                         numpy_version=np.array(np.__version__))
+    np.savez_compressed(os.path.join(HERE, "coils.npz"), **coil_cases())
     print("golden fixtures written to", HERE)
 
 

@@ -51,6 +51,16 @@ def test_operator_matches_reference(case):
     np.testing.assert_allclose(A.adjoint(g[f"{case}_Y"]), g[f"{case}_AHY"], rtol=0, atol=1e-12)
 
 
+def test_coil_operator_matches_reference():
+    """c = 3 coil maps: the oracle restatement against the reference's own outputs."""
+    g = load("coils.npz")
+    A = oop.CartesianOperator(g["op_pattern"], tuple(g["op_shape"]), coil_maps=g["op_coils"])
+    np.testing.assert_allclose(A.apply(g["op_X"]), g["op_AX"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(A.adjoint(g["op_Y"]), g["op_AHY"], rtol=0, atol=1e-12)
+    V, Xc = g["op_V"], g["op_Xc"]
+    np.testing.assert_allclose(A.apply(Xc @ V.conj().T), g["op_AXc"], rtol=0, atol=1e-12)
+
+
 def test_operator_adjoint_identity_3d():
     """3-D restatement (cfg4): <A X, Y> == <X, A^H Y>."""
     rng = np.random.default_rng(4)
