@@ -99,9 +99,14 @@ int cbb_project_best(const void* z, int32_t z_c128, int64_t n, const cbb_dict_vi
  * (projection.py:64 write-back of the winners a shard owns; outputs are summed over ranks). */
 int cbb_scaled_rows(const cbb_dict_view* dict, int64_t atom_offset, const int64_t* idx,
                     const double* gamma, int64_t n, void* out, int32_t out_c128, void* stream);
-/* Number of voxels that needed the exhaustive fp64 rescan in the last call (synchronises). */
+/* Number of voxels the last call's screening pass could not certify (candidate lists full or
+ * non-finite input): they were rescanned exhaustively in fp64.  Synchronises. */
 int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count_host,
                                void* stream);
+/* counts_host[0] as above; counts_host[1] = voxels whose tcgen05 candidate lists held many
+ * chunks (coherent dictionaries) and were rescored warp-cooperatively.  Synchronises. */
+int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,
+                                void* stream);
 /* Bring-up / test hook: prologue only (bf16 voxel tiles + windows in the workspace). */
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
                          void* workspace, size_t workspace_bytes, void* stream);

@@ -51,6 +51,7 @@ SIGNATURES = {
                                  c_vp, c_size, c_i32, c_vp]),
     "cbb_scaled_rows": (c_int, [ctypes.POINTER(DictView), c_i64, c_vp, c_vp, c_i64, c_vp, c_i32,
                                 c_vp]),
+    "cbb_project_overflow_counts": (c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "cbb_project_overflow_count": (c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_int), c_vp]),
     "cbb_project_prologue": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_size,
                                      c_vp]),

@@ -31,6 +31,7 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr);
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st);
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st);
+int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st);
 int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile, int b_tile,
                     float* out, cudaStream_t st);
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr, cudaStream_t st);
@@ -180,6 +181,12 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
 int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count_host,
                                void* stream) {
   return project_overflow_count(workspace, n, s, count_host, S(stream));
+}
+
+int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,
+                                void* stream) {
+  if (!workspace || !counts_host) return kErrArgument;
+  return project_overflow_counts(workspace, n, s, counts_host, S(stream));
 }
 
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,

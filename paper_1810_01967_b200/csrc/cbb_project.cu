@@ -73,6 +73,32 @@ __device__ __forceinline__ double exact_score_g(const ZSource& zs, int64_t v, in
 
 // Winner write-back: idx, gamma = max(score, 0) (projection.py:42), gamma * D_j (projection.py:64),
 // and for the IPG trial dX = P - X with its squared norm (solver.py:129-130).
+// Re<z, d_j> in fp64 with z staged as planar (zr, zi); the same fma order as every other
+// exact-score path.  S > 0: fully unrolled, predicated on k < s (all 2s loads in flight);
+// S == 0: runtime loop (s > 32).
+template <int S>
+__device__ __forceinline__ double dot_atom(const double* zr, const double* zi,
+                                           const double2* __restrict__ a, int s) {
+  double acc = 0.0;
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      if (k < s) {
+        const double2 ak = a[k];
+        acc = fma(zr[k], ak.x, acc);
+        acc = fma(zi[k], ak.y, acc);
+      }
+    }
+  } else {
+    for (int k = 0; k < s; ++k) {
+      const double2 ak = a[k];
+      acc = fma(zr[k], ak.x, acc);
+      acc = fma(zi[k], ak.y, acc);
+    }
+  }
+  return acc;
+}
+
 __device__ void write_winner(const ProjOut& out, const DictView& dv, int64_t v, int64_t j,
                              double score) {
   const int s = dv.s;
@@ -138,6 +164,76 @@ struct CandList {
     cs[cnt * stride] = sc;
     cj[cnt * stride] = j;
     ++cnt;
+  }
+};
+
+// tcgen05 screen candidate list: a kCandCap-entry shared-memory list (fast, enough for
+// incoherent dictionaries) that spills to a kGCap-entry list in GLOBAL memory (L2-resident)
+// when compaction cannot make room -- coherent dictionaries (fine MRF grids) put up to a few
+// hundred chunks inside the fp16 window.  Global entry c sits at gbase[c * gstride] as
+// (packed chunk, approximate chunk max bits).  Stale entries are dropped lazily.
+constexpr int kGCap = 128;
+
+__device__ __noinline__ int gcand_compact(int2* base, int64_t stride, int cnt, float thr) {
+  int k = 0;
+  for (int c = 0; c < cnt; ++c) {
+    const int2 e = base[c * stride];
+    if (__int_as_float(e.y) >= thr) base[(k++) * stride] = e;
+  }
+  return k;
+}
+
+struct HCandList {
+  int* cj;           // shared-memory list, column layout [kCandCap][stride]
+  float* cs;
+  int stride;
+  int cnt;
+  int2* gbase;       // global spill list
+  int64_t gstride;
+  int gcnt;
+  bool ovf;
+
+  __device__ __noinline__ void spill(float thr) {
+    // move the live shared entries to the global list (compacting it first if needed)
+    int live = 0;
+    for (int c = 0; c < cnt; ++c) live += cs[c * stride] >= thr;
+    if (gcnt + live > kGCap) gcnt = gcand_compact(gbase, gstride, gcnt, thr);
+    if (gcnt + live > kGCap) {
+      ovf = true;
+      return;
+    }
+    for (int c = 0; c < cnt; ++c)
+      if (cs[c * stride] >= thr)
+        gbase[(gcnt++) * gstride] = make_int2(cj[c * stride], __float_as_int(cs[c * stride]));
+    cnt = 0;
+  }
+
+  __device__ __forceinline__ void insert(int j, float sc, float thr) {
+    if (cnt == kCandCap) {
+      cnt = cand_compact(cj, cs, stride, thr);
+      if (cnt == kCandCap) {
+        spill(thr);
+        if (ovf) return;
+      }
+    }
+    cs[cnt * stride] = sc;
+    cj[cnt * stride] = j;
+    ++cnt;
+  }
+
+  // hand-off: append the surviving shared entries to the global list; returns the total or
+  // -1 on overflow
+  __device__ __forceinline__ int finish(float thr) {
+    if (ovf) return -1;
+    for (int c = 0; c < cnt; ++c) {
+      const float x = cs[c * stride];
+      if (x >= thr) {
+        if (gcnt == kGCap) gcnt = gcand_compact(gbase, gstride, gcnt, thr);
+        if (gcnt == kGCap) return -1;
+        gbase[(gcnt++) * gstride] = make_int2(cj[c * stride], __float_as_int(x));
+      }
+    }
+    return gcnt;
   }
 };
 
@@ -381,9 +477,13 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
 }
 
 // ============================================================== FFMA screening
+// vlist != nullptr: screen only the *vcount voxels listed (the tcgen05 pass's overflows --
+// coherent dictionaries whose fp16 window holds more chunks than its candidate lists).
 template <int S>
 __global__ void __launch_bounds__(128) mf_ffma_kernel(ZSource zs, DictView dv, int64_t n,
                                                       const float* __restrict__ win32,
+                                                      const int* __restrict__ vcount,
+                                                      const int64_t* __restrict__ vlist,
                                                       ProjOut out, int* ovf_count,
                                                       int64_t* ovf_list) {
   constexpr int TA = 128;  // atoms per shared tile
@@ -391,8 +491,11 @@ __global__ void __launch_bounds__(128) mf_ffma_kernel(ZSource zs, DictView dv, i
   __shared__ int cj[kCandCap * 128];
   __shared__ float cs[kCandCap * 128];
   const int tid = threadIdx.x;
-  const int64_t v = int64_t(blockIdx.x) * 128 + tid;
-  const bool live = v < n;
+  const int64_t cnt = vlist ? int64_t(*vcount) : n;
+  if (int64_t(blockIdx.x) * 128 >= cnt) return;  // block-uniform
+  const int64_t slot = int64_t(blockIdx.x) * 128 + tid;
+  const bool live = slot < cnt;
+  const int64_t v = live ? (vlist ? vlist[slot] : slot) : 0;
   float zr[S], zi[S];
 #pragma unroll
   for (int k = 0; k < S; ++k) {
@@ -443,6 +546,7 @@ __global__ void __launch_bounds__(128) mf_ffma_kernel(ZSource zs, DictView dv, i
 
 // ============================================================== exhaustive fp64 scan
 // Warp per voxel.  Handles the overflow list (list != null) or every voxel (list == null).
+template <int S>
 __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv, int64_t n,
                                                          const int* ovf_count,
                                                          const int64_t* ovf_list,
@@ -464,13 +568,7 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
     double bs = -INFINITY;
     int64_t best = INT64_MAX;
     for (int64_t j = lane; j < dv.d; j += 32) {
-      const double2* a = dv.atoms64 + j * s;
-      double acc = 0.0;
-      for (int k = 0; k < s; ++k) {
-        double2 ak = a[k];
-        acc = fma(zw[k], ak.x, acc);
-        acc = fma(zw[s + k], ak.y, acc);
-      }
+      const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
       if (acc > bs) { bs = acc; best = j; }
     }
 #pragma unroll
@@ -611,7 +709,7 @@ __device__ __forceinline__ __half hmax_halves(__half2 m) {
 // Record 32-atom chunk (16 packed registers) with max cm: groups g < 5 -> registers
 // 3g..3g+2 (atoms 6g..6g+5), g = 5 -> register 15 (atoms 30, 31).
 __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64_t jb, __half thr,
-                                             float thr_f, CandList& cl) {
+                                             float thr_f, HCandList& cl) {
   uint32_t mask = __hge(hmax_halves(as_h2(r[15])), thr) ? (1u << 5) : 0u;
 #pragma unroll
   for (int i = 0; i < 5; ++i)
@@ -625,7 +723,7 @@ __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64
 template <int NC>
 __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_t jb, float win,
                                             __half& runmax, __half& thr, bool& active,
-                                            CandList& cl) {
+                                            HCandList& cl) {
   // NC independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
   __half2 c[NC];
 #pragma unroll
@@ -840,7 +938,8 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(0, it);
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
-      CandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0, false};
+      HCandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0,
+                   cand + int64_t(part) * kGCap * n_pad + (live ? v : 0), n_pad, 0, false};
       __half runmax = __ushort_as_half(0xFC00);
       __half thr = __ushort_as_half(active ? 0xFC00 : 0x7C00);
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
@@ -878,25 +977,13 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         ba += kParts;
         if (ba >= nB) ba -= nB;
       }
-      // ---- hand-off (no inter-part barrier): this part's surviving chunk entries and its
-      // running max go to the global candidate buffer; rescore_kernel merges the parts and
-      // rescans the flagged groups in fp64
+      // ---- hand-off (no inter-part barrier): this part's surviving chunk entries are appended
+      // to its global list (after any spills); count and running max go to meta.
+      // rescore_kernel merges the parts and rescans the flagged groups in fp64
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(1, it);
       if (live) {
-        int k = 0;
-        if (!cl.ovf && win >= 0.f) {
-          const float thr_f = __half2float(runmax) - win;
-          for (int c = 0; c < cl.cnt; ++c) {
-            const float x = cl.cs[c * C::kSlots];
-            if (x >= thr_f) {
-              cand[(int64_t(part) * kCandCap + k) * n_pad + v] =
-                  make_int2(cl.cj[c * C::kSlots], __float_as_int(x));
-              ++k;
-            }
-          }
-        }
-        meta[int64_t(part) * n_pad + v] =
-            make_int2(cl.ovf ? -1 : k, __float_as_int(__half2float(runmax)));
+        const int total = (win >= 0.f) ? cl.finish(__half2float(runmax) - win) : 0;
+        meta[int64_t(part) * n_pad + v] = make_int2(total, __float_as_int(__half2float(runmax)));
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(2, it);
     }
@@ -909,17 +996,47 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
 }
 
 // ============================================================== fp64 rescoring of tcgen05 candidates
-// One thread per voxel.  Merges the parts' running maxima (gmax), keeps the entries whose
-// approximate chunk max lies inside the final window gmax - win, rescans their flagged groups
-// exactly in fp64 from the caller's atoms and voxel, and writes the winner (lowest index on
-// exact ties, projection.py:62).  Zero voxels -> index 0 / gamma 0; overflowed candidate lists
-// and non-finite voxels -> exhaustive list.
-__global__ void __launch_bounds__(256) rescore_kernel(ZSource zs, DictView dv, int64_t n,
-                                                      int64_t n_pad,
-                                                      const float* __restrict__ win_tc,
-                                                      const int2* __restrict__ cand,
-                                                      const int2* __restrict__ meta, ProjOut out,
-                                                      int* ovf_count, int64_t* ovf_list) {
+// rescore_fast_kernel (below) handles every voxel with few entries; this one takes the heavy
+// list.  One WARP per voxel (grid-stride): merges the parts' running maxima (gmax), keeps the chunk
+// entries whose approximate max lies inside the final window gmax - win, and rescans their
+// flagged groups exactly in fp64 from the caller's atoms and voxel -- the entries are spread
+// over the lanes, each lane scoring its entry's atoms against the voxel staged in shared
+// memory; a warp reduction keeps the best score, lowest index on exact ties (projection.py:62).
+// Zero voxels -> index 0 / gamma 0; overflowed candidate lists and non-finite voxels -> the
+// next stage's list (fp32 FFMA re-screen).
+constexpr int kRescoreWarps = 8;
+constexpr int kFastEntries = 8;   // thread-per-voxel rescoring up to this many chunk entries
+
+// Expand one chunk entry and rescore its flagged atoms (chunk mask: 6-atom groups).
+template <int S>
+__device__ __forceinline__ void rescore_entry(int2 en, const double* zr, const double* zi,
+                                              int s, const DictView& dv, int64_t& best,
+                                              double& bs) {
+  const int64_t j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
+  uint32_t mask = uint32_t(en.x) >> kChunkShift;
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
+    for (int i = lo; i < hi; ++i) {
+      const int64_t j = j0 + i;
+      if (j >= dv.d) break;
+      const double acc = dot_atom<S>(zr, zi, dv.atoms64 + j * s, s);
+      if (acc > bs || (acc == bs && j < best)) {
+        bs = acc;
+        best = j;
+      }
+    }
+  }
+}
+
+// One THREAD per voxel: zero voxels, overflow routing and voxels with <= kFastEntries chunk
+// entries (every incoherent dictionary); heavier voxels go to the warp kernel's list.
+template <int S>
+__global__ void __launch_bounds__(256) rescore_fast_kernel(
+    ZSource zs, DictView dv, int64_t n, int64_t n_pad, const float* __restrict__ win_tc,
+    const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
+    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const float win = win_tc[v];
@@ -927,9 +1044,9 @@ __global__ void __launch_bounds__(256) rescore_kernel(ZSource zs, DictView dv, i
     write_winner(out, dv, v, 0, 0.0);
     return;
   }
+  int cnt[kParts];
   float gmax = -INFINITY;
   bool ovf = !(win >= 0.f);
-  int cnt[kParts];
 #pragma unroll
   for (int p = 0; p < kParts; ++p) {
     const int2 m = meta[int64_t(p) * n_pad + v];
@@ -937,33 +1054,108 @@ __global__ void __launch_bounds__(256) rescore_kernel(ZSource zs, DictView dv, i
     ovf |= m.x < 0;
     gmax = fmaxf(gmax, __int_as_float(m.y));
   }
-  int64_t best = -1;
-  double bs = -INFINITY;
-  if (!ovf) {
-    const float thr = gmax - win;
-#pragma unroll
-    for (int p = 0; p < kParts; ++p) {
-      for (int c = 0; c < cnt[p]; ++c) {
-        const int2 e = cand[(int64_t(p) * kCandCap + c) * n_pad + v];
-        if (__int_as_float(e.y) < thr) continue;
-        const int64_t j0 = int64_t(uint32_t(e.x) & ((1u << kChunkShift) - 1)) << 5;
-        uint32_t mask = uint32_t(e.x) >> kChunkShift;
-        while (mask) {
-          const int b = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
-          for (int i = lo; i < hi; ++i)
-            if (j0 + i < dv.d) rescore_one(zs, dv, v, j0 + i, best, bs);
-        }
-      }
-    }
+  if (ovf) {
+    ovf_list[atomicAdd(ovf_count, 1)] = v;
+    return;
   }
-  if (ovf || best < 0) {
-    const int slot = atomicAdd(ovf_count, 1);
-    ovf_list[slot] = v;
+  if (cnt[0] + cnt[1] + cnt[2] > kFastEntries) {
+    heavy_list[atomicAdd(heavy_count, 1)] = v;
+    return;
+  }
+  const int s = dv.s;
+  double zr[32], zi[32];
+  for (int k = 0; k < s; ++k) {
+    const double2 z = load_z(zs, v, s, k);
+    zr[k] = z.x;
+    zi[k] = z.y;
+  }
+  const float thr = gmax - win;
+  int64_t best = INT64_MAX;
+  double bs = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < kParts; ++p)
+    for (int c = 0; c < cnt[p]; ++c) {
+      const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
+      if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zr, zi, s, dv, best, bs);
+    }
+  if (best == INT64_MAX) {
+    ovf_list[atomicAdd(ovf_count, 1)] = v;
     return;
   }
   write_winner(out, dv, v, best, bs);
+}
+
+
+template <int S>
+__global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
+    ZSource zs, DictView dv, int64_t n_pad, const float* __restrict__ win_tc,
+    const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
+    int64_t* ovf_list, const int* heavy_count, const int64_t* heavy_list) {
+  extern __shared__ double zsh_all[];  // kRescoreWarps x 2s
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = dv.s;
+  double* zsh = zsh_all + size_t(wid) * 2 * s;
+  const int64_t nw = int64_t(gridDim.x) * kRescoreWarps;
+  const int64_t nh = *heavy_count;
+  for (int64_t h = int64_t(blockIdx.x) * kRescoreWarps + wid; h < nh; h += nw) {
+    const int64_t v = heavy_list[h];
+    const float win = win_tc[v];
+    if (win < 0.f) {
+      if (lane == 0) write_winner(out, dv, v, 0, 0.0);
+      continue;
+    }
+    int cnt[kParts];
+    float gmax = -INFINITY;
+    bool ovf = !(win >= 0.f);
+#pragma unroll
+    for (int p = 0; p < kParts; ++p) {
+      const int2 m = meta[int64_t(p) * n_pad + v];  // same address in every lane: broadcast
+      cnt[p] = m.x;
+      ovf |= m.x < 0;
+      gmax = fmaxf(gmax, __int_as_float(m.y));
+    }
+    if (ovf) {
+      if (lane == 0) {
+        const int slot = atomicAdd(ovf_count, 1);
+        ovf_list[slot] = v;
+      }
+      continue;
+    }
+    for (int k = lane; k < s; k += 32) {
+      const double2 z = load_z(zs, v, s, k);
+      zsh[k] = z.x;
+      zsh[s + k] = z.y;
+    }
+    __syncwarp();
+    const float thr = gmax - win;
+    const int total = cnt[0] + cnt[1] + cnt[2];
+    int64_t best = INT64_MAX;
+    double bs = -INFINITY;
+    for (int e = lane; e < total; e += 32) {
+      const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
+      const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
+      const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
+      if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zsh, zsh + s, s, dv, best, bs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double obs = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+      if (obs > bs || (obs == bs && ob < best)) {
+        bs = obs;
+        best = ob;
+      }
+    }
+    if (lane == 0) {
+      if (best == INT64_MAX) {
+        const int slot = atomicAdd(ovf_count, 1);
+        ovf_list[slot] = v;
+      } else {
+        write_winner(out, dv, v, best, bs);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // Debug: raw fp16 tcgen05 scores (A = voxel rows staged into TMEM, B = swizzled atom tile in
@@ -1160,13 +1352,15 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
 // Workspace carve-up for one projection call.
 struct ProjWs {
   int64_t n_pad;
-  int2* cand;      // [kParts][kCandCap][n_pad] tcgen05 chunk entries (entry, approx max)
+  int2* cand;      // [kParts][kGCap][n_pad] tcgen05 chunk entries (entry, approx max)
   int2* meta;      // [kParts][n_pad] (entry count or -1 on overflow, part running max)
   uint8_t* ztiles;
   float* win_tc;
   float* win32;
-  int* ovf_count;
+  int* ovf_count;       // tcgen05 / FFMA pass overflows (next stage's voxel list)
   int64_t* ovf_list;
+  int* heavy_count;     // voxels with many tcgen05 chunk entries (warp rescoring)
+  int64_t* heavy_list;
   double* nd_v;
   double* partial;
 };
@@ -1186,12 +1380,14 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   ProjWs w{};
   w.n_pad = n_vt * kVoxPad;
   w.ztiles = take(size_t(n_vt) * kVoxPad * kp * 2);  // first: cbb_debug_tc_scores reads it
-  w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * kCandCap * sizeof(int2)));
+  w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * kGCap * sizeof(int2)));
   w.meta = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * sizeof(int2)));
   w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.ovf_count = reinterpret_cast<int*>(take(16));
   w.ovf_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
+  w.heavy_count = reinterpret_cast<int*>(take(16));
+  w.heavy_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   w.nd_v = reinterpret_cast<double*>(take(size_t(n) * 8));
   w.partial = reinterpret_cast<double*>(take(kReduceBlocks * 8));
   if (ws) *ws = w;
@@ -1229,37 +1425,48 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   return kOk;
 }
 
+// FFMA screening of all n voxels (vlist == nullptr) or of the *vcount listed ones; its own
+// overflows go to (oc, ol) for the exhaustive fp64 rescan.
+struct FfmaArgs {
+  const int* vcount;
+  const int64_t* vlist;
+  int* oc;
+  int64_t* ol;
+};
+
 template <int S>
 static int launch_ffma(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                       const ProjOut& out, cudaStream_t st) {
+                       const ProjOut& out, const FfmaArgs& fa, cudaStream_t st) {
   const int blocks = int((n + 127) / 128);
-  mf_ffma_kernel<S><<<blocks, 128, 0, st>>>(zs, dv, n, w.win32, out, w.ovf_count, w.ovf_list);
+  mf_ffma_kernel<S><<<blocks, 128, 0, st>>>(zs, dv, n, w.win32, fa.vcount, fa.vlist, out, fa.oc,
+                                             fa.ol);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
 
 static int dispatch_ffma(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                         const ProjOut& out, cudaStream_t st) {
+                         const ProjOut& out, const FfmaArgs& fa, cudaStream_t st) {
   switch (dv.s_pad) {
-    case 2: return launch_ffma<2>(w, n, zs, dv, out, st);
-    case 4: return launch_ffma<4>(w, n, zs, dv, out, st);
-    case 6: return launch_ffma<6>(w, n, zs, dv, out, st);
-    case 8: return launch_ffma<8>(w, n, zs, dv, out, st);
-    case 10: return launch_ffma<10>(w, n, zs, dv, out, st);
-    case 12: return launch_ffma<12>(w, n, zs, dv, out, st);
-    case 16: return launch_ffma<16>(w, n, zs, dv, out, st);
-    case 20: return launch_ffma<20>(w, n, zs, dv, out, st);
-    case 24: return launch_ffma<24>(w, n, zs, dv, out, st);
-    case 32: return launch_ffma<32>(w, n, zs, dv, out, st);
+    case 2: return launch_ffma<2>(w, n, zs, dv, out, fa, st);
+    case 4: return launch_ffma<4>(w, n, zs, dv, out, fa, st);
+    case 6: return launch_ffma<6>(w, n, zs, dv, out, fa, st);
+    case 8: return launch_ffma<8>(w, n, zs, dv, out, fa, st);
+    case 10: return launch_ffma<10>(w, n, zs, dv, out, fa, st);
+    case 12: return launch_ffma<12>(w, n, zs, dv, out, fa, st);
+    case 16: return launch_ffma<16>(w, n, zs, dv, out, fa, st);
+    case 20: return launch_ffma<20>(w, n, zs, dv, out, fa, st);
+    case 24: return launch_ffma<24>(w, n, zs, dv, out, fa, st);
+    case 32: return launch_ffma<32>(w, n, zs, dv, out, fa, st);
   }
   return kErrUnsupported;
 }
 
-static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, const int* cnt,
-                             const int64_t* list, const ProjOut& out, cudaStream_t st) {
+template <int S>
+static int launch_exhaustive_s(int64_t n, const ZSource& zs, const DictView& dv, const int* cnt,
+                               const int64_t* list, const ProjOut& out, cudaStream_t st) {
   const size_t shm = size_t(8) * 2 * dv.s * sizeof(double);
   if (shm > 48 * 1024) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(exhaustive_kernel,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(exhaustive_kernel<S>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
   }
   int grid = num_sms() * 4;
@@ -1267,7 +1474,45 @@ static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, c
     int64_t need = (n + 7) / 8;
     if (need < grid) grid = int(need > 0 ? need : 1);
   }
-  exhaustive_kernel<<<grid, 256, shm, st>>>(zs, dv, n, cnt, list, out);
+  exhaustive_kernel<S><<<grid, 256, shm, st>>>(zs, dv, n, cnt, list, out);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+// compile-time width for the fp64 scoring loops (s_pad; 0 = runtime loop for s > 32)
+#define CBB_DISPATCH_S(s_pad, CALL)          \
+  switch (s_pad) {                          \
+    case 2: { constexpr int S_ = 2; CALL; }   \
+    case 4: { constexpr int S_ = 4; CALL; }   \
+    case 6: { constexpr int S_ = 6; CALL; }   \
+    case 8: { constexpr int S_ = 8; CALL; }   \
+    case 10: { constexpr int S_ = 10; CALL; } \
+    case 12: { constexpr int S_ = 12; CALL; } \
+    case 16: { constexpr int S_ = 16; CALL; } \
+    case 20: { constexpr int S_ = 20; CALL; } \
+    case 24: { constexpr int S_ = 24; CALL; } \
+    case 32: { constexpr int S_ = 32; CALL; } \
+    default: { constexpr int S_ = 0; CALL; }  \
+  }
+
+static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, const int* cnt,
+                             const int64_t* list, const ProjOut& out, cudaStream_t st) {
+  const int sp = s_pad_for(dv.s);
+  CBB_DISPATCH_S(sp, return launch_exhaustive_s<S_>(n, zs, dv, cnt, list, out, st));
+  return kOk;
+}
+
+template <int S>
+static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
+                          const ProjOut& o, cudaStream_t st) {
+  rescore_fast_kernel<S><<<int((n + 255) / 256), 256, 0, st>>>(
+      zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
+      w.heavy_list);
+  CBB_CUDA_TRY(cudaGetLastError());
+  const size_t shm = size_t(kRescoreWarps) * 2 * dv.s * sizeof(double);
+  rescore_warp_kernel<S><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
+      zr, dv, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
+      w.heavy_list);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
@@ -1299,6 +1544,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   if (algo == 1 && !tc_ok) return kErrUnsupported;
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
+  CBB_CUDA_TRY(cudaMemsetAsync(w.heavy_count, 0, sizeof(int), st));
   if (algo == 1 || algo == 2) {
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
@@ -1308,16 +1554,16 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
+    const FfmaArgs all{nullptr, nullptr, w.ovf_count, w.ovf_list};
     int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
                                           : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
-                         : dispatch_ffma(w, n, zr, dv, o, st);
+                         : dispatch_ffma(w, n, zr, dv, o, all, st);
     if (rc) return rc;
     timing_mark(1, st);
     if (algo == 1) {
-      rescore_kernel<<<int((n + 255) / 256), 256, 0, st>>>(zr, dv, n, w.n_pad, w.win_tc, w.cand,
-                                                           w.meta, o, w.ovf_count, w.ovf_list);
-      CBB_CUDA_TRY(cudaGetLastError());
-      count_launches(1);
+      CBB_DISPATCH_S(dv.s_pad, rc = launch_rescore<S_>(w, n, zr, dv, o, st); break);
+      if (rc) return rc;
+      count_launches(2);
     }
     count_launches(3);  // prologue, screening kernel, exhaustive rescan
     {
@@ -1350,6 +1596,15 @@ int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cuda
   ProjWs w;
   project_ws_bytes(n, s, &w, ws_ptr);
   CBB_CUDA_TRY(cudaMemcpyAsync(host_count, w.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBB_CUDA_TRY(cudaStreamSynchronize(st));
+  return kOk;
+}
+
+int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st) {
+  ProjWs w;
+  project_ws_bytes(n, s, &w, ws_ptr);
+  CBB_CUDA_TRY(cudaMemcpyAsync(host2, w.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBB_CUDA_TRY(cudaMemcpyAsync(host2 + 1, w.heavy_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   CBB_CUDA_TRY(cudaStreamSynchronize(st));
   return kOk;
 }

@@ -175,8 +175,21 @@ def _project_pipelined(zh: torch.Tensor, dd: DeviceDictionary, algo: str, dev):
     return hidx, hgam, hproj
 
 
+def overflow_counts(n: int, s: int):
+    """(voxels rescanned exhaustively in fp64, voxels with many tcgen05 candidate chunks that
+    were rescored warp-cooperatively) of the last projection of this shape (diagnostic)."""
+    lib = _lib.load()
+    dev = require_cuda()
+    wsb = lib.cbb_project_workspace_bytes(n, s)
+    ws = workspace(wsb, dev, "project")
+    out = (ctypes.c_int32 * 2)()
+    _lib.check(lib.cbb_project_overflow_counts(ws.data_ptr(), n, s, out, _lib.stream_ptr()),
+               "overflow_counts")
+    return int(out[0]), int(out[1])
+
+
 def overflow_count(n: int, s: int) -> int:
-    """Voxels that needed the exhaustive fp64 rescan in the last projection (diagnostic)."""
+    """Voxels the last projection rescanned exhaustively in fp64 (diagnostic)."""
     lib = _lib.load()
     dev = require_cuda()
     wsb = lib.cbb_project_workspace_bytes(n, s)

@@ -11,7 +11,11 @@ in-vivo scans are absent, so every config is generated from fixed seeds
         random lines per frame; 30 dB noise (reference ``harness.py:145-153`` rule).
 * cfg1  N = 2^20 voxels x D = 2^17 random unit atoms, s = 10, voxel = atom x
         PD~U(0.2,1) x random phase + complex noise at 20 dB.
-* cfg2/3 shapes are provided for the parity tests at reduced size.
+* cfg2  256x256, T=1000 frames (same sequence generator), T1 100 x T2 100 (T2 < T1) x
+        dB0 21 values in -50..50 Hz (D = 120,624; SURVEY 8d grid proposal), SVD s = 20,
+        multi-shot EPI 16 of 256 lines per frame (``make_epi_pattern``), 30 dB.  Large enough
+        that the Bloch simulation, the Gram SVD and the measurement FFT run on the GPU
+        (``make_cfg2(device=...)``; same recurrences as the host code, fp64).
 """
 
 from __future__ import annotations
@@ -23,7 +27,8 @@ import numpy as np
 from .dictionary import CompressedDictionary, Dictionary, svd_compress
 
 __all__ = ["sequence_schedule", "bloch_irbssfp", "cfg0_dictionary", "Cfg0", "make_cfg0",
-           "random_atoms", "cone_voxels", "make_cfg1", "random_line_pattern"]
+           "random_atoms", "cone_voxels", "make_cfg1", "random_line_pattern", "make_cfg2",
+           "bloch_irbssfp_torch"]
 
 
 def sequence_schedule(L: int, seed: int = 0):
@@ -179,3 +184,99 @@ def make_cfg1(N: int = 1 << 20, D: int = 1 << 17, s: int = 10, dtype=np.complex6
     atoms = random_atoms(D, s, seed=0)
     Z, gen = cone_voxels(atoms, N, seed=1, dtype=dtype)
     return atoms, Z, gen
+
+
+# ---------------------------------------------------------------- cfg2 (GPU-generated)
+def bloch_irbssfp_torch(params, alpha, tr, device):
+    """``bloch_irbssfp`` on the GPU (torch fp64, identical recurrence).  Returns (d, L)
+    complex128 device tensor."""
+    import torch
+    p = torch.as_tensor(np.atleast_2d(np.asarray(params, dtype=float)), device=device)
+    t1, t2, b0 = p[:, 0], p[:, 1], p[:, 2]
+    d, L = p.shape[0], len(alpha)
+    mx = torch.zeros(d, dtype=torch.float64, device=device)
+    my = torch.zeros_like(mx)
+    mz = -torch.ones_like(mx)
+    out = torch.empty((d, L), dtype=torch.complex128, device=device)
+    for t in range(L):
+        tau = float(tr[t]) / 2.0
+        e1, e2 = torch.exp(-tau / t1), torch.exp(-tau / t2)
+        phi = 2.0 * np.pi * b0 * tau / 1000.0
+        c, sn = torch.cos(phi), torch.sin(phi)
+        a = float(alpha[t]) * (1.0 if t % 2 == 0 else -1.0)
+        ca, sa = np.cos(a), np.sin(a)
+        my, mz = ca * my + sa * mz, -sa * my + ca * mz
+        mx, my = e2 * (c * mx - sn * my), e2 * (sn * mx + c * my)
+        mz = e1 * mz + (1.0 - e1)
+        sign = 1.0 if t % 2 == 0 else -1.0
+        out[:, t] = torch.complex(sign * mx, sign * my)
+        mx, my = e2 * (c * mx - sn * my), e2 * (sn * mx + c * my)
+        mz = e1 * mz + (1.0 - e1)
+    return out
+
+
+@dataclass
+class Cfg2:
+    cdict: CompressedDictionary
+    pattern: np.ndarray          # (L, m)
+    spatial_shape: tuple
+    Y: np.ndarray                # (m, L) reference layout, complex64
+    d: int
+    setup_seconds: float
+
+
+def make_cfg2(h=256, w=256, L=1000, s=20, lines=16, snr_db=30.0, n_t1=100, n_t2=100,
+              n_b0=21, classes=6, device=None) -> Cfg2:
+    """BASELINE configs[2]: 2-D IPG with an off-resonance dictionary (GPU-generated)."""
+    import time
+
+    import torch
+
+    from .forward_model import make_epi_pattern
+    t0 = time.perf_counter()
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    alpha, tr = sequence_schedule(L, seed=0)
+    t1 = np.geomspace(100.0, 5000.0, n_t1)
+    t2 = np.geomspace(50.0, 5000.0, n_t2)
+    b0 = np.linspace(-50.0, 50.0, n_b0)
+    g1, g2, g3 = np.meshgrid(t1, t2, b0, indexing="ij")
+    triples = np.stack([g1.ravel(), g2.ravel(), g3.ravel()], axis=1)
+    triples = triples[triples[:, 1] < triples[:, 0]]
+    raw = bloch_irbssfp_torch(triples, alpha, tr, dev)
+    raw /= torch.linalg.vector_norm(raw, dim=1, keepdim=True)
+    # dictionary.py:176-183 large-d route: second-moment matrix, eigh, top-s (conjugated)
+    gram = (raw.transpose(0, 1) @ raw.conj()).cpu().numpy()
+    _, vecs = np.linalg.eigh(gram)
+    basis = np.ascontiguousarray(vecs[:, ::-1][:, :s].conj())
+    comp = raw @ torch.from_numpy(basis).to(dev)
+    factors = torch.linalg.vector_norm(comp, dim=1)
+    atoms_c = (comp / factors[:, None]).cpu().numpy()
+    parent = Dictionary(atoms=np.zeros((len(triples), 1)), norms=None, lookup_table=triples,
+                        tr_ms=float(np.mean(tr)), L=L)
+    cd = CompressedDictionary(basis=basis, atoms_compressed=atoms_c,
+                              renorm_factors=factors.cpu().numpy(), s=s, parent=parent)
+    # phantom: `classes` horizontal bands inside a background border, one atom per class
+    rng = np.random.default_rng(1)
+    rr, cc = np.mgrid[0:h, 0:w]
+    bd = max(1, min(h, w) // 16)
+    inside = (rr >= bd) & (rr < h - bd) & (cc >= bd) & (cc < w - bd)
+    lab = np.where(inside, 1 + (rr * classes) // h, 0).ravel()
+    class_atoms = rng.integers(len(triples), size=classes + 1)
+    pd = np.where(lab > 0, rng.uniform(0.5, 1.0, size=h * w), 0.0)
+    idx = torch.as_tensor(class_atoms[lab], device=dev)
+    gt = torch.as_tensor(pd, device=dev)[:, None] * raw[idx]          # (n, L) complex128
+    del raw
+    pat = make_epi_pattern((h, w), lines, L)
+    pattern = np.asarray(pat.indices)
+    F = torch.fft.fft2(gt.reshape(h, w, L), dim=(0, 1), norm="ortho").reshape(h * w, L)
+    del gt
+    Y0 = torch.gather(F, 0, torch.as_tensor(pattern.T, device=dev))
+    del F
+    nrng = np.random.default_rng(3)
+    xi = nrng.standard_normal(Y0.shape) + 1j * nrng.standard_normal(Y0.shape)
+    Y0 = Y0.cpu().numpy()
+    xi *= np.linalg.norm(Y0) / np.linalg.norm(xi) * 10 ** (-snr_db / 20.0)
+    Y = (Y0 + xi).astype(np.complex64)
+    torch.cuda.empty_cache()
+    return Cfg2(cdict=cd, pattern=pattern, spatial_shape=(h, w), Y=Y, d=len(triples),
+                setup_seconds=time.perf_counter() - t0)

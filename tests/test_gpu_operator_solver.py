@@ -320,3 +320,13 @@ def test_coil_ipg_matches_reference_trace():
     assert np.all(np.abs(f[:k] - g["ipg_fidelity"][:k]) / g["ipg_fidelity"][:k] < 1e-3)
     assert np.mean(maps.t1 == g["ipg_t1"]) > 0.99
     assert rel(X, g["ipg_X"]) < 1e-3
+
+
+def test_bloch_torch_matches_host_simulation():
+    """cfg2's GPU dictionary generator runs the same recurrence as ``bloch_irbssfp``."""
+    from paper_1810_01967_b200 import workloads
+    alpha, tr = workloads.sequence_schedule(120, seed=0)
+    params = np.array([[800.0, 60.0, 0.0], [1500.0, 200.0, -30.0], [300.0, 100.0, 50.0]])
+    host = workloads.bloch_irbssfp(params, alpha, tr)
+    dev = workloads.bloch_irbssfp_torch(params, alpha, tr, "cuda").cpu().numpy()
+    np.testing.assert_allclose(dev, host, rtol=1e-12, atol=1e-14)
