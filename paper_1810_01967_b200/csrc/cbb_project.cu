@@ -583,6 +583,69 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
   }
 }
 
+// Overflow-list mode of the exhaustive scan: each listed voxel's dictionary is split into
+// kExhSplits atom ranges scanned by different warps (a short list still fills the GPU); the
+// per-range (best score, lowest index) partials are merged by exhaustive_finish_kernel.
+constexpr int kExhSplits = 16;
+
+template <int S>
+__global__ void __launch_bounds__(256) exhaustive_split_kernel(ZSource zs, DictView dv,
+                                                               const int* __restrict__ cnt,
+                                                               const int64_t* __restrict__ list,
+                                                               double2* __restrict__ partial) {
+  extern __shared__ double zsh[];  // 8 warps x 2s
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = dv.s;
+  double* zw = zsh + size_t(wid) * 2 * s;
+  const int64_t total = int64_t(*cnt) * kExhSplits;
+  const int64_t nw = int64_t(gridDim.x) * 8;
+  const int64_t span = (dv.d + kExhSplits - 1) / kExhSplits;
+  for (int64_t pr = int64_t(blockIdx.x) * 8 + wid; pr < total; pr += nw) {
+    const int64_t i = pr / kExhSplits;
+    const int k = int(pr - i * kExhSplits);
+    const int64_t v = list[i];
+    for (int c = lane; c < s; c += 32) {
+      const double2 z = load_z(zs, v, s, c);
+      zw[c] = z.x;
+      zw[s + c] = z.y;
+    }
+    __syncwarp();
+    double bs = -INFINITY;
+    int64_t best = INT64_MAX;
+    const int64_t lo = int64_t(k) * span, hi = lo + span < dv.d ? lo + span : dv.d;
+    for (int64_t j = lo + lane; j < hi; j += 32) {
+      const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
+      if (acc > bs) { bs = acc; best = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double obs = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+      if (obs > bs || (obs == bs && ob < best)) { bs = obs; best = ob; }
+    }
+    if (lane == 0) partial[pr] = make_double2(bs, __longlong_as_double(best));
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256) exhaustive_finish_kernel(DictView dv,
+                                                                const int* __restrict__ cnt,
+                                                                const int64_t* __restrict__ list,
+                                                                const double2* __restrict__ partial,
+                                                                ProjOut out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= *cnt) return;
+  double bs = -INFINITY;
+  int64_t best = INT64_MAX;
+  for (int k = 0; k < kExhSplits; ++k) {
+    const double2 p = partial[i * kExhSplits + k];
+    const int64_t j = __double_as_longlong(p.y);
+    if (p.x > bs || (p.x == bs && j < best)) { bs = p.x; best = j; }
+  }
+  if (best == INT64_MAX) best = 0;  // all-NaN row: np.argmax returns the first NaN -> 0
+  write_winner(out, dv, list[i], best, bs);
+}
+
 #ifdef CBB_TRACE
 // development tracing: per-tile clock64 stamps of CTA 0 (issuer: after b_full wait, after
 // commit; epilogue part warp q0: after t_full wait, after wait::ld)
@@ -1361,6 +1424,7 @@ struct ProjWs {
   int64_t* ovf_list;
   int* heavy_count;     // voxels with many tcgen05 chunk entries (warp rescoring)
   int64_t* heavy_list;
+  double2* exh_partial; // [n][kExhSplits] (score, index) of the split exhaustive scan
   double* nd_v;
   double* partial;
 };
@@ -1388,6 +1452,7 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   w.ovf_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   w.heavy_count = reinterpret_cast<int*>(take(16));
   w.heavy_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
+  w.exh_partial = reinterpret_cast<double2*>(take(size_t(n) * kExhSplits * sizeof(double2)));
   w.nd_v = reinterpret_cast<double*>(take(size_t(n) * 8));
   w.partial = reinterpret_cast<double*>(take(kReduceBlocks * 8));
   if (ws) *ws = w;
@@ -1503,6 +1568,27 @@ static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, c
 }
 
 template <int S>
+static int launch_exhaustive_list_s(int64_t n, const ZSource& zs, const DictView& dv,
+                                    const int* cnt, const int64_t* list, double2* partial,
+                                    const ProjOut& out, cudaStream_t st) {
+  const size_t shm = size_t(8) * 2 * dv.s * sizeof(double);
+  exhaustive_split_kernel<S><<<num_sms() * 8, 256, shm, st>>>(zs, dv, cnt, list, partial);
+  CBB_CUDA_TRY(cudaGetLastError());
+  exhaustive_finish_kernel<<<int((n + 255) / 256), 256, 0, st>>>(dv, cnt, list, partial, out);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+// exhaustive fp64 rescan of the overflow list (count on the device), dictionary split 16 ways
+static int launch_exhaustive_list(int64_t n, const ZSource& zs, const DictView& dv,
+                                  const int* cnt, const int64_t* list, double2* partial,
+                                  const ProjOut& out, cudaStream_t st) {
+  const int sp = s_pad_for(dv.s);
+  CBB_DISPATCH_S(sp, return launch_exhaustive_list_s<S_>(n, zs, dv, cnt, list, partial, out, st));
+  return kOk;
+}
+
+template <int S>
 static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
                           const ProjOut& o, cudaStream_t st) {
   rescore_fast_kernel<S><<<int((n + 255) / 256), 256, 0, st>>>(
@@ -1565,11 +1651,9 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
       if (rc) return rc;
       count_launches(2);
     }
-    count_launches(3);  // prologue, screening kernel, exhaustive rescan
-    {
-      rc = launch_exhaustive(n, zr, dv, w.ovf_count, w.ovf_list, o, st);
-      if (rc) return rc;
-    }
+    count_launches(4);  // prologue, screening kernel, exhaustive rescan (split + finish)
+    rc = launch_exhaustive_list(n, zr, dv, w.ovf_count, w.ovf_list, w.exh_partial, o, st);
+    if (rc) return rc;
   } else if (algo == 3) {
     if (zs.x != nullptr) {
       // materialise Z = X - mu G (same fp32 rounding as the prologue)
