@@ -1068,7 +1068,9 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
 // Zero voxels -> index 0 / gamma 0; overflowed candidate lists and non-finite voxels -> the
 // next stage's list (fp32 FFMA re-screen).
 constexpr int kRescoreWarps = 8;
-constexpr int kFastEntries = 8;   // thread-per-voxel rescoring up to this many chunk entries
+constexpr int kFastEntries = 2;   // thread-per-voxel rescoring up to this many surviving entries
+constexpr int kFastRead = 12;     // ... among at most this many recorded entries
+constexpr int kWarpAtoms = 32 * 32;  // per-warp atom list: one round of 32 chunk entries
 
 // Expand one chunk entry and rescore its flagged atoms (chunk mask: 6-atom groups).
 template <int S>
@@ -1121,7 +1123,17 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     ovf_list[atomicAdd(ovf_count, 1)] = v;
     return;
   }
-  if (cnt[0] + cnt[1] + cnt[2] > kFastEntries) {
+  const float thr = gmax - win;
+  bool heavy = cnt[0] + cnt[1] + cnt[2] > kFastRead;
+  if (!heavy) {  // entries inside the final (cross-part) window
+    int live = 0;
+#pragma unroll
+    for (int p = 0; p < kParts; ++p)
+      for (int c = 0; c < cnt[p]; ++c)
+        live += __int_as_float(cand[(int64_t(p) * kGCap + c) * n_pad + v].y) >= thr;
+    heavy = live > kFastEntries;
+  }
+  if (heavy) {
     heavy_list[atomicAdd(heavy_count, 1)] = v;
     return;
   }
@@ -1132,7 +1144,6 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     zr[k] = z.x;
     zi[k] = z.y;
   }
-  const float thr = gmax - win;
   int64_t best = INT64_MAX;
   double bs = -INFINITY;
 #pragma unroll
@@ -1154,10 +1165,12 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     ZSource zs, DictView dv, int64_t n_pad, const float* __restrict__ win_tc,
     const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
     int64_t* ovf_list, const int* heavy_count, const int64_t* heavy_list) {
-  extern __shared__ double zsh_all[];  // kRescoreWarps x 2s
+  extern __shared__ double zsh_all[];  // kRescoreWarps x 2s doubles, then the atom lists
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = dv.s;
   double* zsh = zsh_all + size_t(wid) * 2 * s;
+  int* alist = reinterpret_cast<int*>(zsh_all + size_t(kRescoreWarps) * 2 * s) +
+               size_t(wid) * kWarpAtoms;
   const int64_t nw = int64_t(gridDim.x) * kRescoreWarps;
   const int64_t nh = *heavy_count;
   for (int64_t h = int64_t(blockIdx.x) * kRescoreWarps + wid; h < nh; h += nw) {
@@ -1194,11 +1207,48 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     const int total = cnt[0] + cnt[1] + cnt[2];
     int64_t best = INT64_MAX;
     double bs = -INFINITY;
-    for (int e = lane; e < total; e += 32) {
-      const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
-      const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
-      const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
-      if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zsh, zsh + s, s, dv, best, bs);
+    // rounds of 32 entries: each lane expands its entry's flagged atoms into the warp's atom
+    // list (warp prefix sum of the counts), then the lanes score the list round-robin
+    for (int e0 = 0; e0 < total; e0 += 32) {
+      const int e = e0 + lane;
+      int64_t j0 = 0;
+      uint32_t mask = 0;
+      if (e < total) {
+        const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
+        const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
+        const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
+        if (__int_as_float(en.y) >= thr) {
+          j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
+          mask = uint32_t(en.x) >> kChunkShift;
+        }
+      }
+      // groups 0..4: 6 atoms, group 5: 2 atoms
+      const int na = 6 * __popc(mask & 0x1Fu) + 2 * ((mask >> 5) & 1u);
+      int off = na;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += y;
+      }
+      const int round_total = __shfl_sync(0xffffffffu, off, 31);
+      off -= na;
+      while (mask) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
+        for (int i = lo; i < hi; ++i) alist[off++] = int(j0 + i);
+      }
+      __syncwarp();
+      for (int a = lane; a < round_total; a += 32) {
+        const int64_t j = alist[a];
+        if (j >= dv.d) continue;
+        const double acc = dot_atom<S>(zsh, zsh + s, dv.atoms64 + j * s, s);
+        if (acc > bs || (acc == bs && j < best)) {
+          bs = acc;
+          best = j;
+        }
+      }
+      __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1595,7 +1645,7 @@ static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const D
       zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
       w.heavy_list);
   CBB_CUDA_TRY(cudaGetLastError());
-  const size_t shm = size_t(kRescoreWarps) * 2 * dv.s * sizeof(double);
+  const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) + kWarpAtoms * sizeof(int));
   rescore_warp_kernel<S><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
       zr, dv, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
       w.heavy_list);
