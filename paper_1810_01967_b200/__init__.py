@@ -20,7 +20,7 @@ __all__ = [
 ]
 
 
-_LAZY = ("forward_model", "solver", "distributed", "workloads")
+_LAZY = ("forward_model", "solver", "distributed", "workloads", "containers")
 
 
 def __getattr__(name):  # lazy: operator / solver / distributed pull in more modules

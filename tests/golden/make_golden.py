@@ -184,6 +184,18 @@ def coil_cases():
     return out
 
 
+def container_files():
+    """CBDICT01 / CBMEAS01 / EPI pattern JSON written by the reference's own savers."""
+    dct = workloads.cfg0_dictionary(L=12, n_t1=5, n_t2=6, seed=0)
+    rdict = ref_dict.Dictionary(atoms=dct.atoms, norms=dct.norms, lookup_table=dct.lookup_table,
+                                tr_ms=dct.tr_ms, L=dct.L)
+    ref_dict.save_dictionary(rdict, os.path.join(HERE, "small.cbdict"))
+    rng = np.random.default_rng(50)
+    Y = rng.standard_normal((24, 12)) + 1j * rng.standard_normal((24, 12))
+    ref_fm.save_measurements(Y, os.path.join(HERE, "small.cbmeas"))
+    ref_fm.save_pattern(ref_fm.make_epi_pattern((8, 8), 2, 12), os.path.join(HERE, "epi.json"))
+
+
 def cfg0_reference():
     """BASELINE configs[0] through the reference (20 iterations, s = 10)."""
     cfg = workloads.make_cfg0()
@@ -217,6 +229,8 @@ def main():
     if only:
         if "coils" in only:
             np.savez_compressed(os.path.join(HERE, "coils.npz"), **coil_cases())
+        if "containers" in only:
+            container_files()
         print("golden fixtures written to", HERE, only)
         return
     np.savez_compressed(os.path.join(HERE, "projection.npz"), **projection_cases())
@@ -225,6 +239,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "cfg0_reference.npz"), **cfg0_reference(),
                         numpy_version=np.array(np.__version__))
     np.savez_compressed(os.path.join(HERE, "coils.npz"), **coil_cases())
+    container_files()
     print("golden fixtures written to", HERE)
 
 
