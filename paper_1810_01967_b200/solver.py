@@ -252,6 +252,86 @@ class IpgState:
         return Xs if self.V is None else Xs @ self.V.conj().transpose(0, 1)
 
 
+def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
+    """The IPG iterations of solver.py:199-257 over a state object (``IpgState`` on one GPU,
+    ``sharded.ShardedIpgState`` across ranks).  Returns (trace, have_proj)."""
+    # X = 0: AX = 0, R = -w Y, obj = ||Y||_w^2
+    st.residual(0)
+    (obj,) = st.read(0)
+    trace = SolveTrace()
+    max_iters = 1 if config.mode == "tm" else config.max_iters
+    start = time.perf_counter()
+    trace.start = start
+    have_proj = False
+    for k in range(1, max_iters + 1):
+        t0 = time.perf_counter()
+        st.gradient()
+        mu = mu_base
+        shrinks = 0
+        fixed_pt = False
+        while True:                              # step_shrinkage, solver.py:116-144
+            st.project_step(mu, 1)
+            if config.fixed_step is not None:
+                (nd,) = st.read(1)
+                fixed_pt = nd == 0.0
+                break
+            st.apply_norm2(st.dX, 2)
+            nd, den = st.read(1, 2)
+            if nd == 0.0:
+                fixed_pt = True
+                break
+            ratio = math.inf if den == 0.0 else nd / den
+            if mu <= ratio:
+                break
+            mu /= config.zeta
+            shrinks += 1
+            if shrinks > config.max_shrink_per_iter:
+                raise SolverError(
+                    "step-size collapse: shrinkage exceeded "
+                    f"{config.max_shrink_per_iter} sub-iterations")
+        if on_iter is not None:
+            on_iter(k, st, mu, shrinks, fixed_pt)
+        if fixed_pt:
+            break
+        st.X, st.Xn = st.Xn, st.X
+        st.idx, st.idx_n = st.idx_n, st.idx
+        st.gam, st.gam_n = st.gam_n, st.gam
+        have_proj = True
+        st.apply(st.X, st.AX)
+        if k == 1 and config.fixed_step is None:   # kappa rescale, solver.py:220-230
+            st.norm2(st.AX, 3)
+            st.scaled_obj(1.0, 4)
+            (e2, obj_x) = st.read(3, 4)
+            e = math.sqrt(e2)
+            if e > 0.0:
+                kappa = y_norm / e
+                st.scaled_obj(kappa, 5)
+                (obj_k,) = st.read(5)
+                if obj_k <= obj_x:
+                    st.scale(st.X, kappa)
+                    st.scale(st.AX, kappa)
+                    st.gam.mul_(kappa)
+                    mu_base *= kappa
+        elif config.step_policy == "carry_over":
+            mu_base = mu
+        st.residual(0)
+        (new_obj,) = st.read(0)
+        if not math.isfinite(new_obj):
+            raise SolverError(f"non-finite fidelity at iteration {k}: {new_obj}")
+        nmse = None
+        if gt_t is not None:
+            nmse = float(torch.linalg.vector_norm(st.decompress(st.X) - gt_t)) / gt_norm
+        trace.add(iter=k, fidelity=math.sqrt(new_obj), mu=mu, shrinks=shrinks, cost=n * d,
+                  nmse=nmse, seconds=time.perf_counter() - t0)
+        if obj > 0.0 and (obj - new_obj) / obj < config.rel_tol:
+            obj = new_obj
+            break
+        obj = new_obj
+        if obj == 0.0:
+            break
+    return trace, have_proj
+
+
 def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_device=False):
     """Device IPG loop following solver.py:155-257."""
     Ynp = np.asarray(Y, dtype=complex)
@@ -279,81 +359,10 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
             gt_data = gt.data if hasattr(gt, "data") and not isinstance(gt, np.ndarray) else gt
             gt_t = torch.from_numpy(np.ascontiguousarray(gt_data, dtype=np.complex64)).to(dev)
             gt_norm = float(np.linalg.norm(gt_data))
-        # X = 0: AX = 0, R = -w Y, obj = ||Y||_w^2
-        st.residual(0)
-        (obj,) = st.read(0)
-        trace = SolveTrace()
-        max_iters = 1 if config.mode == "tm" else config.max_iters
-        start = time.perf_counter()
-        have_proj = False
-        for k in range(1, max_iters + 1):
-            t0 = time.perf_counter()
-            st.gradient()
-            mu = mu_base
-            shrinks = 0
-            fixed_pt = False
-            while True:                              # step_shrinkage, solver.py:116-144
-                st.project_step(mu, 1)
-                if config.fixed_step is not None:
-                    (nd,) = st.read(1)
-                    fixed_pt = nd == 0.0
-                    break
-                st.apply_norm2(st.dX, 2)
-                nd, den = st.read(1, 2)
-                if nd == 0.0:
-                    fixed_pt = True
-                    break
-                ratio = math.inf if den == 0.0 else nd / den
-                if mu <= ratio:
-                    break
-                mu /= config.zeta
-                shrinks += 1
-                if shrinks > config.max_shrink_per_iter:
-                    raise SolverError(
-                        "step-size collapse: shrinkage exceeded "
-                        f"{config.max_shrink_per_iter} sub-iterations")
-            if on_iter is not None:
-                on_iter(k, st, mu, shrinks, fixed_pt)
-            if fixed_pt:
-                break
-            st.X, st.Xn = st.Xn, st.X
-            st.idx, st.idx_n = st.idx_n, st.idx
-            st.gam, st.gam_n = st.gam_n, st.gam
-            have_proj = True
-            st.apply(st.X, st.AX)
-            if k == 1 and config.fixed_step is None:   # kappa rescale, solver.py:220-230
-                st.norm2(st.AX, 3)
-                st.scaled_obj(1.0, 4)
-                (e2, obj_x) = st.read(3, 4)
-                e = math.sqrt(e2)
-                if e > 0.0:
-                    kappa = y_norm / e
-                    st.scaled_obj(kappa, 5)
-                    (obj_k,) = st.read(5)
-                    if obj_k <= obj_x:
-                        st.scale(st.X, kappa)
-                        st.scale(st.AX, kappa)
-                        st.gam.mul_(kappa)
-                        mu_base *= kappa
-            elif config.step_policy == "carry_over":
-                mu_base = mu
-            st.residual(0)
-            (new_obj,) = st.read(0)
-            if not math.isfinite(new_obj):
-                raise SolverError(f"non-finite fidelity at iteration {k}: {new_obj}")
-            nmse = None
-            if gt_t is not None:
-                nmse = float(torch.linalg.vector_norm(st.decompress(st.X) - gt_t)) / gt_norm
-            trace.add(iter=k, fidelity=math.sqrt(new_obj), mu=mu, shrinks=shrinks, cost=n * d,
-                      nmse=nmse, seconds=time.perf_counter() - t0)
-            if obj > 0.0 and (obj - new_obj) / obj < config.rel_tol:
-                obj = new_obj
-                break
-            obj = new_obj
-            if obj == 0.0:
-                break
+        trace, have_proj = _ipg_loop(st, config, mu_base, y_norm, gt_t,
+                                     gt_norm if gt_t is not None else None, n, d, on_iter)
         torch.cuda.current_stream(dev).synchronize()
-        trace.total_time = time.perf_counter() - start
+        trace.total_time = time.perf_counter() - trace.start
         if return_device:
             return st, trace
         idx = st.idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)

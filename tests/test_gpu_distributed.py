@@ -83,3 +83,31 @@ def test_project_atom_sharded_world1_nccl():
         np.testing.assert_allclose(proj.cpu().numpy(), ref.projected, rtol=1e-12, atol=1e-14)
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_solve_world1_nccl_matches_single_gpu_solve():
+    """The CUDA ShardedIpgState (NCCL collectives, frame-sharded s-channel operator, voxel
+    shards) against the one-GPU solve_compressed on a reduced cfg0 problem."""
+    import torch.distributed as dist
+    from paper_1810_01967_b200 import workloads
+    from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
+    from paper_1810_01967_b200.sharded import solve_compressed_sharded
+    from paper_1810_01967_b200.solver import SolverConfig, solve_compressed
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        cfg = workloads.make_cfg0(h=24, w=24, L=40, s=6, lines=6, n_t1=12, n_t2=12)
+        A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape))
+        conf = SolverConfig(mode="blip_exact", max_iters=6, zeta=2.0, compressed=6)
+        X1, maps1, gam1, tr1 = solve_compressed(cfg.Y, A, cfg.cdict, None, conf)
+        X2, maps2, gam2, tr2 = solve_compressed_sharded(cfg.Y, A, cfg.cdict, conf)
+        assert [r["shrinks"] for r in tr1.records] == [r["shrinks"] for r in tr2.records]
+        np.testing.assert_allclose([r["mu"] for r in tr2.records],
+                                   [r["mu"] for r in tr1.records], rtol=1e-6)
+        np.testing.assert_allclose(tr2.fidelities(), tr1.fidelities(), rtol=1e-5)
+        np.testing.assert_array_equal(maps2.t1, maps1.t1)
+        assert np.linalg.norm(X2 - X1) <= 1e-5 * np.linalg.norm(X1)
+    finally:
+        dist.destroy_process_group()

@@ -101,7 +101,7 @@ def test_tc_debug_scores_match_f16_emulation():
             # bit-exact except rare 1-ulp flips where the tensor core's internal (aligned,
             # finite-width) K=16 sum is not exact under heavy cancellation
             # (a flip in an intermediate accumulator propagates: compare with its ulp)
-            ulp = (kp // 16) * np.spacing(peak.astype(np.float16)).astype(np.float64)
+            ulp = (kp // 16) * 2.0 ** (np.floor(np.log2(np.maximum(peak, 2.0 ** -14))) - 10)
             flips = got != exp
             assert flips.mean() < 1e-3, (s, at, bt, flips.sum())
             assert np.all(np.abs(got - exp)[flips] <= ulp[flips]), (s, at, bt)
