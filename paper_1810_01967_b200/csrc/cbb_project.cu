@@ -183,6 +183,21 @@ __device__ __noinline__ int gcand_compact(int2* base, int64_t stride, int cnt, f
   return k;
 }
 
+// Move the live shared entries of one list to its global list (compacting that first if
+// needed).  Plain values in and out (no struct by reference): the caller's list state stays in
+// registers.  Returns the new global count, or -1 on overflow.
+__device__ __noinline__ int hcand_spill(const int* cj, const float* cs, int stride, int cnt,
+                                        int2* gbase, int64_t gstride, int gcnt, float thr) {
+  int live = 0;
+  for (int c = 0; c < cnt; ++c) live += cs[c * stride] >= thr;
+  if (gcnt + live > kGCap) gcnt = gcand_compact(gbase, gstride, gcnt, thr);
+  if (gcnt + live > kGCap) return -1;
+  for (int c = 0; c < cnt; ++c)
+    if (cs[c * stride] >= thr)
+      gbase[(gcnt++) * gstride] = make_int2(cj[c * stride], __float_as_int(cs[c * stride]));
+  return gcnt;
+}
+
 struct HCandList {
   int* cj;           // shared-memory list, column layout [kCandCap][stride]
   float* cs;
@@ -193,27 +208,17 @@ struct HCandList {
   int gcnt;
   bool ovf;
 
-  __device__ __noinline__ void spill(float thr) {
-    // move the live shared entries to the global list (compacting it first if needed)
-    int live = 0;
-    for (int c = 0; c < cnt; ++c) live += cs[c * stride] >= thr;
-    if (gcnt + live > kGCap) gcnt = gcand_compact(gbase, gstride, gcnt, thr);
-    if (gcnt + live > kGCap) {
-      ovf = true;
-      return;
-    }
-    for (int c = 0; c < cnt; ++c)
-      if (cs[c * stride] >= thr)
-        gbase[(gcnt++) * gstride] = make_int2(cj[c * stride], __float_as_int(cs[c * stride]));
-    cnt = 0;
-  }
-
   __device__ __forceinline__ void insert(int j, float sc, float thr) {
     if (cnt == kCandCap) {
       cnt = cand_compact(cj, cs, stride, thr);
       if (cnt == kCandCap) {
-        spill(thr);
-        if (ovf) return;
+        const int g = hcand_spill(cj, cs, stride, cnt, gbase, gstride, gcnt, thr);
+        if (g < 0) {
+          ovf = true;
+          return;
+        }
+        gcnt = g;
+        cnt = 0;
       }
     }
     cs[cnt * stride] = sc;
@@ -927,7 +932,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
       if (lane == 0) CBB_STAMP(4, kk);
-      mbar_wait_sleep(b_full + st, ph);
+      mbar_wait(b_full + st, ph);
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
@@ -1008,7 +1013,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
       for (; kk < kend; kk += kParts) {
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-        mbar_wait_sleep(t_full + tb, ph);
+        mbar_wait(t_full + tb, ph);
         tc_fence_after();
         if (q == 0 && lane == 0) CBB_STAMP(2, kk);
         uint32_t r[16 * C::kChunks];
