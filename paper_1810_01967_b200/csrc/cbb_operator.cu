@@ -176,40 +176,31 @@ __global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict_
 }
 
 // K[(ci*s + k)*n + w] = sum over the pattern entries e = t*m + i with Omega_t(i) = w (CSR,
-// ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per k-space location; unsampled
-// locations get 0 (the zero-fill of forward_model.py:160-162).
-template <int SMAX>
-__global__ void __launch_bounds__(128) kspace_s_kernel(const float2* __restrict__ R,
+// ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per (k-space location, channel k):
+// unsampled locations get 0 (the zero-fill of forward_model.py:160-162).
+__global__ void __launch_bounds__(256) kspace_s_kernel(const float2* __restrict__ R,
                                                        const int* __restrict__ csr_off,
                                                        const int64_t* __restrict__ csr_e,
                                                        int64_t n, int m, int c, int s,
                                                        const float2* __restrict__ V,
                                                        float2* __restrict__ K) {
-  const int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (wloc >= n) return;
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n * s) return;
+  const int k = int(g / n);
+  const int64_t wloc = g - int64_t(k) * n;  // consecutive threads: consecutive locations
   const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
   const int64_t cm = int64_t(c) * m;
   for (int ci = 0; ci < c; ++ci) {
-    float2 acc[SMAX];
-#pragma unroll
-    for (int k = 0; k < SMAX; ++k) acc[k] = make_float2(0.f, 0.f);
+    float2 acc = make_float2(0.f, 0.f);
     for (int j = b; j < e_end; ++j) {
       const int64_t e = csr_e[j];
       const int64_t t = e / m, i = e - t * m;
       const float2 r = R[t * cm + int64_t(ci) * m + i];
-      const float2* vt = V + t * s;
-#pragma unroll
-      for (int k = 0; k < SMAX; ++k) {
-        if (k < s) {
-          const float2 v = vt[k];
-          acc[k].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[k].x));
-          acc[k].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[k].y));
-        }
-      }
+      const float2 v = V[t * s + k];
+      acc.x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc.x));
+      acc.y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc.y));
     }
-#pragma unroll
-    for (int k = 0; k < SMAX; ++k)
-      if (k < s) K[(int64_t(ci) * s + k) * n + wloc] = acc[k];
+    K[(int64_t(ci) * s + k) * n + wloc] = acc;
   }
 }
 
@@ -548,15 +539,8 @@ int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float
                           cudaStream_t st) {
   if (s < 1 || s > 32) return kErrUnsupported;
   float2* K = ws_frames(ws);
-  const unsigned g = unsigned((op->n + 127) / 128);
-  if (s <= 8)
-    kspace_s_kernel<8><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V, K);
-  else if (s <= 16)
-    kspace_s_kernel<16><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V,
-                                            K);
-  else
-    kspace_s_kernel<32><<<g, 128, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V,
-                                            K);
+  kspace_s_kernel<<<unsigned((op->n * s + 255) / 256), 256, 0, st>>>(
+      R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V, K);
   CBB_CUDA_TRY(cudaGetLastError());
   int rc = fft_channels(op, K, op->c * s, CUFFT_INVERSE, st);
   if (rc) return rc;

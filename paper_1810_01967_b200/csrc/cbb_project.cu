@@ -1106,7 +1106,7 @@ template <int S>
 __global__ void __launch_bounds__(256) rescore_fast_kernel(
     ZSource zs, DictView dv, int64_t n, int64_t n_pad, const float* __restrict__ win_tc,
     const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
-    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list) {
+    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list, int fast_entries) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const float win = win_tc[v];
@@ -1129,14 +1129,14 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     return;
   }
   const float thr = gmax - win;
-  bool heavy = cnt[0] + cnt[1] + cnt[2] > kFastRead;
+  bool heavy = fast_entries == 0 || cnt[0] + cnt[1] + cnt[2] > kFastRead;
   if (!heavy) {  // entries inside the final (cross-part) window
     int live = 0;
 #pragma unroll
     for (int p = 0; p < kParts; ++p)
       for (int c = 0; c < cnt[p]; ++c)
         live += __int_as_float(cand[(int64_t(p) * kGCap + c) * n_pad + v].y) >= thr;
-    heavy = live > kFastEntries;
+    heavy = live > fast_entries;
   }
   if (heavy) {
     heavy_list[atomicAdd(heavy_count, 1)] = v;
@@ -1646,9 +1646,12 @@ static int launch_exhaustive_list(int64_t n, const ZSource& zs, const DictView& 
 template <int S>
 static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
                           const ProjOut& o, cudaStream_t st) {
+  // small projections: too few threads for the thread-per-voxel path to hide L2 latency, every
+  // voxel goes to the warp kernel
+  const int fast = n >= int64_t(num_sms()) * 256 ? kFastEntries : 0;
   rescore_fast_kernel<S><<<int((n + 255) / 256), 256, 0, st>>>(
       zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
-      w.heavy_list);
+      w.heavy_list, fast);
   CBB_CUDA_TRY(cudaGetLastError());
   const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) + kWarpAtoms * sizeof(int));
   rescore_warp_kernel<S><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
