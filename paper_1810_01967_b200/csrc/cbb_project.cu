@@ -99,6 +99,33 @@ __device__ __forceinline__ double dot_atom(const double* zr, const double* zi,
   return acc;
 }
 
+// Re<z, d_j> in fp32 from the planar fp32 atom copy ([re_0..re_{sp-1}, im_0..im_{sp-1}]); the
+// FFMA window win32 certifies it (any summation order).
+template <int S>
+__device__ __forceinline__ float dot_atom32(const float* zr, const float* zi,
+                                           const float* __restrict__ a, int s, int sp) {
+  float acc = 0.f;
+  if constexpr (S > 0 && S % 4 == 0) {
+    // 16-byte loads of the planar row (sp == S, rows 16-byte aligned); padding lanes are zero
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+#pragma unroll
+    for (int q = 0; q < S / 4; ++q) {
+      const float4 re = a4[q], im = a4[S / 4 + q];
+      acc = fmaf(zr[4 * q], re.x, fmaf(zi[4 * q], im.x, acc));
+      acc = fmaf(zr[4 * q + 1], re.y, fmaf(zi[4 * q + 1], im.y, acc));
+      acc = fmaf(zr[4 * q + 2], re.z, fmaf(zi[4 * q + 2], im.z, acc));
+      acc = fmaf(zr[4 * q + 3], re.w, fmaf(zi[4 * q + 3], im.w, acc));
+    }
+  } else if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (k < s) acc = fmaf(zr[k], a[k], fmaf(zi[k], a[sp + k], acc));
+  } else {
+    for (int k = 0; k < s; ++k) acc = fmaf(zr[k], a[k], fmaf(zi[k], a[sp + k], acc));
+  }
+  return acc;
+}
+
 __device__ void write_winner(const ProjOut& out, const DictView& dv, int64_t v, int64_t j,
                              double score) {
   const int s = dv.s;
@@ -1076,6 +1103,7 @@ constexpr int kRescoreWarps = 8;
 constexpr int kFastEntries = 2;   // thread-per-voxel rescoring up to this many surviving entries
 constexpr int kFastRead = 12;     // ... among at most this many recorded entries
 constexpr int kWarpAtoms = 32 * 32;  // per-warp atom list: one round of 32 chunk entries
+constexpr int kLaneSurv = 16;        // per-lane fp32-window survivors (atom, fp32 score)
 
 // Expand one chunk entry and rescore its flagged atoms (chunk mask: 6-atom groups).
 template <int S>
@@ -1168,14 +1196,20 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
 template <int S>
 __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     ZSource zs, DictView dv, int64_t n_pad, const float* __restrict__ win_tc,
-    const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
-    int64_t* ovf_list, const int* heavy_count, const int64_t* heavy_list) {
-  extern __shared__ double zsh_all[];  // kRescoreWarps x 2s doubles, then the atom lists
+    const float* __restrict__ win32, const int2* __restrict__ cand,
+    const int2* __restrict__ meta, ProjOut out, int* ovf_count, int64_t* ovf_list,
+    const int* heavy_count, const int64_t* heavy_list) {
+  // shared per warp: z (2s doubles), z (2s floats), the atom list, the lanes' fp32 survivors
+  extern __shared__ double zsh_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int s = dv.s;
+  const int s = dv.s, sp = dv.s_pad;
   double* zsh = zsh_all + size_t(wid) * 2 * s;
-  int* alist = reinterpret_cast<int*>(zsh_all + size_t(kRescoreWarps) * 2 * s) +
-               size_t(wid) * kWarpAtoms;
+  float* z32base = reinterpret_cast<float*>(zsh_all + size_t(kRescoreWarps) * 2 * s);
+  float* z32 = z32base + size_t(wid) * 2 * sp;                 // planar, zero-padded to sp
+  int* alist_base = reinterpret_cast<int*>(z32base + size_t(kRescoreWarps) * 2 * sp);
+  int* alist = alist_base + size_t(wid) * kWarpAtoms;
+  int2* surv = reinterpret_cast<int2*>(alist_base + size_t(kRescoreWarps) * kWarpAtoms) +
+               (size_t(wid) * 32 + lane) * kLaneSurv;
   const int64_t nw = int64_t(gridDim.x) * kRescoreWarps;
   const int64_t nh = *heavy_count;
   for (int64_t h = int64_t(blockIdx.x) * kRescoreWarps + wid; h < nh; h += nw) {
@@ -1206,12 +1240,25 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       const double2 z = load_z(zs, v, s, k);
       zsh[k] = z.x;
       zsh[s + k] = z.y;
+      z32[k] = float(z.x);
+      z32[sp + k] = float(z.y);
+    }
+    for (int k = s + lane; k < sp; k += 32) {
+      z32[k] = 0.f;
+      z32[sp + k] = 0.f;
     }
     __syncwarp();
     const float thr = gmax - win;
+    const float w32 = win32[v];
     const int total = cnt[0] + cnt[1] + cnt[2];
     int64_t best = INT64_MAX;
     double bs = -INFINITY;
+    // fp32 pre-filter (certified window w32): every lane keeps the atoms within w32 of its own
+    // running fp32 max (a superset of the final survivors); only those are rescored in fp64.
+    // A full lane list sends the voxel through the fp64 pass below instead.
+    float lmax = -INFINITY;
+    int nsurv = 0;
+    bool full = false;
     // rounds of 32 entries: each lane expands its entry's flagged atoms into the warp's atom
     // list (warp prefix sum of the counts), then the lanes score the list round-robin
     for (int e0 = 0; e0 < total; e0 += 32) {
@@ -1247,13 +1294,48 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       for (int a = lane; a < round_total; a += 32) {
         const int64_t j = alist[a];
         if (j >= dv.d) continue;
-        const double acc = dot_atom<S>(zsh, zsh + s, dv.atoms64 + j * s, s);
-        if (acc > bs || (acc == bs && j < best)) {
-          bs = acc;
-          best = j;
+        const float sc = dot_atom32<S>(z32, z32 + sp, dv.atoms32 + j * 2 * sp, s, sp);
+        lmax = fmaxf(lmax, sc);
+        if (sc >= lmax - w32) {
+          if (nsurv == kLaneSurv) {  // drop survivors the running max has since excluded
+            int k2 = 0;
+            for (int c = 0; c < kLaneSurv; ++c)
+              if (__int_as_float(surv[c].y) >= lmax - w32) surv[k2++] = surv[c];
+            nsurv = k2;
+          }
+          if (nsurv < kLaneSurv) surv[nsurv++] = make_int2(int(j), __float_as_int(sc));
+          else full = true;
         }
       }
       __syncwarp();
+    }
+    float gmax32 = lmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmax32 = fmaxf(gmax32, __shfl_xor_sync(0xffffffffu, gmax32, o));
+    const float thr32 = gmax32 - w32;
+    for (int c = 0; c < nsurv; ++c) {
+      const int2 e2 = surv[c];
+      if (__int_as_float(e2.y) < thr32) continue;
+      const int64_t j = e2.x;
+      const double acc = dot_atom<S>(zsh, zsh + s, dv.atoms64 + j * s, s);
+      if (acc > bs || (acc == bs && j < best)) {
+        bs = acc;
+        best = j;
+      }
+    }
+    if (__any_sync(0xffffffffu, full) || !(w32 >= 0.f)) {
+      // fp64 over every flagged atom (the pre-filter could not keep all its survivors)
+      best = INT64_MAX;
+      bs = -INFINITY;
+      for (int e0 = 0; e0 < total; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < total) {
+          const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
+          const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
+          const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
+          if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zsh, zsh + s, s, dv, best, bs);
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1653,10 +1735,16 @@ static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const D
       zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
       w.heavy_list, fast);
   CBB_CUDA_TRY(cudaGetLastError());
-  const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) + kWarpAtoms * sizeof(int));
+  const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) +
+                                               2 * dv.s_pad * sizeof(float) +
+                                               kWarpAtoms * sizeof(int) +
+                                               32 * kLaneSurv * sizeof(int2));
+  if (shm > 48 * 1024)
+    CBB_CUDA_TRY(cudaFuncSetAttribute(rescore_warp_kernel<S>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
   rescore_warp_kernel<S><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
-      zr, dv, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
-      w.heavy_list);
+      zr, dv, w.n_pad, w.win_tc, w.win32, w.cand, w.meta, o, w.ovf_count, w.ovf_list,
+      w.heavy_count, w.heavy_list);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
