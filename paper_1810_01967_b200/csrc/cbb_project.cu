@@ -620,15 +620,23 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
 // per-range (best score, lowest index) partials are merged by exhaustive_finish_kernel.
 constexpr int kExhSplits = 16;
 
+constexpr int kExhSurv = 8;  // per-lane fp32-window survivors in the split scan
+
 template <int S>
 __global__ void __launch_bounds__(256) exhaustive_split_kernel(ZSource zs, DictView dv,
                                                                const int* __restrict__ cnt,
                                                                const int64_t* __restrict__ list,
+                                                               const float* __restrict__ win32,
                                                                double2* __restrict__ partial) {
-  extern __shared__ double zsh[];  // 8 warps x 2s
+  // per warp: z (2s doubles), z (2 sp floats, zero-padded), lane survivor lists
+  extern __shared__ double zsh[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int s = dv.s;
+  const int s = dv.s, sp = dv.s_pad;
   double* zw = zsh + size_t(wid) * 2 * s;
+  float* z32 = reinterpret_cast<float*>(zsh + size_t(8) * 2 * s) + size_t(wid) * 2 * sp;
+  int2* surv = reinterpret_cast<int2*>(reinterpret_cast<float*>(zsh + size_t(8) * 2 * s) +
+                                       size_t(8) * 2 * sp) +
+               (size_t(wid) * 32 + lane) * kExhSurv;
   const int64_t total = int64_t(*cnt) * kExhSplits;
   const int64_t nw = int64_t(gridDim.x) * 8;
   const int64_t span = (dv.d + kExhSplits - 1) / kExhSplits;
@@ -640,14 +648,56 @@ __global__ void __launch_bounds__(256) exhaustive_split_kernel(ZSource zs, DictV
       const double2 z = load_z(zs, v, s, c);
       zw[c] = z.x;
       zw[s + c] = z.y;
+      z32[c] = float(z.x);
+      z32[sp + c] = float(z.y);
+    }
+    for (int c = s + lane; c < sp; c += 32) {
+      z32[c] = 0.f;
+      z32[sp + c] = 0.f;
     }
     __syncwarp();
+    const float w32 = win32[v];
     double bs = -INFINITY;
     int64_t best = INT64_MAX;
     const int64_t lo = int64_t(k) * span, hi = lo + span < dv.d ? lo + span : dv.d;
-    for (int64_t j = lo + lane; j < hi; j += 32) {
-      const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
-      if (acc > bs) { bs = acc; best = j; }
+    // fp32 pre-filter (certified window w32) with per-lane survivors; a full list or a
+    // non-finite voxel (w32 NaN) scans the slice in fp64 instead
+    bool full = !(w32 >= 0.f);
+    float lmax = -INFINITY;
+    int ns = 0;
+    if (!full) {
+      for (int64_t j = lo + lane; j < hi; j += 32) {
+        const float sc = dot_atom32<S>(z32, z32 + sp, dv.atoms32 + j * 2 * sp, s, sp);
+        lmax = fmaxf(lmax, sc);
+        if (sc >= lmax - w32) {
+          if (ns == kExhSurv) {
+            int k2 = 0;
+            for (int c = 0; c < kExhSurv; ++c)
+              if (__int_as_float(surv[c].y) >= lmax - w32) surv[k2++] = surv[c];
+            ns = k2;
+          }
+          if (ns < kExhSurv) surv[ns++] = make_int2(int(j), __float_as_int(sc));
+          else full = true;
+        }
+      }
+    }
+    float gmax32 = lmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmax32 = fmaxf(gmax32, __shfl_xor_sync(0xffffffffu, gmax32, o));
+    if (__any_sync(0xffffffffu, full)) {
+      for (int64_t j = lo + lane; j < hi; j += 32) {
+        const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
+        if (acc > bs) { bs = acc; best = j; }
+      }
+    } else {
+      const float thr32 = gmax32 - w32;
+      for (int c = 0; c < ns; ++c) {
+        const int2 e2 = surv[c];
+        if (__int_as_float(e2.y) < thr32) continue;
+        const int64_t j = e2.x;
+        const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
+        if (acc > bs || (acc == bs && j < best)) { bs = acc; best = j; }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1706,10 +1756,14 @@ static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, c
 
 template <int S>
 static int launch_exhaustive_list_s(int64_t n, const ZSource& zs, const DictView& dv,
-                                    const int* cnt, const int64_t* list, double2* partial,
-                                    const ProjOut& out, cudaStream_t st) {
-  const size_t shm = size_t(8) * 2 * dv.s * sizeof(double);
-  exhaustive_split_kernel<S><<<num_sms() * 8, 256, shm, st>>>(zs, dv, cnt, list, partial);
+                                    const int* cnt, const int64_t* list, const float* win32,
+                                    double2* partial, const ProjOut& out, cudaStream_t st) {
+  const size_t shm = size_t(8) * (2 * dv.s * sizeof(double) + 2 * dv.s_pad * sizeof(float) +
+                                  32 * kExhSurv * sizeof(int2));
+  if (shm > 48 * 1024)
+    CBB_CUDA_TRY(cudaFuncSetAttribute(exhaustive_split_kernel<S>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
+  exhaustive_split_kernel<S><<<num_sms() * 8, 256, shm, st>>>(zs, dv, cnt, list, win32, partial);
   CBB_CUDA_TRY(cudaGetLastError());
   exhaustive_finish_kernel<<<int((n + 255) / 256), 256, 0, st>>>(dv, cnt, list, partial, out);
   CBB_CUDA_TRY(cudaGetLastError());
@@ -1718,10 +1772,11 @@ static int launch_exhaustive_list_s(int64_t n, const ZSource& zs, const DictView
 
 // exhaustive fp64 rescan of the overflow list (count on the device), dictionary split 16 ways
 static int launch_exhaustive_list(int64_t n, const ZSource& zs, const DictView& dv,
-                                  const int* cnt, const int64_t* list, double2* partial,
-                                  const ProjOut& out, cudaStream_t st) {
+                                  const int* cnt, const int64_t* list, const float* win32,
+                                  double2* partial, const ProjOut& out, cudaStream_t st) {
   const int sp = s_pad_for(dv.s);
-  CBB_DISPATCH_S(sp, return launch_exhaustive_list_s<S_>(n, zs, dv, cnt, list, partial, out, st));
+  CBB_DISPATCH_S(sp, return launch_exhaustive_list_s<S_>(n, zs, dv, cnt, list, win32, partial,
+                                                         out, st));
   return kOk;
 }
 
@@ -1798,7 +1853,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
       count_launches(2);
     }
     count_launches(4);  // prologue, screening kernel, exhaustive rescan (split + finish)
-    rc = launch_exhaustive_list(n, zr, dv, w.ovf_count, w.ovf_list, w.exh_partial, o, st);
+    rc = launch_exhaustive_list(n, zr, dv, w.ovf_count, w.ovf_list, w.win32, w.exh_partial, o,
+                                st);
     if (rc) return rc;
   } else if (algo == 3) {
     if (zs.x != nullptr) {
