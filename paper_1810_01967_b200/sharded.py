@@ -33,7 +33,7 @@ from . import _lib
 from .dictionary import device_dictionary
 from .distributed import shard_range
 from .forward_model import ForwardOperator, SamplingPattern, as_device_operator
-from .solver import IpgState, SolverError, _ipg_loop, _maps_from
+from .solver import IpgState, SolverError, _image_to_host, _ipg_loop, _maps_from
 
 __all__ = ["ShardComm", "ShardedIpgState", "solve_compressed_sharded"]
 
@@ -209,5 +209,5 @@ def solve_compressed_sharded(Y, A, cdict, config, gt=None, group=None, on_iter=N
         idx = idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
         gam = gam.cpu().numpy() if have_proj else np.zeros(n)
         maps = _maps_from(cdict, idx, gam)
-        out = (Xs @ st.V_full.conj().transpose(0, 1)).cpu().numpy().astype(np.complex128)
+        out = _image_to_host(Xs @ st.V_full.conj().transpose(0, 1))
         return out, maps, gam, trace

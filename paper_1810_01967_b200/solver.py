@@ -252,6 +252,16 @@ class IpgState:
         return Xs if self.V is None else Xs @ self.V.conj().transpose(0, 1)
 
 
+def _image_to_host(X: torch.Tensor) -> np.ndarray:
+    """(n, L) device image -> complex128 numpy (the reference's return type): upcast on the
+    GPU, one D2H into a pinned buffer (torch's caching host allocator reuses it)."""
+    Xd = X.to(torch.complex128)
+    host = torch.empty(Xd.shape, dtype=torch.complex128, pin_memory=True)
+    host.copy_(Xd, non_blocking=True)
+    torch.cuda.current_stream(X.device).synchronize()
+    return host.numpy()
+
+
 def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
     """The IPG iterations of solver.py:199-257 over a state object (``IpgState`` on one GPU,
     ``sharded.ShardedIpgState`` across ranks).  Returns (trace, have_proj)."""
@@ -368,7 +378,7 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
         idx = st.idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
         gam = st.gam.cpu().numpy() if have_proj else np.zeros(n)
         maps = _maps_from(dictionary, idx, gam)
-        out = st.decompress(st.X).cpu().numpy().astype(np.complex128)
+        out = _image_to_host(st.decompress(st.X))
         return out, maps, gam, trace
 
 
