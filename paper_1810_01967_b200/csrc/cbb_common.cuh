@@ -40,8 +40,8 @@ void count_launches(int k);                    // kernels enqueued by this libra
 void timing_mark(int which, cudaStream_t st);  // 0 = before / 1 = after the matched filter
 
 // ---------------------------------------------------------------- layout
-// Tensor-core operand rows: K_PAD fp16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, 0.., sentinel]
-// with 2s < K_PAD: the last column is the padding sentinel (voxel rows 1.0, real atoms 0, the
+// Tensor-core operand rows: K_PAD fp16 per row = [re_0..re_{s-1}, im_0..im_{s-1}, sentinel, 0..]
+// with 2s < K_PAD: column 2s is the padding sentinel (voxel rows 1.0, real atoms 0, the
 // zero-padded atom rows of the last tile -65504 so they can never win or enter a window).
 // stored in 128-row tiles with the UMMA K-major SWIZZLE_64B (K_PAD=32) or
 // SWIZZLE_128B (K_PAD=64) canonical layout so a flat bulk copy lands a tile in
@@ -49,6 +49,9 @@ void timing_mark(int which, cudaStream_t st);  // 0 = before / 1 = after the mat
 constexpr int kTileRows = 128;
 
 __host__ __device__ inline int kpad_for(int s) { return (2 * s < 32) ? 32 : 64; }
+// K = 16 MMA steps that carry data: columns [0, 2s) plus the sentinel at column 2s (the steps
+// after it multiply zeros only and are skipped)
+__host__ __device__ inline int mma_ksteps(int s) { return (2 * s + 1 + 15) / 16; }
 constexpr unsigned short kF16One = 0x3C00, kF16MinusMax = 0xFBFF;  // 1.0, -65504
 
 // Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.

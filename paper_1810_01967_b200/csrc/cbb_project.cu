@@ -368,7 +368,7 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
   if (j >= d_pad) return;
   const int tile = int(j / kTileRows), r = int(j % kTileRows);
   uint8_t* trow = atoms_tc + size_t(tile) * kTileRows * kpad * 2;
-  const int e_sent = kpad - 1;
+  const int e_sent = 2 * s;  // sentinel right after the data: nq = ceil((2s+1)/16) K-steps
   if (j >= d) {  // zero-padded row of the last tile: sentinel score -65504 for every voxel
     *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_sent >> 3, kpad) +
                                        (e_sent & 7) * 2) = kF16MinusMax;
@@ -491,7 +491,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     eh += (re - fre) * (re - fre) + (im - fim) * (im - fim);
     nzh += fre * fre + fim * fim;
   }
-  row[kpad - 1] = kF16One;  // sentinel column (2s < kpad)
+  row[2 * s] = kF16One;  // sentinel column right after the data (2s < kpad)
   for (int c = 0; c < kpad / 8; ++c) {
     uint4 pk;
     pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
@@ -501,7 +501,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     *reinterpret_cast<uint4*>(trow + c * 16) = pk;
   }
   const double sd = bounds[kBScaleD], dh = bounds[kBDhMax], delh = bounds[kBDeltaH];
-  const double nq = double(kpad / 16);
+  const double nq = double(mma_ksteps(s));  // fp16 roundings of nonzero partial sums
   const double acc_tc = nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
   const double eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh +
                     nq * 0x1p-24;
@@ -995,6 +995,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   } else if (warp >= 1 && warp <= kParts) {
     // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
     const int me = warp - 1;
+    const int nks = mma_ksteps(dv.s);
     const uint32_t b_base = smem_u32(smem + C::kOffB);
     int sacc = me;  // accumulator stage kk % kAcc
     int tb = me;    // completion barrier kk % kTBars
@@ -1018,8 +1019,9 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq)
-          tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * kq), C::kIdesc,
-                        kq > 0 ? 1u : 0u);
+          if (kq < nks)
+            tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * kq), C::kIdesc,
+                          kq > 0 ? 1u : 0u);
         tc_commit(b_empty + st);
         tc_commit(t_full + tb);
         // this issuer's last tile of the voxel tile: A buffer recyclable once it retires

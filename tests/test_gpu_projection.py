@@ -88,8 +88,8 @@ def test_tc_debug_scores_match_f16_emulation():
         zr[:300, :2 * s] = np.concatenate([Z.real, Z.imag], 1) * sv[:, None]
         ar = np.zeros((384, kp))
         ar[:300, :2 * s] = np.concatenate([atoms.real, atoms.imag], 1) * sd
-        zr[:300, kp - 1] = 1.0        # sentinel column: voxel rows 1,
-        ar[300:, kp - 1] = -65504.0   # zero-padded atom rows of the last tile -65504
+        zr[:300, 2 * s] = 1.0         # sentinel column right after the data: voxel rows 1,
+        ar[300:, 2 * s] = -65504.0    # zero-padded atom rows of the last tile -65504
         zh, ah = zr.astype(np.float16), ar.astype(np.float16)
         assert np.all(np.isfinite(zh)) and np.abs(zh).max() < 2.0 ** 13
         for at, bt in ((0, 0), (1, 2), (2, 1)):
@@ -108,7 +108,8 @@ def test_tc_debug_scores_match_f16_emulation():
             # and the accumulation error stays inside the certified acc term
             z64 = zh[at * 128:(at + 1) * 128].astype(np.float64)
             a64 = ah[bt * 128:(bt + 1) * 128].astype(np.float64)
-            bound = (kp // 16) * 2.0 ** -11 * 1.002 * np.outer(np.linalg.norm(z64, axis=1),
+            nks = (2 * s + 1 + 15) // 16    # K-steps that carry data (the production kernel)
+            bound = nks * 2.0 ** -11 * 1.002 * np.outer(np.linalg.norm(z64, axis=1),
                                                              np.linalg.norm(a64, axis=1))
             assert np.all(np.abs(got - z64 @ a64.T) <= bound + 2.0 ** -24)
 
