@@ -84,11 +84,13 @@ int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_d
                            int32_t proj_c128, void* workspace, size_t workspace_bytes,
                            int32_t algo, void* stream);
 /* One IPG trial (solver.py:128-130): Z = X - mu*G (c64, written to z_out), project,
- * X' = proj (c64), dX = X' - X (c64), nd_out[0] = ||dX||^2 (fp64, deterministic). */
+ * X' = proj (c64), dX = X' - X (c64), nd_out[0] = ||dX||^2 (fp64, deterministic).
+ * idx_hint (optional, int32 per voxel, e.g. the previous iterate's atoms): the hinted atom's
+ * exact score seeds the screening threshold (warm start; results are unchanged). */
 int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64_t n,
-                     const cbb_dict_view* dict, int32_t* idx_out, double* gamma_out,
-                     void* xnext_out, void* dx_out, double* nd_out, void* workspace,
-                     size_t workspace_bytes, int32_t algo, void* stream);
+                     const cbb_dict_view* dict, const int32_t* idx_hint, int32_t* idx_out,
+                     double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
+                     void* workspace, size_t workspace_bytes, int32_t algo, void* stream);
 /* Atom-sharded building block (multi-GPU): per voxel the shard-local exact argmax
  * reported as a GLOBAL atom index (local + atom_offset, int64) and its raw fp64 score
  * Re<z, d_j*> (not clipped at 0), for the cross-rank combine (cbb_argmax_select). */

@@ -46,7 +46,7 @@ SIGNATURES = {
     "cbb_project_cone_exact": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_i32,
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_step": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, ctypes.POINTER(DictView), c_vp,
-                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32, c_vp]),
+                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_best": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_i64, c_vp, c_vp,
                                  c_vp, c_size, c_i32, c_vp]),
     "cbb_scaled_rows": (c_int, [ctypes.POINTER(DictView), c_i64, c_vp, c_vp, c_i64, c_vp, c_i32,

@@ -135,7 +135,7 @@ int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_d
     set_last_error("cbb_project_cone_exact: null input");
     return kErrArgument;
   }
-  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr};
+  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr, nullptr};
   ProjOut o{idx_out, idx_int64, gamma_out, proj_out, proj_c128, nullptr, nullptr, nullptr,
             nullptr, 0};
   return project(zs, n, to_view(dict), o, nullptr, workspace, workspace_bytes, algo, 0,
@@ -150,7 +150,7 @@ int cbb_project_best(const void* z, int32_t z_c128, int64_t n, const cbb_dict_vi
     set_last_error("cbb_project_best: null argument");
     return kErrArgument;
   }
-  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr};
+  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr, nullptr};
   ProjOut o{idx_out, 1, nullptr, nullptr, 0, nullptr, nullptr, nullptr, score_out, atom_offset};
   return project(zs, n, to_view(dict), o, nullptr, workspace, workspace_bytes, algo, 0,
                  S(stream));
@@ -163,16 +163,16 @@ int cbb_scaled_rows(const cbb_dict_view* dict, int64_t atom_offset, const int64_
 }
 
 int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64_t n,
-                     const cbb_dict_view* dict, int32_t* idx_out, double* gamma_out,
-                     void* xnext_out, void* dx_out, double* nd_out, void* workspace,
-                     size_t workspace_bytes, int32_t algo, void* stream) {
+                     const cbb_dict_view* dict, const int32_t* idx_hint, int32_t* idx_out,
+                     double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
+                     void* workspace, size_t workspace_bytes, int32_t algo, void* stream) {
   if (int rc = check_view(dict)) return rc;
   if (n > 0 && (!x || !g || !z_out || !xnext_out || !dx_out)) {
     set_last_error("cbb_project_step: null argument");
     return kErrArgument;
   }
   ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), float(mu),
-             static_cast<float2*>(z_out)};
+             static_cast<float2*>(z_out), idx_hint};
   ProjOut o{idx_out, 0, gamma_out, xnext_out, 0, static_cast<const float2*>(x),
             static_cast<float2*>(dx_out), nullptr, nullptr, 0};
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));
@@ -193,7 +193,7 @@ int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dic
                          void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_view(dict)) return rc;
   if (workspace_bytes < project_ws_bytes(n, dict->s, nullptr, nullptr)) return kErrArgument;
-  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr};
+  ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr, nullptr};
   return prologue_only(zs, n, to_view(dict), workspace, S(stream));
 }
 

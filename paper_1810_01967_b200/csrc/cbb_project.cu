@@ -409,7 +409,8 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
 __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int kpad,
                                 const float* __restrict__ bounds, uint8_t* __restrict__ ztiles,
                                 float* __restrict__ win_tc, float* __restrict__ win32,
-                                int s_pad) {
+                                int s_pad, const double2* __restrict__ atoms64,
+                                int64_t d_atoms, float* __restrict__ init_tc) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
   // plain row-major fp16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
@@ -506,6 +507,23 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   const double eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh +
                     nq * 0x1p-24;
   win_tc[v] = __double2float_ru(2.0 * eb * 1.001 + 1e-30);
+  if (init_tc) {
+    // warm start: any atom's exact score lower-bounds the approximate maximum once the
+    // certified half-window is subtracted (s~_max >= s~_j >= s_j - eps), in scaled units
+    float init = -INFINITY;
+    const int64_t jh = zs.hint ? int64_t(zs.hint[v]) : -1;
+    if (jh >= 0 && jh < d_atoms) {
+      const double2* a = atoms64 + jh * s;
+      double acc = 0.0;
+      for (int k = 0; k < s; ++k) {
+        const double2 z = load_z(zs, v, s, k);
+        acc = fma(z.x, a[k].x, acc);
+        acc = fma(z.y, a[k].y, acc);
+      }
+      init = __double2float_rd(acc * sv * sd - eb * 1.001);
+    }
+    init_tc[v] = init;
+  }
 }
 
 // ============================================================== FFMA screening
@@ -928,8 +946,8 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
 template <int KP>
 __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
-                 const float* __restrict__ win_tc, DictView dv, int64_t n_pad,
-                 int2* __restrict__ cand, int2* __restrict__ meta) {
+                 const float* __restrict__ win_tc, const float* __restrict__ init_tc,
+                 DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta) {
   using C = TcCfg<KP>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -1087,8 +1105,11 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       bool active = live && win >= 0.f;
       HCandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0,
                    cand + int64_t(part) * kGCap * n_pad + (live ? v : 0), n_pad, 0, false};
-      __half runmax = __ushort_as_half(0xFC00);
-      __half thr = __ushort_as_half(active ? 0xFC00 : 0x7C00);
+      // running max seeded with the warm-start lower bound (-inf without a hint)
+      const float init = live ? fmaxf(init_tc[v], -65504.f) : -INFINITY;
+      __half runmax = active ? __float2half_rd(init) : __ushort_as_half(0xFC00);
+      __half thr = active ? __float2half_rd(__half2float(runmax) - win)
+                          : __ushort_as_half(0x7C00);
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
       for (; kk < kend; kk += kParts) {
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
@@ -1608,6 +1629,7 @@ struct ProjWs {
   int2* meta;      // [kParts][n_pad] (entry count or -1 on overflow, part running max)
   uint8_t* ztiles;
   float* win_tc;
+  float* init_tc;  // warm-start lower bound of each voxel's approximate max (scaled units)
   float* win32;
   int* ovf_count;       // tcgen05 / FFMA pass overflows (next stage's voxel list)
   int64_t* ovf_list;
@@ -1636,6 +1658,7 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * kGCap * sizeof(int2)));
   w.meta = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * sizeof(int2)));
   w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
+  w.init_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.ovf_count = reinterpret_cast<int*>(take(16));
   w.ovf_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
@@ -1673,8 +1696,8 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
-  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, dv,
-                                                        w.n_pad, w.cand, w.meta);
+  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, w.init_tc,
+                                                        dv, w.n_pad, w.cand, w.meta);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
@@ -1839,7 +1862,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     const int threads = 256;
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
         zs, n, n_pad, dv.s, dv.kpad, dv.bounds, algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32,
-        dv.s_pad);
+        dv.s_pad, dv.atoms64, dv.d, algo == 1 ? w.init_tc : nullptr);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
@@ -1864,7 +1887,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
       const int64_t n_pad = n;
       prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                                dv.bounds, nullptr, nullptr,
-                                                               nullptr, dv.s_pad);
+                                                               nullptr, dv.s_pad, dv.atoms64,
+                                                               dv.d, nullptr);
       CBB_CUDA_TRY(cudaGetLastError());
     }
     int rc = launch_exhaustive(n, zs, dv, nullptr, nullptr, o, st);
@@ -1938,7 +1962,8 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
   const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
   prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
-                                                             w.win32, dv.s_pad);
+                                                             w.win32, dv.s_pad, dv.atoms64, dv.d,
+                                                             w.init_tc);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

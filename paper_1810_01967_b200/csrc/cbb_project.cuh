@@ -52,6 +52,8 @@ struct ZSource {
   const float2* g;
   float mu;
   float2* z_out;
+  const int32_t* hint; // optional per-voxel atom index (e.g. the previous IPG winner): its exact
+                       // score seeds the screen's running max (warm start); may be null
 };
 
 // Outputs.  Any pointer may be null (not produced).

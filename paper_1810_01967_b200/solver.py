@@ -244,7 +244,8 @@ class IpgState:
         o = self.scal[slot:slot + 1]
         _lib.check(self.lib.cbb_project_step(
             self.X.data_ptr(), self.G.data_ptr(), float(mu), self.Z.data_ptr(), self.n,
-            ctypes.byref(self.dd.view), self.idx_n.data_ptr(), self.gam_n.data_ptr(),
+            ctypes.byref(self.dd.view), self.idx.data_ptr(),   # warm start: current atoms
+            self.idx_n.data_ptr(), self.gam_n.data_ptr(),
             self.Xn.data_ptr(), self.dX.data_ptr(), o.data_ptr(), ws.data_ptr(), self.pws_bytes,
             self.algo, _lib.stream_ptr()), "cbb_project_step")
 
