@@ -195,21 +195,39 @@ def ipg_rate(device):
             "final_fidelity": trace.fidelities()[-1]}
 
 
-def ipg_rate_cfg2(device, peaks):
+def ipg_rate_cfg2(device, peaks, world=1):
     """BASELINE configs[2] IPG (256x256, L=1000, D=120,624 off-resonance atoms, s=20, EPI 16/256
-    lines, 30 iterations) through the public solve_compressed, with the SURVEY 8d roofline
-    model of one iteration (materialised-frame byte model + r projections on the tensor cores)."""
+    lines, 30 iterations) through the public solve_compressed -- or, under torchrun, through
+    sharded.solve_compressed_sharded over all ranks (voxel-sharded projection, frame-sharded
+    operator; wall time = max over ranks) -- with the SURVEY 8d roofline model of one
+    iteration (materialised-frame byte model + r projections on the tensor cores)."""
+    import torch
     from paper_1810_01967_b200 import workloads
     from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
     from paper_1810_01967_b200.solver import SolverConfig, solve_compressed
     cfg = workloads.make_cfg2(device=device)
     A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape), device=device)
-    solve_compressed(cfg.Y, A, cfg.cdict, None,
-                     SolverConfig(mode="blip_exact", max_iters=2, zeta=2.0, compressed=20))
+    solve = solve_compressed
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1810_01967_b200.sharded import solve_compressed_sharded
+        solve = solve_compressed_sharded
+    def run(conf):
+        if world == 1:
+            return solve(cfg.Y, A, cfg.cdict, None, conf)
+        return solve(cfg.Y, A, cfg.cdict, conf)
+
+    run(SolverConfig(mode="blip_exact", max_iters=2, zeta=2.0, compressed=20))   # warm-up
     conf = SolverConfig(mode="blip_exact", max_iters=30, zeta=2.0, compressed=20)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    X, maps, gam, trace = solve_compressed(cfg.Y, A, cfg.cdict, None, conf)
+    X, maps, gam, trace = run(conf)
+    torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t)
     its = trace.iterations
     trials = sum(r["shrinks"] + 1 for r in trace.records)
     n, L, m, s, D = 256 * 256, 1000, A.m, 20, cfg.d
@@ -219,13 +237,15 @@ def ipg_rate_cfg2(device, peaks):
     b_p = 8 * (4 * n * s + D * s + n)
     b_iter = b_ah + 24 * m * L + r * (b_p + b_a + 16 * m * L)
     f_p = 4.0 * s * n * D
-    bw = float(peaks.get("hbm_gbs", 6555.2)) * 1e9
-    tc = float(peaks.get("bf16_tflops", 1605.7)) * 1e12
+    bw = float(peaks.get("hbm_gbs", 6555.2)) * 1e9 * world       # aggregate over the ranks
+    tc = float(peaks.get("bf16_tflops", 1605.7)) * 1e12 * world
     t_roof = b_iter / bw + r * f_p / tc
     t_meas = dt / its
     return {"config": "BASELINE configs[2] (256x256, L=1000, D=120624 = T1 100 x T2 100 (T2<T1) "
                       "x dB0 21 Bloch IR-bSSFP atoms, s=20, EPI 16/256 lines, 30 dB, zeta=2, "
                       "max 30 iters)",
+            "n_gpus": world, "sharding": "none" if world == 1 else
+            "voxel-sharded state/projection, frame-sharded s-channel operator (NCCL)",
             "setup_seconds": cfg.setup_seconds, "iterations": its, "projection_trials": trials,
             "seconds": dt, "iters_per_s": its / dt, "ms_per_iter": 1e3 * t_meas,
             "final_fidelity": trace.fidelities()[-1],
@@ -318,6 +338,12 @@ def run_ours(args, rank, world, local_rank):
     e2e_s = float(te)
     agree = float(np.mean(res.indices == gen))
 
+    ipg2_multi = None
+    if world > 1 and not args.skip_cfg2:       # every rank takes part (collectives)
+        try:
+            ipg2_multi = ipg_rate_cfg2(dev, measured_peaks()[0], world)
+        except Exception as exc:  # report, never hide
+            ipg2_multi = {"error": repr(exc)}
     if rank != 0:
         return 0
     peaks, peak_kind = measured_peaks()
@@ -355,6 +381,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "argmax_re_vs_generator": agree,
     }
+    if ipg2_multi is not None:
+        line["ipg_cfg2"] = ipg2_multi
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(atoms, Z)
         try:
