@@ -421,7 +421,8 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
         *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
   }
-  double nz = 0, ez32 = 0, nz32 = 0;
+  // pass 1: Z (IPG: X - mu G, written to z_out) and its largest component magnitude
+  double amax = 0;
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (zs.x != nullptr) {
@@ -436,14 +437,12 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       float2 a = reinterpret_cast<const float2*>(zs.z)[v * s + k];
       re = a.x; im = a.y;
     }
-    const float re32 = float(re), im32 = float(im);
-    nz += re * re + im * im;
-    ez32 += (re - re32) * (re - re32) + (im - im32) * (im - im32);
-    nz32 += double(re32) * re32 + double(im32) * im32;
+    amax = fmax(amax, fmax(fabs(re), fabs(im)));
+    if (re != re || im != im) amax = re + im;  // propagate NaN
   }
   const double dmax = bounds[kBDmax];
   const double d32 = bounds[kBD32Max], del32 = bounds[kBDelta32];
-  if (nz == 0.0) {
+  if (amax == 0.0) {  // all-zero row (decided on the components: |z|^2 may underflow)
     if (win_tc) win_tc[v] = -1.f;
     if (win32) win32[v] = -1.f;
     if (trow)
@@ -451,13 +450,27 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
         *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
   }
-  if (!isfinite(nz)) {  // inf / NaN voxel: no screening, the exhaustive fp64 scan decides
+  int ea = 0;
+  if (isfinite(amax)) frexp(amax, &ea);
+  if (!isfinite(amax) || ea < -80 || ea > 80) {
+    // inf / NaN voxel, or one whose squares / fp32 copy would under- or overflow: no
+    // screening, the exhaustive fp64 scan decides (NaN windows route it there)
     if (win_tc) win_tc[v] = __int_as_float(0x7fc00000);
     if (win32) win32[v] = __int_as_float(0x7fc00000);
     if (trow)
       for (int c = 0; c < kpad / 8; ++c)
         *reinterpret_cast<uint4*>(trow + c * 16) = make_uint4(0, 0, 0, 0);
     return;
+  }
+  // pass 2: norms and the fp32 rounding error (no under- / overflow for |z| in 2^[-80, 80])
+  double nz = 0, ez32 = 0, nz32 = 0;
+  for (int k = 0; k < s; ++k) {
+    const double2 z = load_z(zs, v, s, k);
+    const double re = z.x, im = z.y;
+    const float re32 = float(re), im32 = float(im);
+    nz += re * re + im * im;
+    ez32 += (re - re32) * (re - re32) + (im - im32) * (im - im32);
+    nz32 += double(re32) * re32 + double(im32) * im32;
   }
   const double acc32 = double(2 * s_pad + 4) * 0x1p-24;
   const double e3 = sqrt(ez32) * dmax + sqrt(nz32) * del32 + acc32 * sqrt(nz32) * d32;
@@ -527,13 +540,9 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
 }
 
 // ============================================================== FFMA screening
-// vlist != nullptr: screen only the *vcount voxels listed (the tcgen05 pass's overflows --
-// coherent dictionaries whose fp16 window holds more chunks than its candidate lists).
 template <int S>
 __global__ void __launch_bounds__(128) mf_ffma_kernel(ZSource zs, DictView dv, int64_t n,
                                                       const float* __restrict__ win32,
-                                                      const int* __restrict__ vcount,
-                                                      const int64_t* __restrict__ vlist,
                                                       ProjOut out, int* ovf_count,
                                                       int64_t* ovf_list) {
   constexpr int TA = 128;  // atoms per shared tile
@@ -541,11 +550,8 @@ __global__ void __launch_bounds__(128) mf_ffma_kernel(ZSource zs, DictView dv, i
   __shared__ int cj[kCandCap * 128];
   __shared__ float cs[kCandCap * 128];
   const int tid = threadIdx.x;
-  const int64_t cnt = vlist ? int64_t(*vcount) : n;
-  if (int64_t(blockIdx.x) * 128 >= cnt) return;  // block-uniform
-  const int64_t slot = int64_t(blockIdx.x) * 128 + tid;
-  const bool live = slot < cnt;
-  const int64_t v = live ? (vlist ? vlist[slot] : slot) : 0;
+  const int64_t v = int64_t(blockIdx.x) * 128 + tid;
+  const bool live = v < n;
   float zr[S], zi[S];
 #pragma unroll
   for (int k = 0; k < S; ++k) {
@@ -1702,38 +1708,28 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   return kOk;
 }
 
-// FFMA screening of all n voxels (vlist == nullptr) or of the *vcount listed ones; its own
-// overflows go to (oc, ol) for the exhaustive fp64 rescan.
-struct FfmaArgs {
-  const int* vcount;
-  const int64_t* vlist;
-  int* oc;
-  int64_t* ol;
-};
-
 template <int S>
 static int launch_ffma(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                       const ProjOut& out, const FfmaArgs& fa, cudaStream_t st) {
+                       const ProjOut& out, cudaStream_t st) {
   const int blocks = int((n + 127) / 128);
-  mf_ffma_kernel<S><<<blocks, 128, 0, st>>>(zs, dv, n, w.win32, fa.vcount, fa.vlist, out, fa.oc,
-                                             fa.ol);
+  mf_ffma_kernel<S><<<blocks, 128, 0, st>>>(zs, dv, n, w.win32, out, w.ovf_count, w.ovf_list);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
 
 static int dispatch_ffma(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                         const ProjOut& out, const FfmaArgs& fa, cudaStream_t st) {
+                         const ProjOut& out, cudaStream_t st) {
   switch (dv.s_pad) {
-    case 2: return launch_ffma<2>(w, n, zs, dv, out, fa, st);
-    case 4: return launch_ffma<4>(w, n, zs, dv, out, fa, st);
-    case 6: return launch_ffma<6>(w, n, zs, dv, out, fa, st);
-    case 8: return launch_ffma<8>(w, n, zs, dv, out, fa, st);
-    case 10: return launch_ffma<10>(w, n, zs, dv, out, fa, st);
-    case 12: return launch_ffma<12>(w, n, zs, dv, out, fa, st);
-    case 16: return launch_ffma<16>(w, n, zs, dv, out, fa, st);
-    case 20: return launch_ffma<20>(w, n, zs, dv, out, fa, st);
-    case 24: return launch_ffma<24>(w, n, zs, dv, out, fa, st);
-    case 32: return launch_ffma<32>(w, n, zs, dv, out, fa, st);
+    case 2: return launch_ffma<2>(w, n, zs, dv, out, st);
+    case 4: return launch_ffma<4>(w, n, zs, dv, out, st);
+    case 6: return launch_ffma<6>(w, n, zs, dv, out, st);
+    case 8: return launch_ffma<8>(w, n, zs, dv, out, st);
+    case 10: return launch_ffma<10>(w, n, zs, dv, out, st);
+    case 12: return launch_ffma<12>(w, n, zs, dv, out, st);
+    case 16: return launch_ffma<16>(w, n, zs, dv, out, st);
+    case 20: return launch_ffma<20>(w, n, zs, dv, out, st);
+    case 24: return launch_ffma<24>(w, n, zs, dv, out, st);
+    case 32: return launch_ffma<32>(w, n, zs, dv, out, st);
   }
   return kErrUnsupported;
 }
@@ -1866,10 +1862,9 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
-    const FfmaArgs all{nullptr, nullptr, w.ovf_count, w.ovf_list};
     int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
                                           : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
-                         : dispatch_ffma(w, n, zr, dv, o, all, st);
+                         : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
     timing_mark(1, st);
     if (algo == 1) {
