@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define CBB_ABI_VERSION 1
+#define CBB_ABI_VERSION 2
 
 /* Device view of a prepared dictionary (filled by cbb_dict_prepare). */
 typedef struct cbb_dict_view {
@@ -50,12 +50,22 @@ typedef struct cbb_dict_view {
   int32_t n_btiles;   /* ceil(d / 128) */
   const void* atoms64;   /* d x s complex128 */
   const void* atoms32;   /* d x 2*s_pad fp32 planar */
-  const void* atoms_tc;  /* bf16 UMMA tiles */
+  const void* atoms_tc;  /* fp16 UMMA tiles (fp16-accumulated screen) */
   const float* bounds;   /* certified error bounds */
+  const void* atoms_tc2; /* split hi/lo fp16 UMMA tiles (fp32-accumulated screen), s <= 10 */
+  int32_t prefer_split;  /* CBB_ALGO_AUTO uses the split screen: the dictionary is coherent
+                            (its sampled atoms have near-duplicates inside the fp16 window) */
+  int32_t reserved;
 } cbb_dict_view;
 
 /* Projection algorithms. */
-enum { CBB_ALGO_AUTO = 0, CBB_ALGO_TCGEN05 = 1, CBB_ALGO_FFMA = 2, CBB_ALGO_EXHAUSTIVE = 3 };
+enum {
+  CBB_ALGO_AUTO = 0,        /* split tcgen05 if prefer_split (s <= 10), else fp16 tcgen05 ... */
+  CBB_ALGO_TCGEN05 = 1,     /* fp16 operands, fp16 accumulators (2s < 64) */
+  CBB_ALGO_FFMA = 2,        /* fp32 FFMA screen */
+  CBB_ALGO_EXHAUSTIVE = 3,  /* fp64 scan of every atom */
+  CBB_ALGO_TCGEN05_SPLIT = 4 /* hi/lo fp16 operands, fp32 accumulators (s <= 10) */
+};
 
 int cbb_abi_version(void);
 const char* cbb_last_error(void);

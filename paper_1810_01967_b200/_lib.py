@@ -23,13 +23,14 @@ c_vp = ctypes.c_void_p
 
 ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED, ERR_CUFFT = 1, 2, 3, 4
 
-ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3}
+ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3, "tcgen05_split": 4}
 
 
 class DictView(ctypes.Structure):
     _fields_ = [("d", c_i64), ("s", c_i32), ("s_pad", c_i32), ("kpad", c_i32),
                 ("n_btiles", c_i32), ("atoms64", c_vp), ("atoms32", c_vp),
-                ("atoms_tc", c_vp), ("bounds", c_vp)]
+                ("atoms_tc", c_vp), ("bounds", c_vp), ("atoms_tc2", c_vp),
+                ("prefer_split", c_i32), ("reserved", c_i32)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/coverblip_b200.h

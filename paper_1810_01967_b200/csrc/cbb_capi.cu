@@ -23,7 +23,7 @@ void timing_mark(int which, cudaStream_t st) {
 }
 
 // cbb_project.cu
-size_t dict_bytes(int64_t d, int s, size_t*, size_t*, size_t*, size_t*);
+size_t dict_bytes(int64_t d, int s, size_t*, size_t*, size_t*, size_t*, size_t*);
 int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, DictView* view,
                  cudaStream_t st);
 struct ProjWs;
@@ -74,6 +74,8 @@ static DictView to_view(const cbb_dict_view* v) {
   d.atoms32 = static_cast<const float*>(v->atoms32);
   d.atoms_tc = static_cast<const uint8_t*>(v->atoms_tc);
   d.bounds = v->bounds;
+  d.atoms_tc2 = static_cast<const uint8_t*>(v->atoms_tc2);
+  d.prefer_split = v->prefer_split;
   return d;
 }
 
@@ -98,7 +100,7 @@ int cbb_device_sm_count(int* out) {
 }
 
 size_t cbb_dict_storage_bytes(int64_t d, int32_t s) {
-  return dict_bytes(d, s, nullptr, nullptr, nullptr, nullptr);
+  return dict_bytes(d, s, nullptr, nullptr, nullptr, nullptr, nullptr);
 }
 
 int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s, void* storage,
@@ -119,6 +121,9 @@ int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s
   view_out->atoms32 = v.atoms32;
   view_out->atoms_tc = v.atoms_tc;
   view_out->bounds = v.bounds;
+  view_out->atoms_tc2 = v.atoms_tc2;
+  view_out->prefer_split = v.prefer_split;
+  view_out->reserved = 0;
   return kOk;
 }
 

@@ -54,6 +54,12 @@ __host__ __device__ inline int kpad_for(int s) { return (2 * s < 32) ? 32 : 64; 
 __host__ __device__ inline int mma_ksteps(int s) { return (2 * s + 1 + 15) / 16; }
 constexpr unsigned short kF16One = 0x3C00, kF16MinusMax = 0xFBFF;  // 1.0, -65504
 
+// Split-operand screening (fp16 hi/lo operands, fp32 accumulators): voxel rows
+// [z_hi | z_lo | z_hi | 1], atom rows [d_hi | d_hi | d_lo | sentinel], K = 6s + 1 <= 64.
+constexpr int kSplitMaxS = 10;
+constexpr int kSplitKP = 64;
+__host__ __device__ inline int split_ksteps(int s) { return (6 * s + 1 + 15) / 16; }
+
 // Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.
 __host__ __device__ inline uint32_t tile_chunk_offset(int r, int c, int kpad) {
   if (kpad == 32) {  // 64 B rows, Swizzle<2,4,3>: chunk bits [4,6) ^= addr bits [7,9)
@@ -190,6 +196,20 @@ __device__ __forceinline__ void tmem_ld32_pack16(uint32_t taddr, uint32_t (&r)[3
       : "r"(taddr));
 }
 
+// 32 lanes x 32 consecutive 32-bit accumulator columns (fp32 accumulators).
+__device__ __forceinline__ void tmem_ld32_f32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
 // 32 lanes x 32 consecutive 16-bit accumulator columns packed in pairs (.pack::16b).
 __device__ __forceinline__ void tmem_ld16_pack16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -221,6 +241,14 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, int kpa
 // 32-bit TMEM column.
 __host__ __device__ constexpr uint32_t idesc_f16_f16(int M, int N) {
   return (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// kind::f16, A/B = F16, D = F32 (c_format 1).  Measured (scripts/probe_f32acc.cu): each K = 16
+// instruction aligns its products (and the incoming accumulator) to the largest exponent,
+// keeping at least 24 bits below it (smaller contributions are truncated), and rounds the
+// sum once to fp32; on random split rows the error is <= 2^-20.9 sum|a_k b_k| over 4 steps.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+  return (1u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 // ---------------------------------------------------------------- exact scoring

@@ -395,6 +395,88 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
   atomic_max_nonneg(bounds + kBDhMax, __double2float_ru(sqrt(nrm_h)));
 }
 
+// Split-operand tiles (s <= kSplitMaxS): row j = [d_hi (2s) | d_hi (2s) | d_lo (2s) | sentinel],
+// d_hi = fp16(scale_d d), d_lo = fp16(scale_d d - d_hi), K = 64, 128-byte swizzle.  Padded rows
+// carry -65504 in the sentinel column (their fp32-accumulated score is -65504 for every voxel).
+__global__ void prep_tc2_kernel(const double2* __restrict__ atoms64, int64_t d, int64_t d_pad,
+                                int s, uint8_t* __restrict__ atoms_tc2,
+                                float* __restrict__ bounds) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= d_pad) return;
+  const int tile = int(j / kTileRows), r = int(j % kTileRows);
+  uint8_t* trow = atoms_tc2 + size_t(tile) * kTileRows * kSplitKP * 2;
+  auto put = [&](int e, unsigned short h) {
+    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e >> 3, kSplitKP) +
+                                       (e & 7) * 2) = h;
+  };
+  if (j >= d) {
+    put(6 * s, kF16MinusMax);
+    return;
+  }
+  const double sc = dict_scale(bounds);
+  double del = 0, nlo = 0, nhi = 0;
+  for (int k = 0; k < s; ++k) {
+    const double2 a = atoms64[j * s + k];
+    const double x[2] = {a.x * sc, a.y * sc};
+    for (int c = 0; c < 2; ++c) {
+      const unsigned short hi = f16_bits_rn(x[c]);
+      const double fhi = f16_bits_to_double(hi);
+      const unsigned short lo = f16_bits_rn(x[c] - fhi);
+      const double flo = f16_bits_to_double(lo);
+      const int e = c * s + k;  // re parts [0, s), im parts [s, 2s)
+      put(e, hi);
+      put(2 * s + e, hi);
+      put(4 * s + e, lo);
+      const double rem = x[c] - fhi - flo;
+      del += rem * rem;
+      nlo += flo * flo;
+      nhi += fhi * fhi;
+    }
+  }
+  atomic_max_nonneg(bounds + kBDeltaS, __double2float_ru(sqrt(del)));
+  atomic_max_nonneg(bounds + kBDloMax, __double2float_ru(sqrt(nlo)));
+  atomic_max_nonneg(bounds + kBRowMax, __double2float_ru(sqrt(2.0 * nhi + nlo) * (1.0 + 1e-12)));
+}
+
+// Coherence estimate (selects the screen in auto mode): for kCohSamples evenly spaced atoms i,
+// count the other atoms j with Re<d_i, d_j> >= (1 - 2^-6) ||d_i|| ||d_j|| (fp32 from the planar
+// copy).  Atoms that close score within the fp16 screen's window of each other for voxels with
+// cosine >= ~1/2 to their best atom, so every such neighbour becomes a candidate to rescore;
+// the split screen's window is ~2^-16 wide.  One block per sampled atom.
+constexpr int kCohSamples = 256;
+__global__ void __launch_bounds__(256) coherence_kernel(const float* __restrict__ atoms32,
+                                                        int64_t d, int s, int sp,
+                                                        float* __restrict__ bounds) {
+  __shared__ float ai[64];
+  __shared__ int red[8];
+  const int64_t i = (int64_t(blockIdx.x) * d) / gridDim.x;
+  for (int k = threadIdx.x; k < 2 * sp; k += blockDim.x) ai[k] = atoms32[i * 2 * sp + k];
+  __syncthreads();
+  float ni = 0.f;
+  for (int k = 0; k < s; ++k) ni = fmaf(ai[k], ai[k], fmaf(ai[sp + k], ai[sp + k], ni));
+  int cnt = 0;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    if (j == i) continue;
+    const float* aj = atoms32 + j * 2 * sp;
+    float dot = 0.f, nj = 0.f;
+    for (int k = 0; k < s; ++k) {
+      const float re = aj[k], im = aj[sp + k];
+      dot = fmaf(ai[k], re, fmaf(ai[sp + k], im, dot));
+      nj = fmaf(re, re, fmaf(im, im, nj));
+    }
+    cnt += (dot > 0.f && dot * dot >= (1.f - 0x1p-6f) * (1.f - 0x1p-6f) * ni * nj) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    atomicAdd(bounds + kBCoherence, float(t) / float(gridDim.x));
+  }
+}
+
 // ============================================================== prologue
 // One thread per voxel (n_pad = whole voxel tiles).  Produces the fp16 tensor-core voxel rows
 // z~ = fp16(scale_v z) (scale_v a power of two putting ||scale_v z|| in [2^12, 2^13), so with
@@ -410,7 +492,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 const float* __restrict__ bounds, uint8_t* __restrict__ ztiles,
                                 float* __restrict__ win_tc, float* __restrict__ win32,
                                 int s_pad, const double2* __restrict__ atoms64,
-                                int64_t d_atoms, float* __restrict__ init_tc) {
+                                int64_t d_atoms, float* __restrict__ init_tc, int split) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
   // plain row-major fp16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
@@ -482,7 +564,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   unsigned short row[64];
 #pragma unroll
   for (int e = 0; e < 64; ++e) row[e] = 0;
-  double eh = 0, nzh = 0;
+  double eh = 0, nzh = 0, nlo = 0, nhi = 0;
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (zs.x != nullptr) {
@@ -496,16 +578,30 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       float2 a = reinterpret_cast<const float2*>(zs.z)[v * s + k];
       re = a.x; im = a.y;
     }
-    re *= sv;
-    im *= sv;
-    const unsigned short hre = f16_bits_rn(re), him = f16_bits_rn(im);
-    row[k] = hre;
-    row[s + k] = him;
-    const double fre = f16_bits_to_double(hre), fim = f16_bits_to_double(him);
-    eh += (re - fre) * (re - fre) + (im - fim) * (im - fim);
-    nzh += fre * fre + fim * fim;
+    const double x[2] = {re * sv, im * sv};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const unsigned short hi = f16_bits_rn(x[c]);
+      const double fhi = f16_bits_to_double(hi);
+      const int e = c * s + k;
+      row[e] = hi;
+      if (split) {  // [z_hi | z_lo | z_hi]: z~ = z_hi + z_lo
+        const unsigned short lo = f16_bits_rn(x[c] - fhi);
+        const double flo = f16_bits_to_double(lo);
+        row[2 * s + e] = lo;
+        row[4 * s + e] = hi;
+        const double rem = x[c] - fhi - flo;
+        eh += rem * rem;
+        nzh += (fhi + flo) * (fhi + flo);
+        nlo += flo * flo;
+        nhi += fhi * fhi;
+      } else {
+        eh += (x[c] - fhi) * (x[c] - fhi);
+        nzh += fhi * fhi;
+      }
+    }
   }
-  row[2 * s] = kF16One;  // sentinel column right after the data (2s < kpad)
+  row[split ? 6 * s : 2 * s] = kF16One;  // sentinel column right after the data (< kpad)
   for (int c = 0; c < kpad / 8; ++c) {
     uint4 pk;
     pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
@@ -514,11 +610,25 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     pk.w = uint32_t(row[c * 8 + 6]) | (uint32_t(row[c * 8 + 7]) << 16);
     *reinterpret_cast<uint4*>(trow + c * 16) = pk;
   }
-  const double sd = bounds[kBScaleD], dh = bounds[kBDhMax], delh = bounds[kBDeltaH];
-  const double nq = double(mma_ksteps(s));  // fp16 roundings of nonzero partial sums
-  const double acc_tc = nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
-  const double eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh +
-                    nq * 0x1p-24;
+  const double sd = bounds[kBScaleD];
+  double eb;
+  if (split) {
+    // s~ = z_hi.d_hi + z_lo.d_hi + z_hi.d_lo = z~.d~ - z_lo.d_lo (z~ = z_hi + z_lo, d~ likewise):
+    //   |s~ - s| <= ||scale_v z - z~|| scale_d max||d|| + ||z~|| max||scale_d d - d~||
+    //             + ||z_lo|| max||d_lo|| + acc * ||A_v|| max||B_j||
+    // acc: per issued K = 16 fp32-accumulated instruction, < 16 truncations below 2^-24 of the
+    // largest term plus one fp32 rounding, each <= 2^-24 sum|a_k b_k| <= 2^-24 ||A|| ||B||
+    // (18 instead of 17 as slack), n_q = ceil((6s+1)/16) instructions.
+    const double nq = double(split_ksteps(s));
+    const double acc_tc = nq * 18.0 * 0x1p-24;
+    eb = sqrt(eh) * sd * dmax + sqrt(nzh) * bounds[kBDeltaS] + sqrt(nlo) * bounds[kBDloMax] +
+         acc_tc * sqrt(2.0 * nhi + nlo) * bounds[kBRowMax] + nq * 0x1p-40;
+  } else {
+    const double dh = bounds[kBDhMax], delh = bounds[kBDeltaH];
+    const double nq = double(mma_ksteps(s));  // fp16 roundings of nonzero partial sums
+    const double acc_tc = nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
+    eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh + nq * 0x1p-24;
+  }
   win_tc[v] = __double2float_ru(2.0 * eb * 1.001 + 1e-30);
   if (init_tc) {
     // warm start: any atom's exact score lower-bounds the approximate maximum once the
@@ -803,17 +913,32 @@ __device__ long long g_trace_vt[256 * 4];  // per voxel tile of CTA 0: loop star
 // Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
 constexpr int kParts = 3;
 
-template <int KP>
+// SPLIT: hi/lo fp16 operands with fp32 accumulators (KP = 64): 128-atom tiles (N = 128 MMAs;
+// measured faster than 64-atom tiles with six stages), screened in two 64-register halves.
+template <int KP, bool SPLIT = false>
 struct TcCfg {
-  static constexpr int kChunks = KP == 32 ? 5 : 4;           // 32-atom chunks per tile
-  static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 atoms per tile
+  static_assert(!SPLIT || KP == kSplitKP, "split tiles are 64 wide");
+#ifndef CBB_SPLIT_CHUNKS
+#define CBB_SPLIT_CHUNKS 4
+#endif
+  static constexpr int kChunks = SPLIT ? CBB_SPLIT_CHUNKS : (KP == 32 ? 5 : 4);  // 32-atom chunks
+  static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 / 64 (split)
   static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
-  static constexpr int kAcc = 3;                             // x BN accumulator columns
+#ifndef CBB_SPLIT_ACC
+#define CBB_SPLIT_ACC 3
+#endif
+  static constexpr int kAcc = SPLIT ? CBB_SPLIT_ACC : 3;     // x BN accumulator columns
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
   static constexpr int kBBytes = BN * KP * 2;
-  static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
+#ifndef CBB_RING_F16_KB
+#define CBB_RING_F16_KB 96
+#endif
+#ifndef CBB_RING_SPLIT_KB
+#define CBB_RING_SPLIT_KB 144
+#endif
+  static constexpr int kRing = (SPLIT ? CBB_RING_SPLIT_KB : KP == 32 ? CBB_RING_F16_KB : 144) * 1024;
   static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
   static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
   static constexpr int kStages = (kStagesRaw / kParts) * kParts;
@@ -835,7 +960,7 @@ struct TcCfg {
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr uint32_t kIdesc = idesc_f16_f16(128, BN);
+  static constexpr uint32_t kIdesc = SPLIT ? idesc_f16_f32(128, BN) : idesc_f16_f16(128, BN);
   static constexpr int kMinTiles = kParts;  // every part owns >= 1 tile per voxel tile
 };
 
@@ -928,6 +1053,59 @@ __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_
   }
 }
 
+// Split mode: fp32 scores, one per register (chunk k = registers 32k .. 32k+31).  Same
+// structure as the packed path: one 3-input max chain per 32-atom chunk (FMNMX3), one compare
+// and one warp vote per tile; records carry the chunk's 6-atom group mask.
+__device__ __forceinline__ float fmax3f(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+
+__device__ __forceinline__ void record_chunk_f32(const uint32_t* r, float cm, int64_t jb,
+                                                 float thr, HCandList& cl) {
+  uint32_t mask = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])) >= thr ? (1u << 5) : 0u;
+#pragma unroll
+  for (int g = 0; g < 5; ++g) {
+    const float m = fmaxf(fmax3f(__uint_as_float(r[6 * g]), __uint_as_float(r[6 * g + 1]),
+                                 __uint_as_float(r[6 * g + 2])),
+                          fmax3f(__uint_as_float(r[6 * g + 3]), __uint_as_float(r[6 * g + 4]),
+                                 __uint_as_float(r[6 * g + 5])));
+    mask |= m >= thr ? (1u << g) : 0u;
+  }
+  cl.insert(pack_chunk(jb, mask), cm, thr);
+}
+
+template <int NC>
+__device__ __forceinline__ void screen_tile_f32(const uint32_t (&r)[32 * NC], int64_t jb,
+                                                float win, float& runmax, float& thr,
+                                                bool& active, HCandList& cl) {
+  float c[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const uint32_t* q = r + 32 * k;
+    float a = fmax3f(__uint_as_float(q[0]), __uint_as_float(q[1]), __uint_as_float(q[2]));
+#pragma unroll
+    for (int i = 3; i < 31; i += 2)
+      a = fmax3f(a, __uint_as_float(q[i]), __uint_as_float(q[i + 1]));
+    c[k] = fmaxf(a, __uint_as_float(q[31]));
+  }
+  float cm = c[0];
+#pragma unroll
+  for (int k = 1; k < NC; ++k) cm = fmaxf(cm, c[k]);
+  if (__any_sync(0xffffffffu, cm >= thr)) {
+    if (cm >= thr) {
+      runmax = fmaxf(runmax, cm);
+      if (active) {
+        thr = __fsub_rd(runmax, win);
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+          if (c[k] >= thr && !cl.ovf) record_chunk_f32(r + 32 * k, c[k], jb + 32 * k, thr, cl);
+        if (cl.ovf) {
+          active = false;
+          thr = INFINITY;
+        }
+      }
+    }
+  }
+}
+
 template <int KP>
 __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrows, int64_t v,
                                                 bool live, uint32_t taddr) {
@@ -949,12 +1127,12 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
   tc_wait_st();
 }
 
-template <int KP>
-__global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
+template <int KP, bool SPLIT>
+__global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
                  DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta) {
-  using C = TcCfg<KP>;
+  using C = TcCfg<KP, SPLIT>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
@@ -997,6 +1175,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------ producer (bulk copies of atom tiles)
     const uint64_t pol_b = policy_evict_last();
+    const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < my_vts; ++it) {
@@ -1005,7 +1184,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
         mbar_wait(b_empty + st, ph ^ 1u);
         if (elect_one()) {
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
-          bulk_g2s(smem + C::kOffB + st * C::kBBytes, dv.atoms_tc + size_t(ba) * C::kBBytes,
+          bulk_g2s(smem + C::kOffB + st * C::kBBytes, atiles + size_t(ba) * C::kBBytes,
                    C::kBBytes, b_full + st, pol_b);
         }
         __syncwarp();
@@ -1019,7 +1198,7 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
   } else if (warp >= 1 && warp <= kParts) {
     // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
     const int me = warp - 1;
-    const int nks = mma_ksteps(dv.s);
+    const int nks = SPLIT ? split_ksteps(dv.s) : mma_ksteps(dv.s);
     const uint32_t b_base = smem_u32(smem + C::kOffB);
     int sacc = me;  // accumulator stage kk % kAcc
     int tb = me;    // completion barrier kk % kTBars
@@ -1116,28 +1295,53 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       __half runmax = active ? __float2half_rd(init) : __ushort_as_half(0xFC00);
       __half thr = active ? __float2half_rd(__half2float(runmax) - win)
                           : __ushort_as_half(0x7C00);
+      // split mode: fp32 running max / threshold (thresholds rounded down)
+      float runmax_f = active ? init_tc[v] : -INFINITY;
+      float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
       const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
       for (; kk < kend; kk += kParts) {
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
         mbar_wait(t_full + tb, ph);
         tc_fence_after();
         if (q == 0 && lane == 0) CBB_STAMP(2, kk);
-        uint32_t r[16 * C::kChunks];
+        // split mode: at most two fp32 chunks (64 registers) in flight; wider tiles are
+        // screened in halves and released after the last half is loaded
+        constexpr int kRegChunks = SPLIT ? (C::kChunks < 2 ? C::kChunks : 2) : C::kChunks;
+        uint32_t r[(SPLIT ? 32 : 16) * kRegChunks];
         __syncwarp();
         const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
+        if constexpr (SPLIT) {
 #pragma unroll
-        for (int c = 0; c + 2 <= C::kChunks; c += 2)
-          tmem_ld32_pack16(ta + uint32_t(32 * c), *reinterpret_cast<uint32_t(*)[32]>(r + 16 * c));
-        if (C::kChunks & 1)
-          tmem_ld16_pack16(ta + uint32_t(32 * (C::kChunks - 1)),
-                           *reinterpret_cast<uint32_t(*)[16]>(r + 16 * (C::kChunks - 1)));
-        tc_wait_ld();
-        if (q == 0 && lane == 0) CBB_STAMP(3, kk);
-        // early release: the stage may be overwritten by tile kk + kAcc while we screen
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_full + rel);
-        screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
+          for (int h = 0; h < C::kChunks / kRegChunks; ++h) {
+#pragma unroll
+            for (int c = 0; c < kRegChunks; ++c)
+              tmem_ld32_f32(ta + uint32_t(32 * (h * kRegChunks + c)),
+                            *reinterpret_cast<uint32_t(*)[32]>(r + 32 * c));
+            tc_wait_ld();
+            if (h + 1 == C::kChunks / kRegChunks) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(b_full + rel);
+            }
+            screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win, runmax_f,
+                                        thr_f, active, cl);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c + 2 <= C::kChunks; c += 2)
+            tmem_ld32_pack16(ta + uint32_t(32 * c),
+                             *reinterpret_cast<uint32_t(*)[32]>(r + 16 * c));
+          if (C::kChunks & 1)
+            tmem_ld16_pack16(ta + uint32_t(32 * (C::kChunks - 1)),
+                             *reinterpret_cast<uint32_t(*)[16]>(r + 16 * (C::kChunks - 1)));
+          tc_wait_ld();
+          if (q == 0 && lane == 0) CBB_STAMP(3, kk);
+          // early release: the stage may be overwritten by tile kk + kAcc while we screen
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(b_full + rel);
+          screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
+        }
         if (q == 0 && lane == 0) CBB_STAMP(6, kk);
         sacc += kParts;
         if (sacc >= C::kAcc) sacc -= C::kAcc;
@@ -1156,8 +1360,9 @@ __global__ void __launch_bounds__(TcCfg<KP>::kThreads, 1)
       // rescore_kernel merges the parts and rescans the flagged groups in fp64
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(1, it);
       if (live) {
-        const int total = (win >= 0.f) ? cl.finish(__half2float(runmax) - win) : 0;
-        meta[int64_t(part) * n_pad + v] = make_int2(total, __float_as_int(__half2float(runmax)));
+        const float rm = SPLIT ? runmax_f : __half2float(runmax);
+        const int total = (win >= 0.f) ? cl.finish(rm - win) : 0;
+        meta[int64_t(part) * n_pad + v] = make_int2(total, __float_as_int(rm));
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(2, it);
     }
@@ -1568,7 +1773,8 @@ static int s_pad_for(int s) {
   return -1;
 }
 
-size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc, size_t* offb) {
+size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc, size_t* offb,
+                  size_t* offtc2) {
   const int sp = s_pad_for(s) > 0 ? s_pad_for(s) : s;
   const int kp = kpad_for(s);
   const int64_t nbt = (d + kTileRows - 1) / kTileRows;
@@ -1584,6 +1790,8 @@ size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc,
   // may run past the last 128-row tile
   size_t c = take(size_t(nbt + 2) * kTileRows * kp * 2);
   size_t e = take(kBCount * sizeof(float));
+  size_t f = take(s <= kSplitMaxS ? size_t(nbt + 2) * kTileRows * kSplitKP * 2 : 0);
+  if (offtc2) *offtc2 = f;
   if (off64) *off64 = a;
   if (off32) *off32 = b;
   if (offtc) *offtc = c;
@@ -1594,8 +1802,8 @@ size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc,
 int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, DictView* view,
                  cudaStream_t st) {
   if (d <= 0 || s <= 0) return kErrArgument;
-  size_t o64, o32, otc, ob;
-  const size_t total = dict_bytes(d, s, &o64, &o32, &otc, &ob);
+  size_t o64, o32, otc, ob, otc2;
+  const size_t total = dict_bytes(d, s, &o64, &o32, &otc, &ob, &otc2);
   uint8_t* base = static_cast<uint8_t*>(storage);
   CBB_CUDA_TRY(cudaMemsetAsync(base, 0, total, st));
   DictView v{};
@@ -1608,6 +1816,7 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   v.atoms32 = reinterpret_cast<float*>(base + o32);
   v.atoms_tc = base + otc;
   v.bounds = reinterpret_cast<float*>(base + ob);
+  v.atoms_tc2 = s <= kSplitMaxS ? base + otc2 : nullptr;
   const int threads = 256;
   const int blocks = int((d + threads - 1) / threads);
   prep_dict_kernel<<<blocks, threads, 0, st>>>(atoms, in128, d, s, v.s_pad,
@@ -1623,6 +1832,28 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
         const_cast<float*>(v.bounds));
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
+  }
+  if (v.s <= 32) {  // coherence estimate for the auto screen choice (planar fp32 copy)
+    coherence_kernel<<<kCohSamples, 256, 0, st>>>(v.atoms32, d, s, v.s_pad,
+                                                  const_cast<float*>(v.bounds));
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+  }
+  if (v.atoms_tc2) {  // split-operand tiles (after prep_tc_kernel: it publishes scale_d)
+    const int64_t d_pad = int64_t(v.n_btiles + 2) * kTileRows;
+    prep_tc2_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
+        v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc2), const_cast<float*>(v.bounds));
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+  }
+  v.prefer_split = 0;
+  if (v.atoms_tc2) {
+    // one-time host read of the coherence estimate (dictionary preparation synchronises once)
+    float coh = 0.f;
+    CBB_CUDA_TRY(cudaMemcpyAsync(&coh, v.bounds + kBCoherence, sizeof(float),
+                                 cudaMemcpyDeviceToHost, st));
+    CBB_CUDA_TRY(cudaStreamSynchronize(st));
+    v.prefer_split = coh >= 1.0f ? 1 : 0;
   }
   *view = v;
   return kOk;
@@ -1649,7 +1880,7 @@ constexpr int kReduceBlocks = 256;
 constexpr int kVoxPad = 512;  // voxel tiles are padded to a multiple of the largest TC voxel tile
 
 size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
-  const int kp = kpad_for(s);
+  const int kp = s <= kSplitMaxS ? kSplitKP : kpad_for(s);  // split rows are 64 wide
   const int64_t n_vt = (n + kVoxPad - 1) / kVoxPad;
   size_t o = 0;
   uint8_t* base = static_cast<uint8_t*>(base_ptr);
@@ -1688,13 +1919,13 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int KP>
+template <int KP, bool SPLIT = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
-  using C = TcCfg<KP>;
+  using C = TcCfg<KP, SPLIT>;
   static bool attr_set = false;
   if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
@@ -1702,8 +1933,9 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
-  mf_tc_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc, w.init_tc,
-                                                        dv, w.n_pad, w.cand, w.meta);
+  mf_tc_kernel<KP, SPLIT><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc,
+                                                               w.init_tc, dv, w.n_pad, w.cand,
+                                                               w.meta);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
@@ -1832,7 +2064,10 @@ int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStr
   return kOk;
 }
 
-// algo: 0 = auto (tcgen05 when 2s <= 64), 1 = tcgen05, 2 = FFMA, 3 = exhaustive fp64
+// algo: 0 = auto (split tcgen05 for coherent dictionaries with s <= 10, else tcgen05 when
+// 2s < 64, else FFMA / fp64),
+// 1 = tcgen05 (fp16 accumulators), 2 = FFMA, 3 = exhaustive fp64, 4 = split tcgen05 (hi/lo fp16
+// operands, fp32 accumulators)
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st) {
   if (n < 0) return kErrArgument;
@@ -1848,8 +2083,12 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   // tcgen05 path: K = 2s <= 64; chunk entries pack (atom / 32) into 20 bits; every epilogue
   // part needs >= 2 atom tiles of 64 per voxel tile (d > 320; smaller dictionaries use FFMA)
   const bool tc_ok = (2 * dv.s < 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
-  if (algo == 0) algo = tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
+  const bool split_ok = tc_ok && dv.s <= kSplitMaxS && dv.atoms_tc2 != nullptr;
+  if (algo == 0) algo = (split_ok && dv.prefer_split) ? 4 : tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
   if (algo == 1 && !tc_ok) return kErrUnsupported;
+  if (algo == 4 && !split_ok) return kErrUnsupported;
+  const bool split = algo == 4;
+  if (split) algo = 1;  // same pipeline, split operand tiles
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
   CBB_CUDA_TRY(cudaMemsetAsync(w.heavy_count, 0, sizeof(int), st));
@@ -1857,14 +2096,16 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
-        zs, n, n_pad, dv.s, dv.kpad, dv.bounds, algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32,
-        dv.s_pad, dv.atoms64, dv.d, algo == 1 ? w.init_tc : nullptr);
+        zs, n, n_pad, dv.s, split ? kSplitKP : dv.kpad, dv.bounds,
+        algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
+        algo == 1 ? w.init_tc : nullptr, split ? 1 : 0);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
-    int rc = (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
-                                          : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
-                         : dispatch_ffma(w, n, zr, dv, o, st);
+    int rc = split ? launch_tc<kSplitKP, true>(w, n, zr, dv, o, max_ctas, st)
+             : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
+                                            : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
+                           : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
     timing_mark(1, st);
     if (algo == 1) {
@@ -1883,7 +2124,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
       prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                                dv.bounds, nullptr, nullptr,
                                                                nullptr, dv.s_pad, dv.atoms64,
-                                                               dv.d, nullptr);
+                                                               dv.d, nullptr, 0);
       CBB_CUDA_TRY(cudaGetLastError());
     }
     int rc = launch_exhaustive(n, zs, dv, nullptr, nullptr, o, st);
@@ -1958,7 +2199,7 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
   prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
                                                              w.win32, dv.s_pad, dv.atoms64, dv.d,
-                                                             w.init_tc);
+                                                             w.init_tc, 0);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

@@ -6,7 +6,8 @@
 //   P_v   = g_v * D_j*               (projection.py:64)
 //
 // B200 design: a screening pass scores every (voxel, atom) pair in low
-// precision (fp16 tcgen05 MMA with fp16 accumulation, or fp32 FFMA) and keeps, per voxel, every atom
+// precision (fp16 tcgen05 MMA with fp16 accumulation; split hi/lo fp16 operands with fp32
+// accumulation for s <= 10; or fp32 FFMA) and keeps, per voxel, every atom
 // whose approximate score lies inside a CERTIFIED window below the running
 // maximum (window = 2 * rigorous bound on |approx - exact|).  The surviving
 // candidates are rescored in fp64 from the caller's own atoms and voxels, so
@@ -30,6 +31,9 @@ struct DictView {
   const float* atoms32;        // d x 2*s_pad planar fp32 [re.., im..]
   const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad fp16 (atoms * scale), swizzled
   const float* bounds;         // kB* slots below
+  const uint8_t* atoms_tc2;    // split-operand tiles (s <= kSplitMaxS, else null): 128-row
+                               // swizzled tiles of 64 fp16 [d_hi | d_hi | d_lo | sentinel]
+  int32_t prefer_split;        // auto mode screens with the split tiles (coherent dictionary)
 };
 
 // Bounds slots (all rounded up).  The fp16 tiles hold d~ = fp16(scale_d * d) with scale_d a
@@ -41,7 +45,13 @@ enum {
   kBDelta32 = 3,   // max_j ||d_j - fp32(d_j)||
   kBD32Max = 4,    // max_j ||fp32(d_j)||
   kBScaleD = 5,    // scale_d
-  kBCount = 8
+  // split-operand tiles: d_hi = fp16(scale_d d), d_lo = fp16(scale_d d - d_hi)
+  kBDeltaS = 6,    // max_j ||scale_d d_j - (d_hi + d_lo)||
+  kBDloMax = 7,    // max_j ||d_lo||
+  kBRowMax = 8,    // max_j ||[d_hi, d_hi, d_lo]|| = sqrt(2 ||d_hi||^2 + ||d_lo||^2)
+  kBCoherence = 9, // coherence estimate: mean number of other atoms j with
+                   // Re<d_i, d_j> >= (1 - 2^-6) ||d_i|| ||d_j|| over kCohSamples sampled atoms i
+  kBCount = 12
 };
 
 // Where the projection input Z comes from.

@@ -220,12 +220,19 @@ class DeviceDictionary:
         raw = self.storage[:n]
         return raw.view(torch.complex128).view(self.d, self.s)
 
-    BOUND_SLOTS = ("delta_h", "dmax", "dh_max", "delta32", "d32max", "scale_d")
+    BOUND_SLOTS = ("delta_h", "dmax", "dh_max", "delta32", "d32max", "scale_d", "delta_split",
+                   "dlo_max", "split_row_max", "coherence")
+
+    @property
+    def prefer_split(self) -> bool:
+        """Auto mode screens with the split (hi/lo fp16, fp32-accumulated) tiles: the sampled
+        atoms have near-duplicates inside the fp16 screen's window (``coherence`` bound)."""
+        return bool(self.view.prefer_split)
 
     def bounds(self) -> dict:
         """Certified rounding bounds of the prepared copies (``cbb_project.cuh`` kB* slots)."""
         off = int(self.view.bounds) - self.storage.data_ptr()
-        vals = self.storage[off:off + 32].view(torch.float32).cpu().tolist()
+        vals = self.storage[off:off + 4 * len(self.BOUND_SLOTS)].view(torch.float32).cpu().tolist()
         return dict(zip(self.BOUND_SLOTS, vals))
 
 

@@ -16,6 +16,9 @@ in-vivo scans are absent, so every config is generated from fixed seeds
         multi-shot EPI 16 of 256 lines per frame (``make_epi_pattern``), 30 dB.  Large enough
         that the Bloch simulation, the Gram SVD and the measurement FFT run on the GPU
         (``make_cfg2(device=...)``; same recurrences as the host code, fp64).
+* cfg4  256x256x64 ellipsoid phantom (6 shells), T=500, T1 100 x T2 100 x dB0 26 (D = 149,344),
+        s = 10, per-frame random Cartesian masks at 1/16 of k-space, 30 dB (``make_cfg4``,
+        GPU-generated frame chunk by frame chunk).
 """
 
 from __future__ import annotations
@@ -28,7 +31,7 @@ from .dictionary import CompressedDictionary, Dictionary, svd_compress
 
 __all__ = ["sequence_schedule", "bloch_irbssfp", "cfg0_dictionary", "Cfg0", "make_cfg0",
            "random_atoms", "cone_voxels", "make_cfg1", "random_line_pattern", "make_cfg2",
-           "bloch_irbssfp_torch"]
+           "bloch_irbssfp_torch", "make_cfg4"]
 
 
 def sequence_schedule(L: int, seed: int = 0):
@@ -215,6 +218,33 @@ def bloch_irbssfp_torch(params, alpha, tr, device):
     return out
 
 
+def _offres_dictionary(L, s, n_t1, n_t2, n_b0, dev):
+    """T1 x T2 (T2 < T1) x dB0 Bloch IR-bSSFP dictionary simulated on the GPU, unit-normalised,
+    compressed by the large-d route of ``dictionary.py:176-183`` (second-moment matrix, eigh,
+    top-s, conjugated).  Returns (CompressedDictionary, raw (d, L) complex128 device atoms)."""
+    import torch
+    alpha, tr = sequence_schedule(L, seed=0)
+    t1 = np.geomspace(100.0, 5000.0, n_t1)
+    t2 = np.geomspace(50.0, 5000.0, n_t2)
+    b0 = np.linspace(-50.0, 50.0, n_b0)
+    g1, g2, g3 = np.meshgrid(t1, t2, b0, indexing="ij")
+    triples = np.stack([g1.ravel(), g2.ravel(), g3.ravel()], axis=1)
+    triples = triples[triples[:, 1] < triples[:, 0]]
+    raw = bloch_irbssfp_torch(triples, alpha, tr, dev)
+    raw /= torch.linalg.vector_norm(raw, dim=1, keepdim=True)
+    gram = (raw.transpose(0, 1) @ raw.conj()).cpu().numpy()
+    _, vecs = np.linalg.eigh(gram)
+    basis = np.ascontiguousarray(vecs[:, ::-1][:, :s].conj())
+    comp = raw @ torch.from_numpy(basis).to(dev)
+    factors = torch.linalg.vector_norm(comp, dim=1)
+    atoms_c = (comp / factors[:, None]).cpu().numpy()
+    parent = Dictionary(atoms=np.zeros((len(triples), 1)), norms=None, lookup_table=triples,
+                        tr_ms=float(np.mean(tr)), L=L)
+    cd = CompressedDictionary(basis=basis, atoms_compressed=atoms_c,
+                              renorm_factors=factors.cpu().numpy(), s=s, parent=parent)
+    return cd, raw
+
+
 @dataclass
 class Cfg2:
     cdict: CompressedDictionary
@@ -235,26 +265,8 @@ def make_cfg2(h=256, w=256, L=1000, s=20, lines=16, snr_db=30.0, n_t1=100, n_t2=
     from .forward_model import make_epi_pattern
     t0 = time.perf_counter()
     dev = torch.device(device) if device is not None else torch.device("cuda")
-    alpha, tr = sequence_schedule(L, seed=0)
-    t1 = np.geomspace(100.0, 5000.0, n_t1)
-    t2 = np.geomspace(50.0, 5000.0, n_t2)
-    b0 = np.linspace(-50.0, 50.0, n_b0)
-    g1, g2, g3 = np.meshgrid(t1, t2, b0, indexing="ij")
-    triples = np.stack([g1.ravel(), g2.ravel(), g3.ravel()], axis=1)
-    triples = triples[triples[:, 1] < triples[:, 0]]
-    raw = bloch_irbssfp_torch(triples, alpha, tr, dev)
-    raw /= torch.linalg.vector_norm(raw, dim=1, keepdim=True)
-    # dictionary.py:176-183 large-d route: second-moment matrix, eigh, top-s (conjugated)
-    gram = (raw.transpose(0, 1) @ raw.conj()).cpu().numpy()
-    _, vecs = np.linalg.eigh(gram)
-    basis = np.ascontiguousarray(vecs[:, ::-1][:, :s].conj())
-    comp = raw @ torch.from_numpy(basis).to(dev)
-    factors = torch.linalg.vector_norm(comp, dim=1)
-    atoms_c = (comp / factors[:, None]).cpu().numpy()
-    parent = Dictionary(atoms=np.zeros((len(triples), 1)), norms=None, lookup_table=triples,
-                        tr_ms=float(np.mean(tr)), L=L)
-    cd = CompressedDictionary(basis=basis, atoms_compressed=atoms_c,
-                              renorm_factors=factors.cpu().numpy(), s=s, parent=parent)
+    cd, raw = _offres_dictionary(L, s, n_t1, n_t2, n_b0, dev)
+    triples = cd.parent.lookup_table
     # phantom: `classes` horizontal bands inside a background border, one atom per class
     rng = np.random.default_rng(1)
     rr, cc = np.mgrid[0:h, 0:w]
@@ -280,3 +292,68 @@ def make_cfg2(h=256, w=256, L=1000, s=20, lines=16, snr_db=30.0, n_t1=100, n_t2=
     torch.cuda.empty_cache()
     return Cfg2(cdict=cd, pattern=pattern, spatial_shape=(h, w), Y=Y, d=len(triples),
                 setup_seconds=time.perf_counter() - t0)
+
+
+@dataclass
+class Cfg4:
+    cdict: CompressedDictionary
+    pattern: np.ndarray          # (L, m) sorted flat k-space indices per frame
+    spatial_shape: tuple
+    Y: np.ndarray                # (m, L) reference layout, complex64
+    labels: np.ndarray           # (n,) tissue class per voxel (0 = background)
+    class_atoms: np.ndarray      # (classes + 1,) generating atom per class
+    d: int
+    setup_seconds: float
+
+
+def make_cfg4(shape=(256, 256, 64), L=500, s=10, undersample=16, snr_db=30.0, n_t1=100,
+              n_t2=100, n_b0=26, classes=6, device=None) -> Cfg4:
+    """BASELINE configs[4]: 3-D IPG (GPU-generated).  256x256x64 phantom -- an ellipsoid split
+    into `classes` concentric shells, PD~U(0.5, 1), zero background -- T=500 frames of the same
+    sequence generator, T1 100 x T2 100 (T2 < T1) x dB0 26 atoms (D = 149,344 ~ 1.5e5), SVD s=10,
+    per-frame random Cartesian masks of n/16 k-space locations (seed 2), 30 dB noise (seed 3).
+    The (n, L) ground truth is never materialised: frames are synthesised, 3-D FFT'd and
+    sampled in chunks."""
+    import time
+
+    import torch
+    t0 = time.perf_counter()
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    cd, raw = _offres_dictionary(L, s, n_t1, n_t2, n_b0, dev)
+    d = raw.shape[0]
+    n = int(np.prod(shape))
+    m = n // undersample
+    rng = np.random.default_rng(1)
+    g = np.meshgrid(*[(np.arange(k) + 0.5) / k * 2.0 - 1.0 for k in shape], indexing="ij")
+    rad = np.sqrt(sum(x * x for x in g)).ravel() / 0.9
+    lab = np.where(rad < 1.0, 1 + np.minimum((rad * classes).astype(np.int64), classes - 1), 0)
+    class_atoms = rng.integers(d, size=classes + 1)
+    pd = np.where(lab > 0, rng.uniform(0.5, 1.0, size=n), 0.0)
+    pd_t = torch.as_tensor(pd, device=dev)
+    idx_t = torch.as_tensor(class_atoms[lab], device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2)
+    pat_t = torch.empty((L, m), dtype=torch.int64, device=dev)
+    for t in range(L):
+        pat_t[t] = torch.sort(torch.randperm(n, generator=gen, device=dev)[:m]).values
+    Yfm = torch.empty((L, m), dtype=torch.complex128, device=dev)
+    chunk = 25
+    for f0 in range(0, L, chunk):
+        f1 = min(L, f0 + chunk)
+        frames = (pd_t[None, :] * raw[idx_t, f0:f1].transpose(0, 1)).reshape((f1 - f0,) + shape)
+        F = torch.fft.fftn(frames, dim=(1, 2, 3), norm="ortho").reshape(f1 - f0, n)
+        Yfm[f0:f1] = torch.gather(F, 1, pat_t[f0:f1])
+        del frames, F
+    del raw
+    gen.manual_seed(3)
+    xi = torch.complex(torch.randn((L, m), generator=gen, device=dev, dtype=torch.float64),
+                       torch.randn((L, m), generator=gen, device=dev, dtype=torch.float64))
+    xi *= torch.linalg.vector_norm(Yfm) / torch.linalg.vector_norm(xi) * 10 ** (-snr_db / 20.0)
+    Yfm += xi
+    del xi
+    Y = Yfm.to(torch.complex64).transpose(0, 1).contiguous().cpu().numpy()
+    pattern = pat_t.cpu().numpy()
+    del Yfm, pat_t
+    torch.cuda.empty_cache()
+    return Cfg4(cdict=cd, pattern=pattern, spatial_shape=tuple(shape), Y=Y, labels=lab,
+                class_atoms=class_atoms, d=d, setup_seconds=time.perf_counter() - t0)

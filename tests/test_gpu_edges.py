@@ -1,8 +1,10 @@
-"""GPU edge cases of the certified tcgen05 path against the fp64 oracle.
+"""GPU edge cases of the certified tcgen05 paths (fp16 screen and split hi/lo screen) against
+the fp64 oracle.
 
-* dictionary sizes around the 160-atom tile / 128-row storage tile (sentinel rows, partial tiles)
-  and voxel counts around the 128-voxel tile;
-* s at every K-step boundary of the sentinel layout (2s + 1 = 16, 17, 32, 33, 63);
+* dictionary sizes around the 160- / 128-atom tiles and the 128-row storage tile (sentinel rows,
+  partial tiles) and voxel counts around the 128-voxel tile;
+* s at every K-step boundary of the sentinel layouts (2s + 1 = 16, 17, 32, 33, 63; split:
+  6s + 1 = 13, 19, 31, 37, 43, 49, 61);
 * voxels spanning 60 orders of magnitude (power-of-two scaling of the fp16 operands);
 * the IPG warm-start hint (random, out of range, negative) never changes the result.
 """
@@ -33,15 +35,20 @@ def _check(Z, atoms, res):
                                atol=1e-300)
 
 
-@pytest.mark.parametrize("d", [321, 479, 480, 481, 639, 640, 641, 1280])
-def test_dictionary_tile_boundaries(d):
+ALGOS = ["tcgen05", "tcgen05_split"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("d", [321, 383, 384, 385, 479, 480, 481, 511, 512, 513, 639, 640, 641,
+                               1280])
+def test_dictionary_tile_boundaries(d, algo):
     import paper_1810_01967_b200 as cb
     rng = np.random.default_rng(d)
     atoms = _atoms(rng, d, 10)
     for n in (1, 127, 128, 129, 513):
         Z = rng.standard_normal((n, 10)) + 1j * rng.standard_normal((n, 10))
         Z[0] = 2.0 * atoms[-1]               # the last (sentinel-tile) atom must be findable
-        res = cb.project_cone_exact(Z, atoms, algo="tcgen05")
+        res = cb.project_cone_exact(Z, atoms, algo=algo)
         _check(Z, atoms, res)
         assert res.indices[0] == d - 1
 
@@ -56,19 +63,42 @@ def test_k_step_boundaries(s):
     _check(Z, atoms, cb.project_cone_exact(Z, atoms))        # auto
 
 
-def test_extreme_voxel_magnitudes():
+@pytest.mark.parametrize("s", [1, 2, 3, 5, 6, 7, 8, 10])
+def test_split_k_step_boundaries(s):
+    import paper_1810_01967_b200 as cb
+    rng = np.random.default_rng(300 + s)
+    atoms = _atoms(rng, 700, s)
+    Z = rng.standard_normal((600, s)) + 1j * rng.standard_normal((600, s))
+    _check(Z, atoms, cb.project_cone_exact(Z, atoms, algo="tcgen05_split"))
+
+
+def test_split_rejects_wide_atoms():
+    import paper_1810_01967_b200 as cb
+    from paper_1810_01967_b200._lib import NativeError
+    rng = np.random.default_rng(5)
+    atoms = _atoms(rng, 700, 11)
+    Z = rng.standard_normal((10, 11)) + 1j * rng.standard_normal((10, 11))
+    with pytest.raises(NativeError):
+        cb.project_cone_exact(Z, atoms, algo="tcgen05_split")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_extreme_voxel_magnitudes(algo):
     import paper_1810_01967_b200 as cb
     rng = np.random.default_rng(77)
     atoms = _atoms(rng, 900, 10)
     Z = rng.standard_normal((400, 10)) + 1j * rng.standard_normal((400, 10))
     Z *= 10.0 ** rng.uniform(-30, 30, size=(400, 1))
     Z[5] = 1e-300 * atoms[3]                  # fp64 subnormal-range voxel
-    res = cb.project_cone_exact(Z, atoms, algo="tcgen05")
+    Z[6] = 0.0                                # zero voxel -> index 0, gamma 0
+    res = cb.project_cone_exact(Z, atoms, algo=algo)
     _check(Z, atoms, res)
     assert res.indices[5] == 3
+    assert res.indices[6] == 0 and res.gammas[6] == 0.0
 
 
-def test_warm_start_hint_never_changes_results():
+@pytest.mark.parametrize("algo", [1, 4])
+def test_warm_start_hint_never_changes_results(algo):
     """cbb_project_step with random / out-of-range hints equals the unhinted projection."""
     import paper_1810_01967_b200 as cb
     from paper_1810_01967_b200 import _lib
@@ -99,7 +129,7 @@ def test_warm_start_hint_never_changes_results():
         _lib.check(lib.cbb_project_step(Xt.data_ptr(), Gt.data_ptr(), 0.7, Z.data_ptr(), n,
                                         ctypes.byref(dd.view), None if h is None else h.data_ptr(),
                                         idx.data_ptr(), gam.data_ptr(), Xn.data_ptr(),
-                                        dX.data_ptr(), nd.data_ptr(), ws.data_ptr(), wsb, 1,
+                                        dX.data_ptr(), nd.data_ptr(), ws.data_ptr(), wsb, algo,
                                         _lib.stream_ptr()), "step")
         return idx.cpu().numpy(), gam.cpu().numpy(), Xn.cpu().numpy(), Z.cpu().numpy()
 
