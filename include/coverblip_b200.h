@@ -52,7 +52,7 @@ typedef struct cbb_dict_view {
   const void* atoms32;   /* d x 2*s_pad fp32 planar */
   const void* atoms_tc;  /* fp16 UMMA tiles (fp16-accumulated screen) */
   const float* bounds;   /* certified error bounds */
-  const void* atoms_tc2; /* split hi/lo fp16 UMMA tiles (fp32-accumulated screen), s <= 10 */
+  const void* atoms_tc2; /* split hi/lo fp16 UMMA tiles (fp32-accumulated screen), s <= 21 */
   int32_t prefer_split;  /* CBB_ALGO_AUTO uses the split screen: the dictionary is coherent
                             (its sampled atoms have near-duplicates inside the fp16 window) */
   int32_t reserved;
@@ -60,11 +60,11 @@ typedef struct cbb_dict_view {
 
 /* Projection algorithms. */
 enum {
-  CBB_ALGO_AUTO = 0,        /* split tcgen05 if prefer_split (s <= 10), else fp16 tcgen05 ... */
+  CBB_ALGO_AUTO = 0,        /* split tcgen05 if prefer_split (s <= 21), else fp16 tcgen05 ... */
   CBB_ALGO_TCGEN05 = 1,     /* fp16 operands, fp16 accumulators (2s < 64) */
   CBB_ALGO_FFMA = 2,        /* fp32 FFMA screen */
   CBB_ALGO_EXHAUSTIVE = 3,  /* fp64 scan of every atom */
-  CBB_ALGO_TCGEN05_SPLIT = 4 /* hi/lo fp16 operands, fp32 accumulators (s <= 10) */
+  CBB_ALGO_TCGEN05_SPLIT = 4 /* hi/lo fp16 operands, fp32 accumulators (s <= 21) */
 };
 
 int cbb_abi_version(void);

@@ -55,10 +55,18 @@ __host__ __device__ inline int mma_ksteps(int s) { return (2 * s + 1 + 15) / 16;
 constexpr unsigned short kF16One = 0x3C00, kF16MinusMax = 0xFBFF;  // 1.0, -65504
 
 // Split-operand screening (fp16 hi/lo operands, fp32 accumulators): voxel rows
-// [z_hi | z_lo | z_hi | 1], atom rows [d_hi | d_hi | d_lo | sentinel], K = 6s + 1 <= 64.
-constexpr int kSplitMaxS = 10;
-constexpr int kSplitKP = 64;
-__host__ __device__ inline int split_ksteps(int s) { return (6 * s + 1 + 15) / 16; }
+// [z_hi | z_lo | z_hi | 1], atom rows [d_hi | d_hi | d_lo | sentinel], K = 6s + 1 <= 128.
+// K = 64 (s <= 10): 128-atom tiles of one 128-byte swizzle block per row; K = 128 (s <= 21):
+// 64-atom tiles stored as two K blocks [block][64 rows][128 B] (one bulk copy per tile).
+constexpr int kSplitMaxS = 21;
+__host__ __device__ constexpr int split_kp(int s) { return 6 * s + 1 <= 64 ? 64 : 128; }
+__host__ __device__ constexpr int split_rows(int kp) { return kp == 64 ? 128 : 64; }
+__host__ __device__ constexpr int split_ksteps(int s) { return (6 * s + 1 + 15) / 16; }
+// byte offset of element e of row r inside one split tile of `rows` rows
+__host__ __device__ inline uint32_t split_elem_offset(int r, int e, int rows) {
+  return uint32_t(e >> 6) * uint32_t(rows) * 128u + uint32_t(r) * 128u +
+         uint32_t((((e & 63) >> 3) ^ (r & 7)) * 16) + uint32_t(e & 7) * 2u;
+}
 
 // Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.
 __host__ __device__ inline uint32_t tile_chunk_offset(int r, int c, int kpad) {

@@ -396,18 +396,19 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
 }
 
 // Split-operand tiles (s <= kSplitMaxS): row j = [d_hi (2s) | d_hi (2s) | d_lo (2s) | sentinel],
-// d_hi = fp16(scale_d d), d_lo = fp16(scale_d d - d_hi), K = 64, 128-byte swizzle.  Padded rows
-// carry -65504 in the sentinel column (their fp32-accumulated score is -65504 for every voxel).
+// d_hi = fp16(scale_d d), d_lo = fp16(scale_d d - d_hi), K = split_kp(s), 128-byte swizzle,
+// split_rows(K)-row tiles (split_elem_offset).  Padded rows carry -65504 in the sentinel column
+// (their fp32-accumulated score is -65504 for every voxel).
 __global__ void prep_tc2_kernel(const double2* __restrict__ atoms64, int64_t d, int64_t d_pad,
                                 int s, uint8_t* __restrict__ atoms_tc2,
                                 float* __restrict__ bounds) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= d_pad) return;
-  const int tile = int(j / kTileRows), r = int(j % kTileRows);
-  uint8_t* trow = atoms_tc2 + size_t(tile) * kTileRows * kSplitKP * 2;
+  const int kp = split_kp(s), rows = split_rows(kp);
+  const int tile = int(j / rows), r = int(j % rows);
+  uint8_t* trow = atoms_tc2 + size_t(tile) * rows * kp * 2;
   auto put = [&](int e, unsigned short h) {
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e >> 3, kSplitKP) +
-                                       (e & 7) * 2) = h;
+    *reinterpret_cast<unsigned short*>(trow + split_elem_offset(r, e, rows)) = h;
   };
   if (j >= d) {
     put(6 * s, kF16MinusMax);
@@ -561,9 +562,9 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   int ez;
   frexp(sqrt(nz), &ez);
   const double sv = ldexp(1.0, 13 - ez);
-  unsigned short row[64];
+  unsigned short row[128];
 #pragma unroll
-  for (int e = 0; e < 64; ++e) row[e] = 0;
+  for (int e = 0; e < 128; ++e) row[e] = 0;
   double eh = 0, nzh = 0, nlo = 0, nhi = 0;
   for (int k = 0; k < s; ++k) {
     double re, im;
@@ -913,32 +914,22 @@ __device__ long long g_trace_vt[256 * 4];  // per voxel tile of CTA 0: loop star
 // Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
 constexpr int kParts = 3;
 
-// SPLIT: hi/lo fp16 operands with fp32 accumulators (KP = 64): 128-atom tiles (N = 128 MMAs;
-// measured faster than 64-atom tiles with six stages), screened in two 64-register halves.
+// SPLIT: hi/lo fp16 operands with fp32 accumulators: KP = 64 -> 128-atom tiles (N = 128 MMAs;
+// measured faster than 64-atom tiles with six stages), screened in two 64-register halves;
+// KP = 128 -> 64-atom tiles (the 16 KB stages keep a 9-deep ring).
 template <int KP, bool SPLIT = false>
 struct TcCfg {
-  static_assert(!SPLIT || KP == kSplitKP, "split tiles are 64 wide");
-#ifndef CBB_SPLIT_CHUNKS
-#define CBB_SPLIT_CHUNKS 4
-#endif
-  static constexpr int kChunks = SPLIT ? CBB_SPLIT_CHUNKS : (KP == 32 ? 5 : 4);  // 32-atom chunks
+  static_assert(!SPLIT || KP == 64 || KP == 128, "split tiles are 64 or 128 wide");
+  // 32-atom chunks per tile (split: the tile is one split_rows(KP)-row storage tile)
+  static constexpr int kChunks = SPLIT ? split_rows(KP) / 32 : (KP == 32 ? 5 : 4);
   static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 / 64 (split)
   static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
-#ifndef CBB_SPLIT_ACC
-#define CBB_SPLIT_ACC 3
-#endif
-  static constexpr int kAcc = SPLIT ? CBB_SPLIT_ACC : 3;     // x BN accumulator columns
+  static constexpr int kAcc = 3;                             // x BN accumulator columns
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
   static constexpr int kBBytes = BN * KP * 2;
-#ifndef CBB_RING_F16_KB
-#define CBB_RING_F16_KB 96
-#endif
-#ifndef CBB_RING_SPLIT_KB
-#define CBB_RING_SPLIT_KB 144
-#endif
-  static constexpr int kRing = (SPLIT ? CBB_RING_SPLIT_KB : KP == 32 ? CBB_RING_F16_KB : 144) * 1024;
+  static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
   static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
   static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
   static constexpr int kStages = (kStagesRaw / kParts) * kParts;
@@ -1217,14 +1208,17 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
-        const uint64_t bdesc = umma_desc_kmajor(b_base + st * C::kBBytes, KP);
         const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kACols);
         const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
-        for (int kq = 0; kq < KP / 16; ++kq)
+        for (int kq = 0; kq < KP / 16; ++kq) {
+          // K-major operand: K blocks of 64 elements (128 B rows) follow each other, BN rows each
+          const uint64_t bdesc =
+              umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * BN * 128, KP < 64 ? KP : 64);
           if (kq < nks)
-            tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * kq), C::kIdesc,
+            tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)), C::kIdesc,
                           kq > 0 ? 1u : 0u);
+        }
         tc_commit(b_empty + st);
         tc_commit(t_full + tb);
         // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
@@ -1790,7 +1784,7 @@ size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc,
   // may run past the last 128-row tile
   size_t c = take(size_t(nbt + 2) * kTileRows * kp * 2);
   size_t e = take(kBCount * sizeof(float));
-  size_t f = take(s <= kSplitMaxS ? size_t(nbt + 2) * kTileRows * kSplitKP * 2 : 0);
+  size_t f = take(s <= kSplitMaxS ? size_t(nbt + 2) * kTileRows * split_kp(s) * 2 : 0);
   if (offtc2) *offtc2 = f;
   if (off64) *off64 = a;
   if (off32) *off32 = b;
@@ -1880,7 +1874,7 @@ constexpr int kReduceBlocks = 256;
 constexpr int kVoxPad = 512;  // voxel tiles are padded to a multiple of the largest TC voxel tile
 
 size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
-  const int kp = s <= kSplitMaxS ? kSplitKP : kpad_for(s);  // split rows are 64 wide
+  const int kp = s <= kSplitMaxS ? split_kp(s) : kpad_for(s);  // split rows are wider
   const int64_t n_vt = (n + kVoxPad - 1) / kVoxPad;
   size_t o = 0;
   uint8_t* base = static_cast<uint8_t*>(base_ptr);
@@ -2064,10 +2058,10 @@ int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStr
   return kOk;
 }
 
-// algo: 0 = auto (split tcgen05 for coherent dictionaries with s <= 10, else tcgen05 when
+// algo: 0 = auto (split tcgen05 for coherent dictionaries with s <= 21, else tcgen05 when
 // 2s < 64, else FFMA / fp64),
 // 1 = tcgen05 (fp16 accumulators), 2 = FFMA, 3 = exhaustive fp64, 4 = split tcgen05 (hi/lo fp16
-// operands, fp32 accumulators)
+// operands, fp32 accumulators, s <= 21)
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st) {
   if (n < 0) return kErrArgument;
@@ -2096,13 +2090,14 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
-        zs, n, n_pad, dv.s, split ? kSplitKP : dv.kpad, dv.bounds,
+        zs, n, n_pad, dv.s, split ? split_kp(dv.s) : dv.kpad, dv.bounds,
         algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
         algo == 1 ? w.init_tc : nullptr, split ? 1 : 0);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
-    int rc = split ? launch_tc<kSplitKP, true>(w, n, zr, dv, o, max_ctas, st)
+    int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, o, max_ctas, st)
+                                           : launch_tc<128, true>(w, n, zr, dv, o, max_ctas, st))
              : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
                                             : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
                            : dispatch_ffma(w, n, zr, dv, o, st);

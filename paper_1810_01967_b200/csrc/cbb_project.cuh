@@ -7,7 +7,7 @@
 //
 // B200 design: a screening pass scores every (voxel, atom) pair in low
 // precision (fp16 tcgen05 MMA with fp16 accumulation; split hi/lo fp16 operands with fp32
-// accumulation for s <= 10; or fp32 FFMA) and keeps, per voxel, every atom
+// accumulation for s <= 21; or fp32 FFMA) and keeps, per voxel, every atom
 // whose approximate score lies inside a CERTIFIED window below the running
 // maximum (window = 2 * rigorous bound on |approx - exact|).  The surviving
 // candidates are rescored in fp64 from the caller's own atoms and voxels, so
@@ -31,8 +31,8 @@ struct DictView {
   const float* atoms32;        // d x 2*s_pad planar fp32 [re.., im..]
   const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad fp16 (atoms * scale), swizzled
   const float* bounds;         // kB* slots below
-  const uint8_t* atoms_tc2;    // split-operand tiles (s <= kSplitMaxS, else null): 128-row
-                               // swizzled tiles of 64 fp16 [d_hi | d_hi | d_lo | sentinel]
+  const uint8_t* atoms_tc2;    // split-operand tiles (s <= kSplitMaxS, else null): swizzled
+                               // rows of split_kp(s) fp16 [d_hi | d_hi | d_lo | sentinel]
   int32_t prefer_split;        // auto mode screens with the split tiles (coherent dictionary)
 };
 

@@ -209,5 +209,5 @@ def solve_compressed_sharded(Y, A, cdict, config, gt=None, group=None, on_iter=N
         idx = idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
         gam = gam.cpu().numpy() if have_proj else np.zeros(n)
         maps = _maps_from(cdict, idx, gam)
-        out = _image_to_host(Xs @ st.V_full.conj().transpose(0, 1))
+        out = _image_to_host(Xs, st.V_full)
         return out, maps, gam, trace

@@ -156,8 +156,18 @@ class IpgState:
         self.dim = self.dd.s
         self.V = (None if basis is None else
                   torch.from_numpy(np.ascontiguousarray(basis, dtype=np.complex64)).to(device))
-        Yfm = np.ascontiguousarray(np.asarray(Y).T, dtype=np.complex64)
-        self.Y = torch.from_numpy(Yfm).to(device)                      # (L, c*m)
+        # upload in the caller's layout and precision; ||Y|| (fp64) and the frame-major complex64
+        # copy are formed on the device (no host transpose / cast of the measurements)
+        Yh = np.asarray(Y)
+        if Yh.shape != (self.cm, self.L):
+            raise ValueError(f"measurements are {Yh.shape}, the operator expects "
+                             f"{(self.cm, self.L)}")
+        if not np.iscomplexobj(Yh):
+            Yh = Yh.astype(np.complex128)
+        Yd = torch.from_numpy(np.ascontiguousarray(Yh)).to(device)     # (c*m, L)
+        self.y_norm = float(torch.linalg.vector_norm(torch.view_as_real(Yd), dtype=torch.float64))
+        self.Y = Yd.transpose(0, 1).to(torch.complex64).contiguous()   # (L, c*m)
+        del Yd
         self.w = (None if weights is None else torch.from_numpy(np.ascontiguousarray(
             np.broadcast_to(weights, np.asarray(Y).shape).T, dtype=np.float32)).to(device))
         c64 = dict(dtype=torch.complex64, device=device)
@@ -253,14 +263,51 @@ class IpgState:
         return Xs if self.V is None else Xs @ self.V.conj().transpose(0, 1)
 
 
-def _image_to_host(X: torch.Tensor) -> np.ndarray:
-    """(n, L) device image -> complex128 numpy (the reference's return type): upcast on the
-    GPU, one D2H into a pinned buffer (torch's caching host allocator reuses it)."""
-    Xd = X.to(torch.complex128)
-    host = torch.empty(Xd.shape, dtype=torch.complex128, pin_memory=True)
-    host.copy_(Xd, non_blocking=True)
-    torch.cuda.current_stream(X.device).synchronize()
-    return host.numpy()
+_STAGE_BYTES = 256 << 20
+_copy_pool = None
+
+
+def _image_to_host(Xs: torch.Tensor, V: torch.Tensor = None) -> np.ndarray:
+    """Image series X = Xs V^H (or Xs itself when V is None) -> (n, L) complex128 numpy (the
+    reference's return type) without materialising it on the device: voxel chunks are
+    decompressed and upcast on the GPU, copied into one of two reusable pinned staging buffers,
+    and moved into the (pageable) result by host threads while the next chunk is copied."""
+    global _copy_pool
+    from concurrent.futures import ThreadPoolExecutor
+    n = int(Xs.shape[0])
+    L = int(Xs.shape[1]) if V is None else int(V.shape[0])
+    out = np.empty((n, L), dtype=np.complex128)
+    if n == 0 or L == 0:
+        return out
+    Vh = None if V is None else V.conj().transpose(0, 1)
+    rows = max(1, min(n, _STAGE_BYTES // (16 * L)))
+    bufs = [torch.empty((rows, L), dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+    if _copy_pool is None:
+        _copy_pool = ThreadPoolExecutor(max_workers=8)
+    pending = [[], []]
+    stream = torch.cuda.current_stream(Xs.device)
+
+    def drain(ev, src, dst):
+        ev.synchronize()
+        np.copyto(dst, src)
+
+    for k, r0 in enumerate(range(0, n, rows)):
+        b = k & 1
+        for f in pending[b]:
+            f.result()                     # the host copy out of this buffer has finished
+        r1 = min(n, r0 + rows)
+        blk = Xs[r0:r1] if Vh is None else Xs[r0:r1] @ Vh
+        bufs[b][:r1 - r0].copy_(blk.to(torch.complex128), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        src = bufs[b].numpy()
+        parts = np.linspace(0, r1 - r0, 9).astype(int)
+        pending[b] = [_copy_pool.submit(drain, ev, src[a:c], out[r0 + a:r0 + c])
+                      for a, c in zip(parts[:-1], parts[1:]) if c > a]
+    for p in pending:
+        for f in p:
+            f.result()
+    return out
 
 
 def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
@@ -345,7 +392,7 @@ def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
 
 def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_device=False):
     """Device IPG loop following solver.py:155-257."""
-    Ynp = np.asarray(Y, dtype=complex)
+    Ynp = np.asarray(Y)
     Ad = as_device_operator(A)
     dev = Ad.device
     weights = None
@@ -364,7 +411,7 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
             mu_base = config.mu_init
         else:
             mu_base = n / Ad.m
-        y_norm = float(np.linalg.norm(Ynp))
+        y_norm = st.y_norm
         gt_t = None
         if gt is not None:
             gt_data = gt.data if hasattr(gt, "data") and not isinstance(gt, np.ndarray) else gt
@@ -379,7 +426,7 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
         idx = st.idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
         gam = st.gam.cpu().numpy() if have_proj else np.zeros(n)
         maps = _maps_from(dictionary, idx, gam)
-        out = _image_to_host(st.decompress(st.X))
+        out = _image_to_host(st.X, st.V)
         return out, maps, gam, trace
 
 

@@ -10,6 +10,26 @@ from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_
 from paper_1810_01967_b200.solver import SolverConfig, solve_compressed
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+
+# wall-time breakdown of the solve wrapper (state construction, output conversion)
+import paper_1810_01967_b200.solver as _sv
+_T = {}
+
+
+def _timed(name, fn):
+    def w(*a, **k):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn(*a, **k)
+        torch.cuda.synchronize()
+        _T[name] = _T.get(name, 0.0) + time.perf_counter() - t0
+        return r
+    return w
+
+
+_sv.IpgState.__init__ = _timed("state_init", _sv.IpgState.__init__)
+_sv._image_to_host = _timed("image_to_host", _sv._image_to_host)
+_sv._maps_from = _timed("maps_from", _sv._maps_from)
 dev = torch.device("cuda:0")
 t = time.perf_counter()
 cfg = workloads.make_cfg4(device=dev)
@@ -33,7 +53,8 @@ for it in ((1,) if prof else (1, iters)):
         torch.cuda.profiler.stop()
     trials = sum(r["shrinks"] + 1 for r in trace.records)
     print(f"iters {trace.iterations} trials {trials} wall {dt:.2f}s loop {trace.total_time:.2f}s "
-          f"fid {trace.fidelities()[-1]:.4g}", flush=True)
+          f"fid {trace.fidelities()[-1]:.4g}  breakdown {_T}", flush=True)
+    _T.clear()
     from paper_1810_01967_b200.projection import overflow_counts
     print("   overflow_counts (exhaustive, warp-rescored) of last projection:",
           overflow_counts(A.n, 10), "of", A.n, flush=True)

@@ -87,3 +87,15 @@ if "coh" in which:
         rng.standard_normal((n, 10)) + 1j * rng.standard_normal((n, 10)))
     dd = device_dictionary(atoms, dev)
     compare("cfg4-coh", torch.from_numpy(Z.astype(np.complex64)).to(dev), dd)
+if "coh20" in which:
+    cd, raw = workloads._offres_dictionary(1000, 20, 100, 100, 21, dev)
+    atoms = cd.atoms_compressed
+    del raw
+    rng = np.random.default_rng(2)
+    n = 65536
+    idx = rng.integers(len(atoms), size=n)
+    Z = atoms[idx] * rng.uniform(0.5, 1, size=(n, 1)) + 0.3 / np.sqrt(40) * (
+        rng.standard_normal((n, 20)) + 1j * rng.standard_normal((n, 20)))
+    dd = device_dictionary(atoms, dev)
+    print("coh20 prefer_split", dd.prefer_split, "coherence", dd.bounds()["coherence"])
+    compare("cfg2-coh", torch.from_numpy(Z.astype(np.complex64)).to(dev), dd)

@@ -4,7 +4,7 @@ the fp64 oracle.
 * dictionary sizes around the 160- / 128-atom tiles and the 128-row storage tile (sentinel rows,
   partial tiles) and voxel counts around the 128-voxel tile;
 * s at every K-step boundary of the sentinel layouts (2s + 1 = 16, 17, 32, 33, 63; split:
-  6s + 1 = 13, 19, 31, 37, 43, 49, 61);
+  6s + 1 = 13, 19, 31, 37, 43, 49, 61 | 67, 79, 85, 91, 97, 109, 115, 127);
 * voxels spanning 60 orders of magnitude (power-of-two scaling of the fp16 operands);
 * the IPG warm-start hint (random, out of range, negative) never changes the result.
 """
@@ -63,7 +63,7 @@ def test_k_step_boundaries(s):
     _check(Z, atoms, cb.project_cone_exact(Z, atoms))        # auto
 
 
-@pytest.mark.parametrize("s", [1, 2, 3, 5, 6, 7, 8, 10])
+@pytest.mark.parametrize("s", [1, 2, 3, 5, 6, 7, 8, 10, 11, 13, 14, 15, 16, 18, 19, 21])
 def test_split_k_step_boundaries(s):
     import paper_1810_01967_b200 as cb
     rng = np.random.default_rng(300 + s)
@@ -76,8 +76,8 @@ def test_split_rejects_wide_atoms():
     import paper_1810_01967_b200 as cb
     from paper_1810_01967_b200._lib import NativeError
     rng = np.random.default_rng(5)
-    atoms = _atoms(rng, 700, 11)
-    Z = rng.standard_normal((10, 11)) + 1j * rng.standard_normal((10, 11))
+    atoms = _atoms(rng, 700, 22)
+    Z = rng.standard_normal((10, 22)) + 1j * rng.standard_normal((10, 22))
     with pytest.raises(NativeError):
         cb.project_cone_exact(Z, atoms, algo="tcgen05_split")
 

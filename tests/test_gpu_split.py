@@ -42,10 +42,16 @@ def _voxels(rng, atoms, n, noise):
     return Z
 
 
+@pytest.fixture(scope="module")
+def coherent_atoms20():
+    return _coherent(s=20)
+
+
+@pytest.mark.parametrize("s", [10, 20])
 @pytest.mark.parametrize("noise", [0.0, 0.02, 0.3])
-def test_all_screens_agree_on_coherent_dictionary(coherent_atoms, noise):
+def test_all_screens_agree_on_coherent_dictionary(coherent_atoms, coherent_atoms20, noise, s):
     import paper_1810_01967_b200 as cb
-    atoms = coherent_atoms
+    atoms = coherent_atoms if s == 10 else coherent_atoms20
     rng = np.random.default_rng(int(noise * 100) + 1)
     Z = _voxels(rng, atoms, 5000, noise)
     dd = cb.device_dictionary(atoms)
@@ -86,8 +92,8 @@ def test_auto_screen_follows_coherence(coherent_atoms):
     assert not d_rand.prefer_split
     assert d_coh.prefer_split
     assert d_coh.bounds()["coherence"] > 1.0 > d_rand.bounds()["coherence"]
-    # s > 10: no split tiles, never preferred
-    wide = rng.standard_normal((4000, 12)) + 1j * rng.standard_normal((4000, 12))
+    # s > 21: no split tiles, never preferred
+    wide = rng.standard_normal((4000, 22)) + 1j * rng.standard_normal((4000, 22))
     assert not cb.device_dictionary(wide).prefer_split
 
 
