@@ -195,42 +195,60 @@ def ipg_rate(device):
             "final_fidelity": trace.fidelities()[-1]}
 
 
-def ipg_rate_cfg2(device, peaks, world=1):
-    """BASELINE configs[2] IPG (256x256, L=1000, D=120,624 off-resonance atoms, s=20, EPI 16/256
-    lines, 30 iterations) through the public solve_compressed -- or, under torchrun, through
-    sharded.solve_compressed_sharded over all ranks (voxel-sharded projection, frame-sharded
-    operator; wall time = max over ranks) -- with the SURVEY 8d roofline model of one
-    iteration (materialised-frame byte model + r projections on the tensor cores)."""
+LARGE_IPG = {
+    "cfg2": dict(make="make_cfg2", s=20, iters=30,
+                 config="BASELINE configs[2] (256x256, L=1000, D=120624 = T1 100 x T2 100 (T2<T1) "
+                        "x dB0 21 Bloch IR-bSSFP atoms, s=20, EPI 16/256 lines, 30 dB, zeta=2, "
+                        "max 30 iters)"),
+    "cfg4": dict(make="make_cfg4", s=10, iters=20,
+                 config="BASELINE configs[4] (256x256x64 ellipsoid phantom, 6 classes, "
+                        "PD~U(0.5,1), L=500, D=149344 = T1 100 x T2 100 (T2<T1) x dB0 26 Bloch "
+                        "IR-bSSFP atoms, s=10, per-frame random Cartesian masks at 1/16 of "
+                        "k-space, 30 dB, zeta=2, 20 iters)"),
+}
+
+
+def ipg_rate_large(device, peaks, which, world=1):
+    """BASELINE configs[2] / configs[4] IPG through the public solve_compressed -- or, under
+    torchrun, through sharded.solve_compressed_sharded over all ranks (voxel-sharded
+    projection, frame-sharded operator; times = max over ranks) -- with the SURVEY 8d roofline
+    model of one iteration (materialised-frame byte model + r projections on the tensor
+    cores).  iters_per_s uses the IPG loop time; solve_seconds is the whole public call
+    (state upload, loop, the (n, L) complex128 image and the maps back on the host)."""
     import torch
     from paper_1810_01967_b200 import workloads
     from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
     from paper_1810_01967_b200.solver import SolverConfig, solve_compressed
-    cfg = workloads.make_cfg2(device=device)
+    spec = LARGE_IPG[which]
+    s = spec["s"]
+    cfg = getattr(workloads, spec["make"])(device=device)
     A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape), device=device)
     solve = solve_compressed
     if world > 1:
         import torch.distributed as dist
         from paper_1810_01967_b200.sharded import solve_compressed_sharded
         solve = solve_compressed_sharded
+
     def run(conf):
         if world == 1:
             return solve(cfg.Y, A, cfg.cdict, None, conf)
         return solve(cfg.Y, A, cfg.cdict, conf)
 
-    run(SolverConfig(mode="blip_exact", max_iters=2, zeta=2.0, compressed=20))   # warm-up
-    conf = SolverConfig(mode="blip_exact", max_iters=30, zeta=2.0, compressed=20)
+    run(SolverConfig(mode="blip_exact", max_iters=2, zeta=2.0, compressed=s))   # warm-up
+    conf = SolverConfig(mode="blip_exact", max_iters=spec["iters"], zeta=2.0, compressed=s)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     X, maps, gam, trace = run(conf)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    loop = trace.total_time
     if world > 1:
-        t = torch.tensor([dt], dtype=torch.float64, device=device)
+        t = torch.tensor([dt, loop], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t)
+        dt, loop = float(t[0]), float(t[1])
     its = trace.iterations
     trials = sum(r["shrinks"] + 1 for r in trace.records)
-    n, L, m, s, D = 256 * 256, 1000, A.m, 20, cfg.d
+    n, L, m, D = int(np.prod(cfg.spatial_shape)), A.L, A.m, cfg.d
     r = trials / its
     b_a = 8 * (n * s + 3 * n * L + 2 * m * L)
     b_ah = 8 * (m * L + 4 * n * L + n * s)
@@ -240,15 +258,13 @@ def ipg_rate_cfg2(device, peaks, world=1):
     bw = float(peaks.get("hbm_gbs", 6555.2)) * 1e9 * world       # aggregate over the ranks
     tc = float(peaks.get("bf16_tflops", 1605.7)) * 1e12 * world
     t_roof = b_iter / bw + r * f_p / tc
-    t_meas = dt / its
-    return {"config": "BASELINE configs[2] (256x256, L=1000, D=120624 = T1 100 x T2 100 (T2<T1) "
-                      "x dB0 21 Bloch IR-bSSFP atoms, s=20, EPI 16/256 lines, 30 dB, zeta=2, "
-                      "max 30 iters)",
-            "n_gpus": world, "sharding": "none" if world == 1 else
+    t_meas = loop / its
+    return {"config": spec["config"], "n_gpus": world,
+            "sharding": "none" if world == 1 else
             "voxel-sharded state/projection, frame-sharded s-channel operator (NCCL)",
             "setup_seconds": cfg.setup_seconds, "iterations": its, "projection_trials": trials,
-            "seconds": dt, "iters_per_s": its / dt, "ms_per_iter": 1e3 * t_meas,
-            "final_fidelity": trace.fidelities()[-1],
+            "loop_seconds": loop, "solve_seconds": dt, "iters_per_s": its / loop,
+            "ms_per_iter": 1e3 * t_meas, "final_fidelity": trace.fidelities()[-1],
             "roofline_model": {
                 "model": "SURVEY 8d: B_iter(r) = B_AH + 24mL + r(B_P + B_A + 16mL) bytes at HBM "
                          "peak + r 4snD flops at the dense tensor peak (materialised n x L "
@@ -396,12 +412,16 @@ def run_ours(args, rank, world, local_rank):
         except Exception as exc:  # report, never hide
             cfg3 = {"error": repr(exc)}
         torch.cuda.empty_cache()
-    ipg2_multi = None
-    if world > 1 and not args.skip_cfg2:       # every rank takes part (collectives)
-        try:
-            ipg2_multi = ipg_rate_cfg2(dev, measured_peaks()[0], world)
-        except Exception as exc:  # report, never hide
-            ipg2_multi = {"error": repr(exc)}
+    ipg_multi = {}
+    if world > 1:                               # every rank takes part (collectives)
+        for which in ("cfg2", "cfg4"):
+            if getattr(args, f"skip_{which}"):
+                continue
+            try:
+                ipg_multi[which] = ipg_rate_large(dev, measured_peaks()[0], which, world)
+            except Exception as exc:  # report, never hide
+                ipg_multi[which] = {"error": repr(exc)}
+            torch.cuda.empty_cache()
     if rank != 0:
         return 0
     peaks, peak_kind = measured_peaks()
@@ -439,8 +459,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "argmax_re_vs_generator": agree,
     }
-    if ipg2_multi is not None:
-        line["ipg_cfg2"] = ipg2_multi
+    for which, res in ipg_multi.items():
+        line[f"ipg_{which}"] = res
     if cfg3 is not None:
         line["cfg3"] = cfg3
     if world == 1:
@@ -449,11 +469,14 @@ def run_ours(args, rank, world, local_rank):
             line["ipg"] = ipg_rate(dev)
         except Exception as exc:  # report, never hide
             line["ipg"] = {"error": repr(exc)}
-        if not args.skip_cfg2:
+        for which in ("cfg2", "cfg4"):
+            if getattr(args, f"skip_{which}"):
+                continue
             try:
-                line["ipg_cfg2"] = ipg_rate_cfg2(dev, peaks)
+                line[f"ipg_{which}"] = ipg_rate_large(dev, peaks, which)
             except Exception as exc:  # report, never hide
-                line["ipg_cfg2"] = {"error": repr(exc)}
+                line[f"ipg_{which}"] = {"error": repr(exc)}
+            torch.cuda.empty_cache()
     print(json.dumps(line), flush=True)
     return 0
 
@@ -467,6 +490,8 @@ def main():
     ap.add_argument("--skip-cfg2", action="store_true", help="skip the cfg2 IPG measurement")
     ap.add_argument("--skip-cfg3", action="store_true",
                     help="skip the cfg3 (8.4M voxels x 2^20 atoms) projection")
+    ap.add_argument("--skip-cfg4", action="store_true",
+                    help="skip the cfg4 (256x256x64, L=500) 3-D IPG measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
