@@ -127,7 +127,21 @@ __global__ void __launch_bounds__(256) channels_kernel(const float2* __restrict_
   }
 }
 
-// y[t][ci*m + i] = scale * sum_k K[(ci*s + k)*n + Omega_t(i)] * conj(V[t*s + k]);
+// KT[(ci*n + w)*s + k] = K[(ci*s + k)*n + w]: channel-planar FFT output -> location-major, so
+// the gather reads one contiguous s-vector per sample instead of s scattered sectors.
+__global__ void __launch_bounds__(256) interleave_kernel(const float2* __restrict__ K, int c,
+                                                         int s, int64_t n,
+                                                         float2* __restrict__ KT) {
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= int64_t(c) * n) return;
+  const int ci = int(g / n);
+  const int64_t w = g - int64_t(ci) * n;
+  const float2* src = K + int64_t(ci) * s * n + w;
+  float2* dst = KT + g * s;
+  for (int k = 0; k < s; ++k) dst[k] = src[int64_t(k) * n];
+}
+
+// y[t][ci*m + i] = scale * sum_k KT[(ci*n + Omega_t(i))*s + k] * conj(V[t*s + k]);
 // modes as gather_kernel (0 write, 1 norm only, 2 weighted residual y - Ymeas).
 __global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict__ K,
                                                        const int* __restrict__ pat, int64_t n,
@@ -148,11 +162,23 @@ __global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict_
     const int r = int(e - t * cm);
     const int ci = r / m, i = r - ci * m;
     const int64_t wloc = pat[t * m + i];
-    const float2* kb = K + int64_t(ci) * s * n + wloc;
+    const float2* kb = K + (int64_t(ci) * n + wloc) * s;
     const float2* vt = V + t * s;
     float yr = 0.f, yi = 0.f;
-    for (int k = 0; k < s; ++k) {
-      const float2 a = kb[int64_t(k) * n], b = vt[k];
+    int k = 0;
+    if ((s & 1) == 0) {  // 16-byte loads of the contiguous s-vector
+      const float4* kb4 = reinterpret_cast<const float4*>(kb);
+      for (; k < s; k += 2) {
+        const float4 a2 = kb4[k >> 1];
+        const float2 b0 = vt[k], b1 = vt[k + 1];
+        yr = fmaf(a2.x, b0.x, fmaf(a2.y, b0.y, yr));   // a * conj(b)
+        yi = fmaf(a2.y, b0.x, fmaf(-a2.x, b0.y, yi));
+        yr = fmaf(a2.z, b1.x, fmaf(a2.w, b1.y, yr));
+        yi = fmaf(a2.w, b1.x, fmaf(-a2.z, b1.y, yi));
+      }
+    }
+    for (; k < s; ++k) {
+      const float2 a = kb[k], b = vt[k];
       yr = fmaf(a.x, b.x, fmaf(a.y, b.y, yr));   // a * conj(b)
       yi = fmaf(a.y, b.x, fmaf(-a.x, b.y, yi));
     }
@@ -176,31 +202,42 @@ __global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict_
 }
 
 // K[(ci*s + k)*n + w] = sum over the pattern entries e = t*m + i with Omega_t(i) = w (CSR,
-// ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per (k-space location, channel k):
-// unsampled locations get 0 (the zero-fill of forward_model.py:160-162).
+// ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per k-space location: each sample of
+// R is read once and feeds all s channel accumulators (registers, S >= s); unsampled locations
+// get 0 (the zero-fill of forward_model.py:160-162).  Consecutive threads write consecutive
+// locations of each channel.
+template <int S>
 __global__ void __launch_bounds__(256) kspace_s_kernel(const float2* __restrict__ R,
                                                        const int* __restrict__ csr_off,
                                                        const int64_t* __restrict__ csr_e,
                                                        int64_t n, int m, int c, int s,
                                                        const float2* __restrict__ V,
                                                        float2* __restrict__ K) {
-  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g >= n * s) return;
-  const int k = int(g / n);
-  const int64_t wloc = g - int64_t(k) * n;  // consecutive threads: consecutive locations
+  const int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (wloc >= n) return;
   const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
   const int64_t cm = int64_t(c) * m;
   for (int ci = 0; ci < c; ++ci) {
-    float2 acc = make_float2(0.f, 0.f);
+    float2 acc[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) acc[k] = make_float2(0.f, 0.f);
     for (int j = b; j < e_end; ++j) {
       const int64_t e = csr_e[j];
       const int64_t t = e / m, i = e - t * m;
       const float2 r = R[t * cm + int64_t(ci) * m + i];
-      const float2 v = V[t * s + k];
-      acc.x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc.x));
-      acc.y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc.y));
+      const float2* vt = V + t * s;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        if (k < s) {
+          const float2 v = vt[k];
+          acc[k].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[k].x));
+          acc[k].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[k].y));
+        }
+      }
     }
-    K[(int64_t(ci) * s + k) * n + wloc] = acc;
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (k < s) K[(int64_t(ci) * s + k) * n + wloc] = acc[k];
   }
 }
 
@@ -322,7 +359,8 @@ struct Op {
   int c;                 // coils (measurement columns per frame: c * m)
   const float2* coils;   // c x n device coil maps (caller-owned), nullptr = all ones
   const int* pattern;
-  cufftHandle plan;      // batch L (uncompressed frame stacks)
+  cufftHandle plan;      // batch L (uncompressed frame stacks), created on first use
+  bool plan_ready;
   int chan_batch[4];     // cached plans for batches of c*s channel images
   cufftHandle chan_plan[4];
   int* csr_off;          // n + 1 offsets into csr_e (s-channel adjoint)
@@ -337,10 +375,11 @@ static int grid_for(int64_t work, int per_block = 256) {
   return int(g > 0 ? g : 1);
 }
 
-// workspace: max(frame stack L*n, c*32 channel images) + per-coil reduction partials
+// workspace: max(frame stack L*n, 2 x c*32 channel images: planar FFT buffer + its
+// location-major copy) + per-coil reduction partials
 static size_t ws_main_bytes(const Op* op) {
   const size_t frames = size_t(op->L) * op->n * sizeof(float2);
-  const size_t chans = size_t(op->c) * 32 * op->n * sizeof(float2);
+  const size_t chans = size_t(op->c) * 64 * op->n * sizeof(float2);
   return ((frames > chans ? frames : chans) + 255) & ~size_t(255);
 }
 size_t op_ws_bytes(const Op* op) {
@@ -402,12 +441,6 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int f
   op->pattern = pattern;
   op->identity = (flags & 1) != 0;
   op->scale = op->identity ? 1.f : float(1.0 / std::sqrt(double(op->n)));
-  if (!op->identity) {
-    if (int rc = make_plan(op, L, &op->plan)) {
-      delete op;
-      return rc;
-    }
-  }
   if (int rc = build_csr(op)) {
     op_destroy(op);
     return rc;
@@ -426,7 +459,7 @@ int op_set_coils(Op* op, int c, const float2* coils) {
 int op_destroy(Op* op) {
   if (!op) return kOk;
   if (!op->identity) {
-    if (op->plan) cufftDestroy(op->plan);
+    if (op->plan_ready) cufftDestroy(op->plan);
     for (int i = 0; i < 4; ++i)
       if (op->chan_batch[i]) cufftDestroy(op->chan_plan[i]);
   }
@@ -448,6 +481,10 @@ static int exec_fft(cufftHandle plan, float2* F, int dir, cudaStream_t st) {
 
 static int fft(Op* op, float2* F, int dir, cudaStream_t st) {
   if (op->identity) return kOk;
+  if (!op->plan_ready) {  // frame-stack plan (batch L): built on first uncompressed use
+    if (int rc = make_plan(op, op->L, &op->plan)) return rc;
+    op->plan_ready = true;
+  }
   return exec_fft(op->plan, F, dir, st);
 }
 
@@ -521,15 +558,19 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   CBB_CUDA_TRY(cudaGetLastError());
   int rc = fft_channels(op, C, op->c * s, CUFFT_FORWARD, st);
   if (rc) return rc;
+  float2* KT = C + size_t(op->c) * s * op->n;
+  interleave_kernel<<<unsigned((int64_t(op->c) * op->n + 255) / 256), 256, 0, st>>>(
+      C, op->c, s, op->n, KT);
+  CBB_CUDA_TRY(cudaGetLastError());
   double* part = ws_partial(op, ws);
   int mode = 0;
   if (Y == nullptr) mode = 1;
   else if (Ymeas != nullptr) mode = 2;
-  gather_s_kernel<<<kRedBlocks, 256, 0, st>>>(C, op->pattern, op->n, op->L, op->m, op->c, s, V,
+  gather_s_kernel<<<kRedBlocks, 256, 0, st>>>(KT, op->pattern, op->n, op->L, op->m, op->c, s, V,
                                               op->scale, mode, Ymeas, w, Y,
                                               (mode != 0 || norm_out) ? part : nullptr);
   CBB_CUDA_TRY(cudaGetLastError());
-  count_launches(norm_out ? 3 : 2);
+  count_launches(norm_out ? 4 : 3);
   if (norm_out) return finish(part, kRedBlocks, norm_out, st);
   return kOk;
 }
@@ -539,8 +580,20 @@ int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float
                           cudaStream_t st) {
   if (s < 1 || s > 32) return kErrUnsupported;
   float2* K = ws_frames(ws);
-  kspace_s_kernel<<<unsigned((op->n * s + 255) / 256), 256, 0, st>>>(
-      R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, V, K);
+  {
+    const unsigned grid = unsigned((op->n + 255) / 256);
+#define CBB_KSPACE(SP)                                                                    \
+  kspace_s_kernel<SP><<<grid, 256, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, \
+                                            V, K)
+    if (s <= 4) CBB_KSPACE(4);
+    else if (s <= 8) CBB_KSPACE(8);
+    else if (s <= 12) CBB_KSPACE(12);
+    else if (s <= 16) CBB_KSPACE(16);
+    else if (s <= 20) CBB_KSPACE(20);
+    else if (s <= 24) CBB_KSPACE(24);
+    else CBB_KSPACE(32);
+#undef CBB_KSPACE
+  }
   CBB_CUDA_TRY(cudaGetLastError());
   int rc = fft_channels(op, K, op->c * s, CUFFT_INVERSE, st);
   if (rc) return rc;
