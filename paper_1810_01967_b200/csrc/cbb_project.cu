@@ -1097,6 +1097,25 @@ __device__ __forceinline__ void screen_tile_f32(const uint32_t (&r)[32 * NC], in
   }
 }
 
+// Max of a tile's scores (warm-start hint tiles: the max over the voxel tile's hint atoms is a
+// lower bound on the approximate max over the dictionary -- same fp16 rows, same MMA result
+// per (voxel, atom) pair -- so it seeds the running max like init_tc; nothing is recorded).
+template <int NC>
+__device__ __forceinline__ float tile_max_f32(const uint32_t (&r)[32 * NC]) {
+  float a = __uint_as_float(r[0]);
+#pragma unroll
+  for (int i = 1; i + 1 < 32 * NC; i += 2)
+    a = fmax3f(a, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+  return fmaxf(a, __uint_as_float(r[32 * NC - 1]));
+}
+template <int NC>
+__device__ __forceinline__ __half tile_max_f16(const uint32_t (&r)[16 * NC]) {
+  __half2 a = as_h2(r[0]);
+#pragma unroll
+  for (int i = 1; i + 1 < 16 * NC; i += 2) a = hmax3(a, as_h2(r[i]), as_h2(r[i + 1]));
+  return hmax_halves(__hmax2(a, as_h2(r[16 * NC - 1])));
+}
+
 template <int KP>
 __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrows, int64_t v,
                                                 bool live, uint32_t taddr) {
@@ -1122,7 +1141,8 @@ template <int KP, bool SPLIT>
 __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
-                 DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta) {
+                 DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta,
+                 const uint8_t* __restrict__ hint_tiles, int n_hint) {
   using C = TcCfg<KP, SPLIT>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -1140,7 +1160,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
   const int nB = int((d + BN - 1) / BN);
   const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
   const int my_vts = (n_vt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
-  const uint32_t total = uint32_t(my_vts) * uint32_t(nB);  // this CTA's atom tiles
+  // per voxel tile: n_hint warm-start tiles (the voxel tile's own hint atoms, each hint tile
+  // repeated for the kParts parts: tile qt -> hint tile qt / kParts), then the nB atom tiles
+  const int T = nB + n_hint;
+  const uint32_t total = uint32_t(my_vts) * uint32_t(T);  // this CTA's tiles
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -1170,16 +1193,19 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < my_vts; ++it) {
+      const int vt = int(blockIdx.x) + it * int(gridDim.x);
       int ba = rot;
-      for (int b = 0; b < nB; ++b) {
+      for (int b = 0; b < T; ++b) {
         mbar_wait(b_empty + st, ph ^ 1u);
         if (elect_one()) {
+          const uint8_t* src =
+              b < n_hint ? hint_tiles + (size_t(vt) * (n_hint / kParts) + b / kParts) * C::kBBytes
+                         : atiles + size_t(ba) * C::kBBytes;
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
-          bulk_g2s(smem + C::kOffB + st * C::kBBytes, atiles + size_t(ba) * C::kBBytes,
-                   C::kBBytes, b_full + st, pol_b);
+          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, C::kBBytes, b_full + st, pol_b);
         }
         __syncwarp();
-        if (++ba == nB) ba = 0;
+        if (b >= n_hint && ++ba == nB) ba = 0;
         if (++st == C::kStages) {
           st = 0;
           ph ^= 1u;
@@ -1200,7 +1226,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
       if (kk >= vt_end) {  // first tile of this issuer in a new voxel tile: wait for its A
         ++itk;
-        vt_end += uint32_t(nB);
+        vt_end += uint32_t(T);
         mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
       if (lane == 0) CBB_STAMP(4, kk);
@@ -1262,8 +1288,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     int tb = part;                 // its completion barrier kk % kTBars, phase (kk / kTBars) & 1
     uint32_t ph = 0;
     int rel = part + C::kAcc;      // release barrier (kk + kAcc) % kStages
-    int ba = rot + part;           // atom tile (rot + kk) % nB
-    if (ba >= nB) ba -= nB;
     for (int it = 0; it < my_vts; ++it) {
       const int vt = int(blockIdx.x) + it * int(gridDim.x);
       const int64_t v = int64_t(vt) * C::kVox + row;
@@ -1292,8 +1316,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       // split mode: fp32 running max / threshold (thresholds rounded down)
       float runmax_f = active ? init_tc[v] : -INFINITY;
       float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
-      const uint32_t kend = uint32_t(it + 1) * uint32_t(nB);
+      const uint32_t kbeg = uint32_t(it) * uint32_t(T), kend = kbeg + uint32_t(T);
       for (; kk < kend; kk += kParts) {
+        const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
+        int ba = rot + qt;                       // atom tile (rot + qt) % nB
+        if (ba >= nB) ba -= nB;
         if (q == 0 && lane == 0) CBB_STAMP(5, kk);
         mbar_wait(t_full + tb, ph);
         tc_fence_after();
@@ -1317,8 +1344,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
               __syncwarp();
               if (lane == 0) mbar_arrive(b_full + rel);
             }
-            screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win, runmax_f,
-                                        thr_f, active, cl);
+            if (qt >= 0)
+              screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win,
+                                          runmax_f, thr_f, active, cl);
+            else if (active)
+              runmax_f = fmaxf(runmax_f, tile_max_f32<kRegChunks>(r));
           }
         } else {
 #pragma unroll
@@ -1334,7 +1364,14 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(b_full + rel);
-          screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
+          if (qt >= 0)
+            screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
+          else if (active)
+            runmax = __hmax(runmax, tile_max_f16<C::kChunks>(r));
+        }
+        if (qt < 0 && active) {  // warm-start tile: raise the threshold, record nothing
+          thr_f = __fsub_rd(runmax_f, win);
+          thr = __float2half_rd(__half2float(runmax) - win);
         }
         if (q == 0 && lane == 0) CBB_STAMP(6, kk);
         sacc += kParts;
@@ -1346,8 +1383,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         }
         rel += kParts;
         if (rel >= C::kStages) rel -= C::kStages;
-        ba += kParts;
-        if (ba >= nB) ba -= nB;
       }
       // ---- hand-off (no inter-part barrier): this part's surviving chunk entries are appended
       // to its global list (after any spills); count and running max go to meta.
@@ -1867,6 +1902,7 @@ struct ProjWs {
   int* heavy_count;     // voxels with many tcgen05 chunk entries (warp rescoring)
   int64_t* heavy_list;
   double2* exh_partial; // [n][kExhSplits] (score, index) of the split exhaustive scan
+  uint8_t* hint_tiles;  // [voxel tile][hint tile] warm-start tiles (IPG)
   double* nd_v;
   double* partial;
 };
@@ -1896,6 +1932,15 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   w.heavy_count = reinterpret_cast<int*>(take(16));
   w.heavy_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   w.exh_partial = reinterpret_cast<double2*>(take(size_t(n) * kExhSplits * sizeof(double2)));
+  {  // hint tiles: the largest per-voxel-tile block of the screens this s can use
+    size_t per_vt = kpad_for(s) == 32 ? 160 * 32 * 2 : 128 * 64 * 2;
+    if (s <= kSplitMaxS) {
+      const int k2 = split_kp(s), rows = split_rows(k2);
+      const size_t sb = size_t((kTileRows + rows - 1) / rows) * rows * k2 * 2;
+      if (sb > per_vt) per_vt = sb;
+    }
+    w.hint_tiles = take(size_t(n_vt) * (kVoxPad / kTileRows) * per_vt);
+  }
   w.nd_v = reinterpret_cast<double*>(take(size_t(n) * 8));
   w.partial = reinterpret_cast<double*>(take(kReduceBlocks * 8));
   if (ws) *ws = w;
@@ -1913,6 +1958,44 @@ static int num_sms() {
   return g_num_sms;
 }
 
+// Warm-start hint tiles: row r of voxel tile vt's hint block = a copy of the storage row of
+// atom hint[vt*128 + r] (the previous IPG winner of that voxel), in the screen's own tile
+// layout; rows without a valid hint (and rows >= 128 of a 160-row tile) copy the first padded
+// row (score -65504 for every voxel).  One thread per 16-byte chunk.
+__global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restrict__ hint,
+                                                         int64_t n, int64_t d, int n_vt,
+                                                         const uint8_t* __restrict__ atiles,
+                                                         int kp, int split, int bn, int nh,
+                                                         uint8_t* __restrict__ out) {
+  const int cpr = kp / 8;  // 16-byte chunks per row
+  const int64_t per_vt = int64_t(nh) * bn * cpr;
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= per_vt * n_vt) return;
+  const int vt = int(g / per_vt);
+  const int rem = int(g - int64_t(vt) * per_vt);
+  const int r = rem / cpr, c = rem - r * cpr;
+  const int64_t v = int64_t(vt) * 128 + r;
+  int64_t j = d;
+  if (r < 128 && v < n) {
+    const int64_t h = hint[v];
+    if (h >= 0 && h < d) j = h;
+  }
+  size_t src, dst;
+  const int hb = r / bn, rr = r - hb * bn;
+  if (split) {
+    const int rows = split_rows(kp);
+    src = size_t(j / rows) * rows * kp * 2 + split_elem_offset(int(j % rows), 8 * c, rows);
+    dst = (size_t(vt) * nh + hb) * bn * kp * 2 + split_elem_offset(rr, 8 * c, bn);
+  } else {
+    src = size_t(j / kTileRows) * kTileRows * kp * 2 + tile_chunk_offset(int(j % kTileRows), c, kp);
+    dst = (size_t(vt) * nh + hb) * bn * kp * 2 + tile_chunk_offset(rr, c, kp);
+  }
+  *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(atiles + src);
+}
+
+template <class C>
+constexpr int BN_of() { return C::BN; }
+
 template <int KP, bool SPLIT = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
@@ -1927,9 +2010,20 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (grid > n_vt) grid = n_vt;
+  int n_hint = 0;
+  if (zs.hint) {  // IPG warm start: the voxel tiles' own hint atoms screened first
+    const int nh = (kTileRows + BN_of<C>() - 1) / BN_of<C>();
+    const int64_t chunks = int64_t(n_vt) * nh * C::BN * (KP / 8);
+    hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
+        zs.hint, n, dv.d, n_vt, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, KP, SPLIT ? 1 : 0, C::BN, nh,
+        w.hint_tiles);
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    n_hint = kParts * nh;
+  }
   mf_tc_kernel<KP, SPLIT><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc,
                                                                w.init_tc, dv, w.n_pad, w.cand,
-                                                               w.meta);
+                                                               w.meta, w.hint_tiles, n_hint);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
