@@ -917,7 +917,10 @@ constexpr int kParts = 3;
 // SPLIT: hi/lo fp16 operands with fp32 accumulators: KP = 64 -> 128-atom tiles (N = 128 MMAs;
 // measured faster than 64-atom tiles with six stages), screened in two 64-register halves;
 // KP = 128 -> 64-atom tiles (the 16 KB stages keep a 9-deep ring).
-template <int KP, bool SPLIT = false>
+// PAIR: the CTAs of a cluster pair run cta_group::2 MMAs (M = 256: each CTA's 128 voxels); every
+// CTA bulk-copies only its half of each atom tile (kBNloc rows), which halves the L2 -> SMEM
+// atom stream that bounds the single-CTA kernel.
+template <int KP, bool SPLIT = false, bool PAIR = false>
 struct TcCfg {
   static_assert(!SPLIT || KP == 64 || KP == 128, "split tiles are 64 or 128 wide");
   // 32-atom chunks per tile (split: the tile is one split_rows(KP)-row storage tile)
@@ -928,7 +931,12 @@ struct TcCfg {
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
-  static constexpr int kBBytes = BN * KP * 2;
+  static constexpr int kBNloc = PAIR ? BN / 2 : BN;          // atom rows in this CTA's SMEM
+  static constexpr int kRowBytes = (KP < 64 ? KP : 64) * 2;   // bytes per row of a K block
+  static constexpr int kBlk = KP <= 64 ? 1 : KP / 64;         // K blocks per tile
+  static constexpr int kBTileBytes = BN * KP * 2;             // one atom tile in global memory
+  static constexpr int kBBytes = kBNloc * KP * 2;             // its part in this CTA
+  static_assert(kBNloc % 8 == 0, "8-row swizzle groups");
   static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
   static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
   static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
@@ -942,7 +950,8 @@ struct TcCfg {
   static constexpr int kOffB = 0;
   static constexpr int kOffCj = kOffB + kStages * kBBytes;
   static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
-  static constexpr int kOffBar = kOffCs + kCandCap * kSlots * 4;
+  static constexpr int kOffPthr = kOffCs + kCandCap * kSlots * 4;  // [kVox][4] u32 thresholds
+  static constexpr int kOffBar = kOffPthr + kVox * 16;
   // completion barriers per tile slot k % kTBars (lcm(kAcc, kParts)): every barrier belongs to
   // one stage AND one part, whose waits consume its phases in order (no parity aliasing)
   static constexpr int kTBars = (kAcc % kParts == 0) ? kAcc : kAcc * kParts;
@@ -951,7 +960,8 @@ struct TcCfg {
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr uint32_t kIdesc = SPLIT ? idesc_f16_f32(128, BN) : idesc_f16_f16(128, BN);
+  static constexpr int kM = PAIR ? 256 : 128;
+  static constexpr uint32_t kIdesc = SPLIT ? idesc_f16_f32(kM, BN) : idesc_f16_f16(kM, BN);
   static constexpr int kMinTiles = kParts;  // every part owns >= 1 tile per voxel tile
 };
 
@@ -1008,7 +1018,7 @@ __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64
 template <int NC>
 __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_t jb, float win,
                                             __half& runmax, __half& thr, bool& active,
-                                            HCandList& cl) {
+                                            HCandList& cl, uint32_t* pub, uint32_t tag) {
   // NC independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
   __half2 c[NC];
 #pragma unroll
@@ -1029,6 +1039,7 @@ __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_
       runmax = __hmax(runmax, cm);
       if (active) {
         thr = __float2half_rd(__half2float(runmax) - win);
+        *pub = tag | __half_as_ushort(thr);  // the other parts screen against it too
         const float thr_f = __half2float(thr);
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
@@ -1116,6 +1127,22 @@ __device__ __forceinline__ __half tile_max_f16(const uint32_t (&r)[16 * NC]) {
   return hmax_halves(__hmax2(a, as_h2(r[16 * NC - 1])));
 }
 
+// Highest of the parts' published thresholds (shared words tag | fp16 bits) whose tag is this
+// voxel tile's; -inf if none.  Words of an older voxel tile (or the -inf init) are ignored.
+__device__ __forceinline__ __half pub_thr(uint32_t w, uint32_t tag) {
+  return __ushort_as_half((w & 0xffff0000u) == tag ? uint16_t(w) : uint16_t(0xFC00));
+}
+__device__ __forceinline__ uint4 lds_v4_volatile(const uint32_t* p) {
+  uint4 w;
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "r"(smem_u32(p)));
+  return w;
+}
+__device__ __forceinline__ __half shared_thr(uint4 w, uint32_t tag) {
+  return __hmax(__hmax(pub_thr(w.x, tag), pub_thr(w.y, tag)), pub_thr(w.z, tag));
+}
+
 template <int KP>
 __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrows, int64_t v,
                                                 bool live, uint32_t taddr) {
@@ -1137,13 +1164,13 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
   tc_wait_st();
 }
 
-template <int KP, bool SPLIT>
-__global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
+template <int KP, bool SPLIT, bool PAIR>
+__global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
                  DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta,
                  const uint8_t* __restrict__ hint_tiles, int n_hint) {
-  using C = TcCfg<KP, SPLIT>;
+  using C = TcCfg<KP, SPLIT, PAIR>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
@@ -1158,8 +1185,16 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t d = dv.d;
   const int nB = int((d + BN - 1) / BN);
-  const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
-  const int my_vts = (n_vt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  // PAIR: the two CTAs (ranks 0 = leader, 1) of a cluster stream the same atom tiles in lockstep
+  // (same rotation, same number of voxel tiles: the surplus ones are dead, every row v >= n).
+  // The leader's issuers run the pair's MMAs; the odd CTA's epilogue and producer signal the
+  // leader's barriers remotely, its issuer warps relay "my half of tile k landed".
+  const int crank = PAIR ? int(cluster_ctarank()) : 0;
+  const bool leader = crank == 0;
+  const int csz = PAIR ? 2 : 1;
+  const int rot = int((int64_t(blockIdx.x / csz) * nB) / (gridDim.x / csz));
+  const int my_vts = PAIR ? (n_vt + int(gridDim.x) - 1) / int(gridDim.x)
+                          : (n_vt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
   // per voxel tile: n_hint warm-start tiles (the voxel tile's own hint atoms, each hint tile
   // repeated for the kParts parts: tile qt -> hint tile qt / kParts), then the nB atom tiles
   const int T = nB + n_hint;
@@ -1167,22 +1202,36 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(a_full + i, 4);         // the 4 part-0 warps stage A
+      mbar_init(a_full + i, 4 * csz);   // the 4 part-0 warps (of both CTAs) stage A
       mbar_init(a_empty + i, kParts);   // each issuer commits after its last tile of a voxel tile
     }
     for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full + i, 1);
+    // b_full: producer (with tx) + the 4 warps releasing the accumulator stage; PAIR leader:
+    // + the odd CTA's 4 releasing warps + its relayed "half landed"; PAIR odd CTA: data only
+    const uint32_t bf_count = PAIR ? (leader ? 1 + 4 + 4 + 1 : 1) : 1 + 4;
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(b_full + i, 1 + 4);     // producer (with tx) + the 4 warps releasing the stage
-      mbar_init(b_empty + i, 1);
+      mbar_init(b_full + i, bf_count);
+      mbar_init(b_empty + i, 1);        // the MMAs reading the stage retired
     }
     // tiles 0 .. kAcc-1 find their accumulator stage free: pre-release their first phase
-    for (int i = 0; i < C::kAcc; ++i)
-      for (int w = 0; w < 4; ++w) mbar_arrive(b_full + i);
+    if (leader)
+      for (int i = 0; i < C::kAcc; ++i)
+        for (int w = 0; w < 4 * csz; ++w) mbar_arrive(b_full + i);
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc2(tmem_holder, 512);
+    else
+      tmem_alloc(tmem_holder, 512);
+  }
+  // published thresholds: tag 0xffff, -inf (matches no voxel tile a CTA reaches in practice,
+  // and would only contribute -inf)
+  for (int i = threadIdx.x; i < 4 * C::kVox; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem + C::kOffPthr)[i] = 0xFFFFFC00u;
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
@@ -1198,11 +1247,26 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       for (int b = 0; b < T; ++b) {
         mbar_wait(b_empty + st, ph ^ 1u);
         if (elect_one()) {
+          // hint tiles belong to the voxel tile (PAIR: to the pair's 256-voxel group)
+          const int hg = PAIR ? vt / 2 : vt, n_hg = PAIR ? (n_vt + 1) / 2 : n_vt;
+          const int hvt = hg < n_hg ? hg : n_hg - 1;  // dead voxel tiles reuse a valid hint
           const uint8_t* src =
-              b < n_hint ? hint_tiles + (size_t(vt) * (n_hint / kParts) + b / kParts) * C::kBBytes
-                         : atiles + size_t(ba) * C::kBBytes;
+              b < n_hint
+                  ? hint_tiles + (size_t(hvt) * (n_hint / kParts) + b / kParts) * C::kBTileBytes
+                  : atiles + size_t(ba) * C::kBTileBytes;
+          uint8_t* dst = smem + C::kOffB + st * C::kBBytes;
+#ifdef CBB_NOCOPY  // development timing variant: no atom stream (wrong results)
+          mbar_arrive(b_full + st);
+#else
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
-          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, C::kBBytes, b_full + st, pol_b);
+          // this CTA's rows [crank * kBNloc, +kBNloc) of every K block
+#pragma unroll
+          for (int kb = 0; kb < C::kBlk; ++kb)
+            bulk_g2s(dst + kb * C::kBNloc * C::kRowBytes,
+                     src + (kb * BN + crank * C::kBNloc) * C::kRowBytes,
+                     uint32_t(C::kBNloc * C::kRowBytes), b_full + st, pol_b);
+#endif
+          CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
         }
         __syncwarp();
         if (b >= n_hint && ++ba == nB) ba = 0;
@@ -1210,6 +1274,22 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
           st = 0;
           ph ^= 1u;
         }
+      }
+    }
+  } else if (PAIR && !leader && warp >= 1 && warp <= kParts) {
+    // ------------------------------------------------ PAIR odd CTA: relay "my half landed"
+    const int me = warp - 1;
+    const uint32_t bf_leader = mapa_shared(smem_u32(b_full), 0);
+    int st = me;
+    uint32_t ph = 0;
+    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
+      mbar_wait(b_full + st, ph);
+      if (lane == 0) mbar_arrive_remote(bf_leader + uint32_t(st * 8));
+      __syncwarp();
+      st += kParts;
+      if (st >= C::kStages) {
+        st -= C::kStages;
+        ph ^= 1u;
       }
     }
   } else if (warp >= 1 && warp <= kParts) {
@@ -1227,10 +1307,16 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       if (kk >= vt_end) {  // first tile of this issuer in a new voxel tile: wait for its A
         ++itk;
         vt_end += uint32_t(T);
-        mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
+        if constexpr (PAIR)
+          mbar_wait_cluster(a_full + (itk & 1), (itk >> 1) & 1);
+        else
+          mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
       if (lane == 0) CBB_STAMP(4, kk);
-      mbar_wait(b_full + st, ph);
+      if constexpr (PAIR)
+        mbar_wait_cluster(b_full + st, ph);
+      else
+        mbar_wait(b_full + st, ph);
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
@@ -1238,17 +1324,29 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq) {
-          // K-major operand: K blocks of 64 elements (128 B rows) follow each other, BN rows each
-          const uint64_t bdesc =
-              umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * BN * 128, KP < 64 ? KP : 64);
-          if (kq < nks)
-            tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)), C::kIdesc,
-                          kq > 0 ? 1u : 0u);
+          // K-major operand: K blocks of 64 elements (128 B rows) follow each other, kBNloc
+          // rows each
+          const uint64_t bdesc = umma_desc_kmajor(
+              b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128, KP < 64 ? KP : 64);
+          if (kq < nks) {
+            if constexpr (PAIR)
+              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)),
+                             C::kIdesc, kq > 0 ? 1u : 0u);
+            else
+              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)),
+                            C::kIdesc, kq > 0 ? 1u : 0u);
+          }
         }
-        tc_commit(b_empty + st);
-        tc_commit(t_full + tb);
-        // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
-        if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
+        if constexpr (PAIR) {  // both CTAs' barriers
+          tc_commit2_mc(b_empty + st, 3);
+          tc_commit2_mc(t_full + tb, 3);
+          if (kk + kParts >= vt_end) tc_commit2_mc(a_empty + (itk & 1), 3);
+        } else {
+          tc_commit(b_empty + st);
+          tc_commit(t_full + tb);
+          // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
+          if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
+        }
         CBB_STAMP(1, kk);
       }
       __syncwarp();
@@ -1273,6 +1371,17 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     const uint32_t lane_off = uint32_t(q * 32) << 16;
     const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
     const uint32_t t_lane = tbase + lane_off;
+    const uint32_t t_stage = t_lane + uint32_t(part * C::kAccCols);  // fp16: stage == part
+    uint32_t* pthr_row = reinterpret_cast<uint32_t*>(smem + C::kOffPthr) + row * 4;
+    // A-staged / stage-released signals go to the leader's barriers (PAIR odd CTA: remotely)
+    const uint32_t lead_delta =
+        (PAIR && !leader) ? mapa_shared(smem_u32(bars), 0) - smem_u32(bars) : 0u;
+    auto arrive_lead = [&](uint64_t* bar) {
+      if (PAIR && !leader)
+        mbar_arrive_remote(smem_u32(bar) + lead_delta);
+      else
+        mbar_arrive(bar);
+    };
 
     // ---- A for the first voxel tile
     if (part == 0 && my_vts > 0) {
@@ -1280,7 +1389,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + 0);
+      if (lane == 0) arrive_lead(a_full + 0);
     }
 
     uint32_t kk = uint32_t(part);  // this part's next tile
@@ -1301,7 +1410,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         stage_voxel_row<KP>(zrows, vn, vn < n, a_lane + uint32_t(nbuf * C::kACols));
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(a_full + nbuf);
+        if (lane == 0) arrive_lead(a_full + nbuf);
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(0, it);
       const float win = live ? win_tc[v] : -1.f;
@@ -1317,21 +1426,79 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       float runmax_f = active ? init_tc[v] : -INFINITY;
       float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
       const uint32_t kbeg = uint32_t(it) * uint32_t(T), kend = kbeg + uint32_t(T);
-      for (; kk < kend; kk += kParts) {
-        const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
-        int ba = rot + qt;                       // atom tile (rot + qt) % nB
+      if constexpr (!SPLIT) {
+        // fp16 screen: the part owns accumulator stage `part` and completion barrier `part`
+        // (kAcc == kTBars == kParts), whose phase flips every tile.  The three parts publish
+        // their thresholds per voxel in shared memory, tagged with the voxel-tile iteration:
+        // any part's rd(runmax - win) is a lower bound on the window edge of the voxel, so each
+        // part screens against the highest one it sees (the slow path runs about half as often).
+        static_assert(C::kAcc == kParts && C::kTBars == kParts, "stage = part");
+        const uint32_t tag = (uint32_t(it) & 0xffffu) << 16;
+        uint32_t* my_pub = pthr_row + part;
+        const uint32_t khint = kbeg + uint32_t(n_hint);
+        uint32_t r[16 * C::kChunks];
+        auto consume = [&]() {
+          if (q == 0 && lane == 0) CBB_STAMP(5, kk);
+          mbar_wait(t_full + part, ph);
+          tc_fence_after();
+          if (q == 0 && lane == 0) CBB_STAMP(2, kk);
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c + 2 <= C::kChunks; c += 2)
+            tmem_ld32_pack16(t_stage + uint32_t(32 * c),
+                             *reinterpret_cast<uint32_t(*)[32]>(r + 16 * c));
+          if (C::kChunks & 1)
+            tmem_ld16_pack16(t_stage + uint32_t(32 * (C::kChunks - 1)),
+                             *reinterpret_cast<uint32_t(*)[16]>(r + 16 * (C::kChunks - 1)));
+          tc_wait_ld();
+          // early release: the stage may be overwritten by tile kk + kAcc while we screen
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_lead(b_full + rel);
+          if (q == 0 && lane == 0) CBB_STAMP(3, kk);
+          ph ^= 1u;
+          rel += kParts;
+          if (rel >= C::kStages) rel -= C::kStages;
+        };
+        // warm-start hint tiles: raise the running max, record nothing
+        for (; kk < khint; kk += kParts) {
+          consume();
+          if (active) runmax = __hmax(runmax, tile_max_f16<C::kChunks>(r));
+        }
+        if (active) {
+          thr = __float2half_rd(__half2float(runmax) - win);
+          *my_pub = tag | __half_as_ushort(thr);
+        }
+        int ba = rot + int(kk - khint);  // atom tile (rot + qt) % nB, qt = kk - khint
         if (ba >= nB) ba -= nB;
-        if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-        mbar_wait(t_full + tb, ph);
-        tc_fence_after();
-        if (q == 0 && lane == 0) CBB_STAMP(2, kk);
-        // split mode: at most two fp32 chunks (64 registers) in flight; wider tiles are
-        // screened in halves and released after the last half is loaded
-        constexpr int kRegChunks = SPLIT ? (C::kChunks < 2 ? C::kChunks : 2) : C::kChunks;
-        uint32_t r[(SPLIT ? 32 : 16) * kRegChunks];
-        __syncwarp();
-        const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
-        if constexpr (SPLIT) {
+        for (; kk < kend; kk += kParts) {
+          const uint4 w = lds_v4_volatile(pthr_row);
+          consume();
+          thr = __hmax(thr, shared_thr(w, tag));
+#if defined(CBB_EPI_EMPTY)  // development timing variants (wrong results)
+          if (r[0] == 0x7fff7fffu) runmax = __hmax(runmax, as_h2(r[1]).x);
+#elif defined(CBB_EPI_NOSLOW)
+          if (__hge(tile_max_f16<C::kChunks>(r), __ushort_as_half(0x7C00))) runmax = thr;
+#else
+          screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl, my_pub, tag);
+#endif
+          if (q == 0 && lane == 0) CBB_STAMP(6, kk);
+          ba += kParts;
+          if (ba >= nB) ba -= nB;
+        }
+      } else {
+        // split screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles
+        // are screened in halves and released after the last half is loaded
+        for (; kk < kend; kk += kParts) {
+          const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
+          int ba = rot + qt;                       // atom tile (rot + qt) % nB
+          if (ba >= nB) ba -= nB;
+          mbar_wait(t_full + tb, ph);
+          tc_fence_after();
+          constexpr int kRegChunks = C::kChunks < 2 ? C::kChunks : 2;
+          uint32_t r[32 * kRegChunks];
+          __syncwarp();
+          const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
 #pragma unroll
           for (int h = 0; h < C::kChunks / kRegChunks; ++h) {
 #pragma unroll
@@ -1342,7 +1509,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
             if (h + 1 == C::kChunks / kRegChunks) {
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(b_full + rel);
+              if (lane == 0) arrive_lead(b_full + rel);
             }
             if (qt >= 0)
               screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win,
@@ -1350,39 +1517,17 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
             else if (active)
               runmax_f = fmaxf(runmax_f, tile_max_f32<kRegChunks>(r));
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c + 2 <= C::kChunks; c += 2)
-            tmem_ld32_pack16(ta + uint32_t(32 * c),
-                             *reinterpret_cast<uint32_t(*)[32]>(r + 16 * c));
-          if (C::kChunks & 1)
-            tmem_ld16_pack16(ta + uint32_t(32 * (C::kChunks - 1)),
-                             *reinterpret_cast<uint32_t(*)[16]>(r + 16 * (C::kChunks - 1)));
-          tc_wait_ld();
-          if (q == 0 && lane == 0) CBB_STAMP(3, kk);
-          // early release: the stage may be overwritten by tile kk + kAcc while we screen
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(b_full + rel);
-          if (qt >= 0)
-            screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl);
-          else if (active)
-            runmax = __hmax(runmax, tile_max_f16<C::kChunks>(r));
+          if (qt < 0 && active) thr_f = __fsub_rd(runmax_f, win);  // warm-start tile
+          sacc += kParts;
+          if (sacc >= C::kAcc) sacc -= C::kAcc;
+          tb += kParts;
+          if (tb >= C::kTBars) {
+            tb -= C::kTBars;
+            ph ^= 1u;
+          }
+          rel += kParts;
+          if (rel >= C::kStages) rel -= C::kStages;
         }
-        if (qt < 0 && active) {  // warm-start tile: raise the threshold, record nothing
-          thr_f = __fsub_rd(runmax_f, win);
-          thr = __float2half_rd(__half2float(runmax) - win);
-        }
-        if (q == 0 && lane == 0) CBB_STAMP(6, kk);
-        sacc += kParts;
-        if (sacc >= C::kAcc) sacc -= C::kAcc;
-        tb += kParts;
-        if (tb >= C::kTBars) {
-          tb -= C::kTBars;
-          ph ^= 1u;
-        }
-        rel += kParts;
-        if (rel >= C::kStages) rel -= C::kStages;
       }
       // ---- hand-off (no inter-part barrier): this part's surviving chunk entries are appended
       // to its global list (after any spills); count and running max go to meta.
@@ -1397,9 +1542,13 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     }
   }
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no peer arrives on this CTA's barriers any more
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    if constexpr (PAIR)
+      tmem_dealloc2(tbase, 512);
+    else
+      tmem_dealloc(tbase, 512);
   }
 }
 
@@ -1960,10 +2109,11 @@ static int num_sms() {
 
 // Warm-start hint tiles: row r of voxel tile vt's hint block = a copy of the storage row of
 // atom hint[vt*128 + r] (the previous IPG winner of that voxel), in the screen's own tile
-// layout; rows without a valid hint (and rows >= 128 of a 160-row tile) copy the first padded
+// layout (vox voxels per tile group: 128, or 256 for a CTA pair); rows without a valid hint
+// (and rows >= vox of the last tile) copy the first padded
 // row (score -65504 for every voxel).  One thread per 16-byte chunk.
 __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restrict__ hint,
-                                                         int64_t n, int64_t d, int n_vt,
+                                                         int64_t n, int64_t d, int n_vt, int vox,
                                                          const uint8_t* __restrict__ atiles,
                                                          int kp, int split, int bn, int nh,
                                                          uint8_t* __restrict__ out) {
@@ -1974,9 +2124,9 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
   const int vt = int(g / per_vt);
   const int rem = int(g - int64_t(vt) * per_vt);
   const int r = rem / cpr, c = rem - r * cpr;
-  const int64_t v = int64_t(vt) * 128 + r;
+  const int64_t v = int64_t(vt) * vox + r;
   int64_t j = d;
-  if (r < 128 && v < n) {
+  if (r < vox && v < n) {
     const int64_t h = hint[v];
     if (h >= 0 && h < d) j = h;
   }
@@ -1996,36 +2146,96 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
 template <class C>
 constexpr int BN_of() { return C::BN; }
 
-template <int KP, bool SPLIT = false>
-static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                     const ProjOut& out, int max_ctas, cudaStream_t st) {
-  using C = TcCfg<KP, SPLIT>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set = true;
+// CTA pairs for the matched-filter screen (cta_group::2, see TcCfg): CBB_TC_PAIR=0 disables.
+static bool tc_pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CBB_TC_PAIR");
+    v = (e && atoi(e) == 0) ? 0 : 1;
   }
-  const int n_vt = int((n + C::kVox - 1) / C::kVox);
-  int grid = num_sms();
-  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (grid > n_vt) grid = n_vt;
+  return v != 0;
+}
+template <class K>
+static int max_coresident_pairs(K kernel, int threads, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(256u);
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
+}
+
+template <int KP, bool SPLIT, bool PAIR>
+static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                        int grid, int n_vt, cudaStream_t st) {
+  using C = TcCfg<KP, SPLIT, PAIR>;
   int n_hint = 0;
-  if (zs.hint) {  // IPG warm start: the voxel tiles' own hint atoms screened first
-    const int nh = (kTileRows + BN_of<C>() - 1) / BN_of<C>();
-    const int64_t chunks = int64_t(n_vt) * nh * C::BN * (KP / 8);
+  if (zs.hint) {  // IPG warm start: the voxel tiles' (pairs') own hint atoms screened first
+    const int vox = PAIR ? 2 * C::kVox : C::kVox;
+    const int n_g = int((n + vox - 1) / vox);
+    const int nh = (vox + C::BN - 1) / C::BN;
+    const int64_t chunks = int64_t(n_g) * nh * C::BN * (KP / 8);
     hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_vt, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, KP, SPLIT ? 1 : 0, C::BN, nh,
-        w.hint_tiles);
+        zs.hint, n, dv.d, n_g, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, KP, SPLIT ? 1 : 0, C::BN,
+        nh, w.hint_tiles);
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     n_hint = kParts * nh;
   }
-  mf_tc_kernel<KP, SPLIT><<<grid, C::kThreads, C::kSmem, st>>>(w.ztiles, n, n_vt, w.win_tc,
-                                                               w.init_tc, dv, w.n_pad, w.cand,
-                                                               w.meta, w.hint_tiles, n_hint);
-  CBB_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(C::kThreads));
+  cfg.dynamicSmemBytes = size_t(C::kSmem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = PAIR ? 1 : 0;
+  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR>, w.ztiles, n, n_vt,
+                                  (const float*)w.win_tc, (const float*)w.init_tc, dv, w.n_pad,
+                                  w.cand, w.meta, (const uint8_t*)w.hint_tiles, n_hint));
   return kOk;
+}
+
+template <int KP, bool SPLIT = false>
+static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                     const ProjOut& out, int max_ctas, cudaStream_t st) {
+  using C1 = TcCfg<KP, SPLIT, false>;
+  using C2 = TcCfg<KP, SPLIT, true>;
+  static bool attr_set = false;
+  static int pairs = 0;
+  if (!attr_set) {
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmem));
+    pairs = max_coresident_pairs(mf_tc_kernel<KP, SPLIT, true>, C2::kThreads, C2::kSmem);
+    attr_set = true;
+  }
+  const int n_vt = int((n + C1::kVox - 1) / C1::kVox);
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (grid > n_vt) grid = n_vt;
+  // CTA pairs halve the atom stream; used when every pair is co-resident (persistent kernel),
+  // at most 5% of the SMs idle, and every CTA gets at least two voxel tiles
+  int grid2 = 2 * pairs < grid ? 2 * pairs : grid - grid % 2;
+  if (tc_pair_enabled() && grid2 >= 8 && grid2 * 20 >= grid * 19 && n_vt >= 2 * grid2)
+    return launch_tc_as<KP, SPLIT, true>(w, n, zs, dv, grid2, n_vt, st);
+  return launch_tc_as<KP, SPLIT, false>(w, n, zs, dv, grid, n_vt, st);
 }
 
 template <int S>

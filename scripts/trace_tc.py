@@ -31,7 +31,9 @@ print("epi: screen (3->6)                  ", med(t[ks, 6] - t[ks, 3]))
 print("epi: loop overhead (6 -> next 5)    ", med(t[ks + 3, 5] - t[ks, 6]))
 print("epi: part period (2 -> next 2)      ", med(t[ks + 3, 2] - t[ks, 2]))
 print("commit -> t_full ready (1->2)       ", med(t[ks, 2] - t[ks, 1]))
-print("release(k-5) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 5, 3]))
+print("release(k-3) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 3, 3]))
+print("producer issue(k) -> issuer ready   ", med(t[ks, 0] - t[ks, 7]))
+print("tile period (issuer ready k -> k+1) ", med(t[ks + 1, 0] - t[ks, 0]))
 print("frac of part time waiting           ", med((t[ks, 2] - t[ks, 5]) / (t[ks + 3, 2] - t[ks, 2])))
 vt = np.zeros(256 * 4, dtype=np.int64)
 assert fn(vt.ctypes.data, -1) == 0
