@@ -2146,12 +2146,15 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
 template <class C>
 constexpr int BN_of() { return C::BN; }
 
-// CTA pairs for the matched-filter screen (cta_group::2, see TcCfg): CBB_TC_PAIR=0 disables.
+// CTA pairs for the matched-filter screen (cta_group::2, see TcCfg): opt-in with CBB_TC_PAIR=1.
+// Measured on cfg1 (1x B200): 19.1 ms vs 8.4 ms for single CTAs -- the odd CTA's remote stage
+// releases lengthen the refill chain of every accumulator stage (release -> issuer 445 -> 1255
+// clk) by more than the halved atom stream saves.
 static bool tc_pair_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CBB_TC_PAIR");
-    v = (e && atoi(e) == 0) ? 0 : 1;
+    v = (e && atoi(e) == 1) ? 1 : 0;
   }
   return v != 0;
 }
