@@ -937,7 +937,11 @@ struct TcCfg {
   static constexpr int kBTileBytes = BN * KP * 2;             // one atom tile in global memory
   static constexpr int kBBytes = kBNloc * KP * 2;             // its part in this CTA
   static_assert(kBNloc % 8 == 0, "8-row swizzle groups");
+#ifdef CBB_RING_KB
+  static constexpr int kRing = CBB_RING_KB * 1024;
+#else
   static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
+#endif
   static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
   static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
   static constexpr int kStages = (kStagesRaw / kParts) * kParts;
@@ -955,7 +959,7 @@ struct TcCfg {
   // completion barriers per tile slot k % kTBars (lcm(kAcc, kParts)): every barrier belongs to
   // one stage AND one part, whose waits consume its phases in order (no parity aliasing)
   static constexpr int kTBars = (kAcc % kParts == 0) ? kAcc : kAcc * kParts;
-  static constexpr int kNumBars = 4 + 2 * kStages + kTBars;
+  static constexpr int kNumBars = 4 + 2 * kStages + kTBars + kAcc;
   static_assert(kStages % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
@@ -1180,6 +1184,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
   uint64_t* b_full = bars + 4;
   uint64_t* b_empty = b_full + C::kStages;
   uint64_t* t_full = b_empty + C::kStages;
+  uint64_t* acc_free = t_full + C::kTBars;  // accumulator stage released by its epilogue part
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1206,17 +1211,15 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
       mbar_init(a_empty + i, kParts);   // each issuer commits after its last tile of a voxel tile
     }
     for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full + i, 1);
-    // b_full: producer (with tx) + the 4 warps releasing the accumulator stage; PAIR leader:
-    // + the odd CTA's 4 releasing warps + its relayed "half landed"; PAIR odd CTA: data only
-    const uint32_t bf_count = PAIR ? (leader ? 1 + 4 + 4 + 1 : 1) : 1 + 4;
+    // b_full: the atom tile landed (producer with tx; PAIR leader: + the odd CTA's relayed "my
+    // half landed").  acc_free: the 4 warps (PAIR: of both CTAs) of the part that read the
+    // accumulator stage released it.  Separate barriers: with one barrier counting both, the
+    // issuer woke ~520 clk after the last release (measured), ~2x the separate waits.
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(b_full + i, bf_count);
+      mbar_init(b_full + i, (PAIR && leader) ? 2 : 1);
       mbar_init(b_empty + i, 1);        // the MMAs reading the stage retired
     }
-    // tiles 0 .. kAcc-1 find their accumulator stage free: pre-release their first phase
-    if (leader)
-      for (int i = 0; i < C::kAcc; ++i)
-        for (int w = 0; w < 4 * csz; ++w) mbar_arrive(b_full + i);
+    for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free + i, 4 * csz);
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -1235,8 +1238,8 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 0) {
-    // ------------------------------------------------ producer (bulk copies of atom tiles)
+  if (warp == 0 && PAIR) {
+    // ------------------------------------------------ PAIR producer (bulk copies of atom tiles)
     const uint64_t pol_b = policy_evict_last();
     const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
     int st = 0;
@@ -1255,9 +1258,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
                   ? hint_tiles + (size_t(hvt) * (n_hint / kParts) + b / kParts) * C::kBTileBytes
                   : atiles + size_t(ba) * C::kBTileBytes;
           uint8_t* dst = smem + C::kOffB + st * C::kBBytes;
-#ifdef CBB_NOCOPY  // development timing variant: no atom stream (wrong results)
-          mbar_arrive(b_full + st);
-#else
           mbar_arrive_expect_tx(b_full + st, C::kBBytes);
           // this CTA's rows [crank * kBNloc, +kBNloc) of every K block
 #pragma unroll
@@ -1265,7 +1265,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
             bulk_g2s(dst + kb * C::kBNloc * C::kRowBytes,
                      src + (kb * BN + crank * C::kBNloc) * C::kRowBytes,
                      uint32_t(C::kBNloc * C::kRowBytes), b_full + st, pol_b);
-#endif
           CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
         }
         __syncwarp();
@@ -1297,7 +1296,46 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
     const int me = warp - 1;
     const int nks = SPLIT ? split_ksteps(dv.s) : mma_ksteps(dv.s);
     const uint32_t b_base = smem_u32(smem + C::kOffB);
+    static_assert(C::kAcc == kParts, "issuer i always fills accumulator stage i");
     int sacc = me;  // accumulator stage kk % kAcc
+    uint32_t aph = 1;  // acc_free parity: the first use of each stage passes at once
+    // The issuers also load the atom tiles (single CTA): issuer i fills the ring stages of its
+    // own tiles, refilling the stage of its previous tile kk - 3 with tile kk - 3 + kStages
+    // (that MMA retired while this issuer waited for its next stage).  A dedicated producer
+    // warp was the measured limiter: ~50 dependent instructions per tile on one warp took
+    // ~300 clk, so it ran barely one tile ahead of the MMAs (skeleton 6.5 ms on cfg1).
+    const uint64_t pol_b = policy_evict_last();
+    const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
+    auto load_tile = [&](int t_it, int t_b, int s) {  // tile t_b of voxel-tile iteration t_it
+      const uint8_t* src;
+      if (t_b < n_hint) {
+        const int vt = int(blockIdx.x) + t_it * int(gridDim.x);
+        src = hint_tiles + (size_t(vt) * (n_hint / kParts) + t_b / kParts) * C::kBTileBytes;
+      } else {
+        int ba = rot + (t_b - n_hint);
+        if (ba >= nB) ba -= nB;
+        src = atiles + size_t(ba) * C::kBTileBytes;
+      }
+      mbar_arrive_expect_tx(b_full + s, C::kBBytes);
+      bulk_g2s(smem + C::kOffB + s * C::kBBytes, src, C::kBBytes, b_full + s, pol_b);
+    };
+    int r_it = 0, r_b = me;  // next tile to load: (voxel-tile iteration, position)
+    auto advance = [&](int& a_it, int& a_b, int by) {
+      a_b += by;
+      while (a_b >= T) {
+        a_b -= T;
+        ++a_it;
+      }
+    };
+    if constexpr (!PAIR) {
+      for (int s0 = me; s0 < C::kStages && uint32_t(s0) < total; s0 += kParts) {
+        if (elect_one()) load_tile(r_it, r_b, s0);
+        __syncwarp();
+        advance(r_it, r_b, kParts);
+      }
+    }
+    int p_st = 0;      // stage of this issuer's previous tile
+    uint32_t p_ph = 0;  // and the b_empty parity of its MMA
     int tb = me;    // completion barrier kk % kTBars
     int itk = -1;
     uint32_t vt_end = 0;  // first tile index of the next voxel tile
@@ -1312,11 +1350,23 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
         else
           mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
-      if (lane == 0) CBB_STAMP(4, kk);
-      if constexpr (PAIR)
+      if constexpr (PAIR) {
+        mbar_wait_cluster(acc_free + sacc, aph);
+        if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait_cluster(b_full + st, ph);
-      else
+      } else {
+        if (kk >= uint32_t(kParts) && kk - kParts + C::kStages < total) {
+          // refill the previous tile's stage with tile kk - 3 + kStages
+          mbar_wait(b_empty + p_st, p_ph);
+          if (elect_one()) load_tile(r_it, r_b, p_st);
+          __syncwarp();
+          advance(r_it, r_b, kParts);
+        }
+        mbar_wait(acc_free + sacc, aph);
+        if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait(b_full + st, ph);
+      }
+      aph ^= 1u;
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
@@ -1350,6 +1400,8 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
         CBB_STAMP(1, kk);
       }
       __syncwarp();
+      p_st = st;
+      p_ph = ph;
       sacc += kParts;
       if (sacc >= C::kAcc) sacc -= C::kAcc;
       tb += kParts;
@@ -1396,7 +1448,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
     int sacc = part;               // its accumulator stage kk % kAcc
     int tb = part;                 // its completion barrier kk % kTBars, phase (kk / kTBars) & 1
     uint32_t ph = 0;
-    int rel = part + C::kAcc;      // release barrier (kk + kAcc) % kStages
     for (int it = 0; it < my_vts; ++it) {
       const int vt = int(blockIdx.x) + it * int(gridDim.x);
       const int64_t v = int64_t(vt) * C::kVox + row;
@@ -1454,11 +1505,9 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
           // early release: the stage may be overwritten by tile kk + kAcc while we screen
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) arrive_lead(b_full + rel);
+          if (lane == 0) arrive_lead(acc_free + part);
           if (q == 0 && lane == 0) CBB_STAMP(3, kk);
           ph ^= 1u;
-          rel += kParts;
-          if (rel >= C::kStages) rel -= C::kStages;
         };
         // warm-start hint tiles: raise the running max, record nothing
         for (; kk < khint; kk += kParts) {
@@ -1509,7 +1558,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
             if (h + 1 == C::kChunks / kRegChunks) {
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) arrive_lead(b_full + rel);
+              if (lane == 0) arrive_lead(acc_free + part);
             }
             if (qt >= 0)
               screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win,
@@ -1525,8 +1574,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
             tb -= C::kTBars;
             ph ^= 1u;
           }
-          rel += kParts;
-          if (rel >= C::kStages) rel -= C::kStages;
         }
       }
       // ---- hand-off (no inter-part barrier): this part's surviving chunk entries are appended
@@ -1549,6 +1596,290 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
       tmem_dealloc2(tbase, 512);
     else
       tmem_dealloc(tbase, 512);
+  }
+}
+
+// ============================================================== dual-voxel-tile fp16 screen
+// Measured on cfg1 (1x B200): mf_tc_kernel's skeleton alone (epilogue reduced to wait + load +
+// release) takes 6.5 of its 8.4 ms and 4.5 ms without the atom stream -- the L2 -> SMEM copy of
+// every atom tile for every 128-voxel tile (68.7 GB per projection, ~9 TB/s) is the limiter.
+// This kernel screens TWO voxel tiles (256 voxels) against each streamed 64-atom tile: per tile
+// the issuer runs 2 x ksteps MMAs (M = 128, N = 64, one per voxel tile, A from TMEM) reading the
+// same SMEM stage, so the atom stream per (voxel, atom) pair halves.  Each epilogue thread owns
+// one row of both voxel tiles.  TMEM: 3 stages x [vt0 | vt1] x 64 fp16 accumulator columns + the
+// A double buffer 2 x [vt0 | vt1] x KP/2 = 448 (KP 32) / 512 (KP 64) columns.  Barriers, parts,
+// records, published thresholds and the hand-off are mf_tc_kernel's (fp16 path).
+template <int KP>
+struct TcDual {
+  static constexpr int BN = 64;
+  static constexpr int kChunks = 2;
+  static constexpr int kACols = KP / 2;         // one voxel tile's A columns
+  static constexpr int kABuf = 2 * kACols;      // one A buffer: [vt0 | vt1]
+  static constexpr int kAcc = 3;
+  static constexpr int kAccCols = 2 * BN;       // one stage: [vt0 scores | vt1 scores]
+  static constexpr int kAColOff = kAcc * kAccCols;
+  static_assert(kAColOff + 2 * kABuf <= 512, "TMEM budget");
+  static constexpr int kBBytes = BN * KP * 2;
+  static constexpr int kRing = 72 * 1024;
+  static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
+  static constexpr int kStages = (kStagesRaw / kParts) * kParts;
+  static_assert(kStages >= 2 * kAcc, "B ring too shallow");
+  static constexpr int kEpiWarps = 4 * kParts;
+  static constexpr int kFirstEpiWarp = 1 + kParts;
+  static constexpr int kThreads = (kFirstEpiWarp + kEpiWarps) * 32;
+  static constexpr int kVox = 128;
+  static constexpr int kSlots = kVox * kParts * 2;
+  static constexpr int kOffB = 0;
+  static constexpr int kOffCj = kOffB + kStages * kBBytes;
+  static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
+  static constexpr int kOffPthr = kOffCs + kCandCap * kSlots * 4;  // [2][kVox][4] u32
+  static constexpr int kOffBar = kOffPthr + 2 * kVox * 16;
+  static constexpr int kNumBars = 4 + 2 * kStages + kAcc;
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+  static constexpr int kSmem = kOffTmem + 16 + 1024;
+  static_assert(kSmem <= 227 * 1024, "shared memory");
+  static constexpr uint32_t kIdesc = idesc_f16_f16(128, BN);
+};
+
+template <int KP>
+__global__ void __launch_bounds__(TcDual<KP>::kThreads, 1)
+    mf_tc_dual_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
+                      const float* __restrict__ win_tc, const float* __restrict__ init_tc,
+                      DictView dv, int64_t n_pad, int2* __restrict__ cand,
+                      int2* __restrict__ meta, const uint8_t* __restrict__ hint_tiles,
+                      int n_hint) {
+  using C = TcDual<KP>;
+  constexpr int BN = C::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024_smem(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 2;
+  uint64_t* b_full = bars + 4;
+  uint64_t* b_empty = b_full + C::kStages;
+  uint64_t* t_full = b_empty + C::kStages;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t d = dv.d;
+  const int nB = int((d + BN - 1) / BN);
+  const int n_pt = (n_vt + 1) / 2;  // voxel-tile pairs (256 voxels)
+  const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
+  const int my_pts = (n_pt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  const int T = nB + n_hint;
+  const uint32_t total = uint32_t(my_pts) * uint32_t(T);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(a_full + i, 4);
+      mbar_init(a_empty + i, kParts);
+    }
+    for (int i = 0; i < C::kAcc; ++i) mbar_init(t_full + i, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(b_full + i, 1 + 4);
+      mbar_init(b_empty + i, 1);
+    }
+    for (int i = 0; i < C::kAcc; ++i)
+      for (int w = 0; w < 4; ++w) mbar_arrive(b_full + i);
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  for (int i = threadIdx.x; i < 2 * 4 * C::kVox; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem + C::kOffPthr)[i] = 0xFFFFFC00u;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer (bulk copies of atom tiles)
+    const uint64_t pol_b = policy_evict_last();
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < my_pts; ++it) {
+      const int pt = int(blockIdx.x) + it * int(gridDim.x);
+      int ba = rot;
+      for (int b = 0; b < T; ++b) {
+        mbar_wait(b_empty + st, ph ^ 1u);
+        if (elect_one()) {
+          const uint8_t* src =
+              b < n_hint ? hint_tiles + (size_t(pt) * (n_hint / kParts) + b / kParts) * C::kBBytes
+                         : dv.atoms_tc + size_t(ba) * C::kBBytes;
+          mbar_arrive_expect_tx(b_full + st, C::kBBytes);
+          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, C::kBBytes, b_full + st, pol_b);
+        }
+        __syncwarp();
+        if (b >= n_hint && ++ba == nB) ba = 0;
+        if (++st == C::kStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 1 && warp <= kParts) {
+    // ------------------------------------------------ MMA issuers: 2 voxel tiles per atom tile
+    const int me = warp - 1;
+    const int nks = mma_ksteps(dv.s);
+    const uint32_t b_base = smem_u32(smem + C::kOffB);
+    int sacc = me;
+    int itk = -1;
+    uint32_t vt_end = 0;
+    int st = me;
+    uint32_t ph = 0;
+    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
+      if (kk >= vt_end) {
+        ++itk;
+        vt_end += uint32_t(T);
+        mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
+      }
+      mbar_wait(b_full + st, ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kABuf);
+        const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
+#pragma unroll
+        for (int kq = 0; kq < KP / 16; ++kq) {
+          const uint64_t bdesc =
+              umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * BN * 128, KP < 64 ? KP : 64) +
+              uint64_t(2 * (kq & 3));
+          if (kq < nks) {
+#pragma unroll
+            for (int vv = 0; vv < 2; ++vv)
+              tc_mma_f16_ts(d_tm + uint32_t(vv * BN), a_tm + uint32_t(vv * C::kACols + kq * 8),
+                            bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
+          }
+        }
+        tc_commit(b_empty + st);
+        tc_commit(t_full + sacc);
+        if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
+      }
+      __syncwarp();
+      st += kParts;
+      if (st >= C::kStages) {
+        st -= C::kStages;
+        ph ^= 1u;
+      }
+    }
+  } else if (warp >= C::kFirstEpiWarp) {
+    // -------------------------------------------------- epilogue parts (one row of each tile)
+    const int e = warp - C::kFirstEpiWarp;
+    const int part = e >> 2, q = warp & 3;
+    const int row = q * 32 + lane;
+    int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
+    float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
+    const uint32_t t_stage = tbase + lane_off + uint32_t(part * C::kAccCols);
+    uint32_t* pthr0 = reinterpret_cast<uint32_t*>(smem + C::kOffPthr) + row * 4;
+    uint32_t* pthr1 = pthr0 + C::kVox * 4;
+
+    if (part == 0 && my_pts > 0) {
+      const int64_t v0 = int64_t(blockIdx.x) * 2 * C::kVox + row;
+      stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
+      stage_voxel_row<KP>(zrows, v0 + C::kVox, v0 + C::kVox < n, a_lane + uint32_t(C::kACols));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + 0);
+    }
+
+    uint32_t kk = uint32_t(part);
+    uint32_t ph = 0;
+    int rel = part + C::kAcc;
+    uint32_t r[32 * 2];
+    for (int it = 0; it < my_pts; ++it) {
+      const int pt = int(blockIdx.x) + it * int(gridDim.x);
+      const int64_t v0 = int64_t(pt) * 2 * C::kVox + row, v1 = v0 + C::kVox;
+      const bool live0 = v0 < n, live1 = v1 < n;
+      if (part == 0 && it + 1 < my_pts) {
+        const int nbuf = (it + 1) & 1;
+        mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const int64_t vn = int64_t(pt + int(gridDim.x)) * 2 * C::kVox + row;
+        const uint32_t ab = a_lane + uint32_t(nbuf * C::kABuf);
+        stage_voxel_row<KP>(zrows, vn, vn < n, ab);
+        stage_voxel_row<KP>(zrows, vn + C::kVox, vn + C::kVox < n, ab + uint32_t(C::kACols));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + nbuf);
+      }
+      const float win0 = live0 ? win_tc[v0] : -1.f, win1 = live1 ? win_tc[v1] : -1.f;
+      bool active0 = live0 && win0 >= 0.f, active1 = live1 && win1 >= 0.f;
+      const int slot0 = (part * 2) * C::kVox + row, slot1 = slot0 + C::kVox;
+      HCandList cl0{cj_base + slot0, cs_base + slot0, C::kSlots, 0,
+                    cand + int64_t(part) * kGCap * n_pad + (live0 ? v0 : 0), n_pad, 0, false};
+      HCandList cl1{cj_base + slot1, cs_base + slot1, C::kSlots, 0,
+                    cand + int64_t(part) * kGCap * n_pad + (live1 ? v1 : 0), n_pad, 0, false};
+      __half runmax0 = active0 ? __float2half_rd(fmaxf(init_tc[v0], -65504.f))
+                               : __ushort_as_half(0xFC00);
+      __half runmax1 = active1 ? __float2half_rd(fmaxf(init_tc[v1], -65504.f))
+                               : __ushort_as_half(0xFC00);
+      __half thr0 = __ushort_as_half(0x7C00), thr1 = __ushort_as_half(0x7C00);
+      const uint32_t tag = (uint32_t(it) & 0xffffu) << 16;
+      const uint32_t kbeg = uint32_t(it) * uint32_t(T), khint = kbeg + uint32_t(n_hint),
+                     kend = kbeg + uint32_t(T);
+      auto consume = [&]() {
+        mbar_wait(t_full + part, ph);
+        tc_fence_after();
+        __syncwarp();
+        tmem_ld32_pack16(t_stage, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32_pack16(t_stage + uint32_t(BN), *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_full + rel);
+        ph ^= 1u;
+        rel += kParts;
+        if (rel >= C::kStages) rel -= C::kStages;
+      };
+      for (; kk < khint; kk += kParts) {  // warm-start hint tiles
+        consume();
+        if (active0)
+          runmax0 = __hmax(runmax0, tile_max_f16<2>(*reinterpret_cast<uint32_t(*)[32]>(r)));
+        if (active1)
+          runmax1 = __hmax(runmax1, tile_max_f16<2>(*reinterpret_cast<uint32_t(*)[32]>(r + 32)));
+      }
+      if (active0) {
+        thr0 = __float2half_rd(__half2float(runmax0) - win0);
+        pthr0[part] = tag | __half_as_ushort(thr0);
+      }
+      if (active1) {
+        thr1 = __float2half_rd(__half2float(runmax1) - win1);
+        pthr1[part] = tag | __half_as_ushort(thr1);
+      }
+      int ba = rot + int(kk - khint);
+      if (ba >= nB) ba -= nB;
+      for (; kk < kend; kk += kParts) {
+        const uint4 w0 = lds_v4_volatile(pthr0), w1 = lds_v4_volatile(pthr1);
+        consume();
+        thr0 = __hmax(thr0, shared_thr(w0, tag));
+        thr1 = __hmax(thr1, shared_thr(w1, tag));
+#if defined(CBB_EPI_EMPTY)  // development timing variant (wrong results)
+        if (r[0] == 0x7fff7fffu) runmax0 = __hmax(runmax0, as_h2(r[33]).x);
+#else
+        screen_tile<2>(*reinterpret_cast<uint32_t(*)[32]>(r), int64_t(ba) * BN, win0, runmax0,
+                       thr0, active0, cl0, pthr0 + part, tag);
+        screen_tile<2>(*reinterpret_cast<uint32_t(*)[32]>(r + 32), int64_t(ba) * BN, win1,
+                       runmax1, thr1, active1, cl1, pthr1 + part, tag);
+#endif
+        ba += kParts;
+        if (ba >= nB) ba -= nB;
+      }
+      if (live0) {
+        const float rm = __half2float(runmax0);
+        meta[int64_t(part) * n_pad + v0] =
+            make_int2((win0 >= 0.f) ? cl0.finish(rm - win0) : 0, __float_as_int(rm));
+      }
+      if (live1) {
+        const float rm = __half2float(runmax1);
+        meta[int64_t(part) * n_pad + v1] =
+            make_int2((win1 >= 0.f) ? cl1.finish(rm - win1) : 0, __float_as_int(rm));
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
   }
 }
 
@@ -2214,6 +2545,45 @@ static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const Dic
   return kOk;
 }
 
+// Dual-voxel-tile fp16 screen (mf_tc_dual_kernel): opt-in with CBB_TC_DUAL=1 (measured on
+// cfg1 with a dedicated producer warp: 10.5 ms vs 8.5 ms).
+static bool tc_dual_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CBB_TC_DUAL");
+    v = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return v != 0;
+}
+
+template <int KP>
+static int launch_tc_dual(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                          int grid, int n_vt, cudaStream_t st) {
+  using C = TcDual<KP>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_dual_kernel<KP>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr_set = true;
+  }
+  int n_hint = 0;
+  if (zs.hint) {  // IPG warm start: each voxel-tile pair's own hint atoms screened first
+    const int vox = 2 * C::kVox;
+    const int n_g = int((n + vox - 1) / vox);
+    const int nh = (vox + C::BN - 1) / C::BN;
+    const int64_t chunks = int64_t(n_g) * nh * C::BN * (KP / 8);
+    hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
+        zs.hint, n, dv.d, n_g, vox, dv.atoms_tc, KP, 0, C::BN, nh, w.hint_tiles);
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    n_hint = kParts * nh;
+  }
+  mf_tc_dual_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(
+      w.ztiles, n, n_vt, w.win_tc, w.init_tc, dv, w.n_pad, w.cand, w.meta, w.hint_tiles, n_hint);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
 template <int KP, bool SPLIT = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
@@ -2232,6 +2602,11 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   const int n_vt = int((n + C1::kVox - 1) / C1::kVox);
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if constexpr (!SPLIT) {
+    // dual-voxel-tile screen when every CTA gets at least one voxel-tile pair
+    const int n_pt = (n_vt + 1) / 2;
+    if (tc_dual_enabled() && n_pt >= grid) return launch_tc_dual<KP>(w, n, zs, dv, grid, n_vt, st);
+  }
   if (grid > n_vt) grid = n_vt;
   // CTA pairs halve the atom stream; used when every pair is co-resident (persistent kernel),
   // at most 5% of the SMs idle, and every CTA gets at least two voxel tiles

@@ -22,7 +22,8 @@ assert fn(buf.ctypes.data, T) == 0
 t = buf.reshape(T, 8).astype(np.float64)
 ks = np.arange(200, 1900)
 def med(x): return float(np.median(x))
-print("issuer: wait b_full (4->0)          ", med(t[ks, 0] - t[ks, 4]))
+print("issuer: data wait after acc_free (4->0)", med(t[ks, 0] - t[ks, 4]))
+print("release(k-3) -> acc_free seen (3->4)", med(t[ks, 4] - t[ks - 3, 3]))
 print("issuer: issue+commit (0->1)         ", med(t[ks, 1] - t[ks, 0]))
 print("issuer: loop overhead (1 -> next 4) ", med(t[ks + 3, 4] - t[ks, 1]))
 print("epi: wait t_full (5->2)             ", med(t[ks, 2] - t[ks, 5]))
