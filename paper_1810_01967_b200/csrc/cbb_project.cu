@@ -1238,8 +1238,8 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 0 && PAIR) {
-    // ------------------------------------------------ PAIR producer (bulk copies of atom tiles)
+  if (warp == 0) {
+    // ------------------------------------------------ producer (bulk copies of atom tiles)
     const uint64_t pol_b = policy_evict_last();
     const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
     int st = 0;
@@ -1299,43 +1299,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
     static_assert(C::kAcc == kParts, "issuer i always fills accumulator stage i");
     int sacc = me;  // accumulator stage kk % kAcc
     uint32_t aph = 1;  // acc_free parity: the first use of each stage passes at once
-    // The issuers also load the atom tiles (single CTA): issuer i fills the ring stages of its
-    // own tiles, refilling the stage of its previous tile kk - 3 with tile kk - 3 + kStages
-    // (that MMA retired while this issuer waited for its next stage).  A dedicated producer
-    // warp was the measured limiter: ~50 dependent instructions per tile on one warp took
-    // ~300 clk, so it ran barely one tile ahead of the MMAs (skeleton 6.5 ms on cfg1).
-    const uint64_t pol_b = policy_evict_last();
-    const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
-    auto load_tile = [&](int t_it, int t_b, int s) {  // tile t_b of voxel-tile iteration t_it
-      const uint8_t* src;
-      if (t_b < n_hint) {
-        const int vt = int(blockIdx.x) + t_it * int(gridDim.x);
-        src = hint_tiles + (size_t(vt) * (n_hint / kParts) + t_b / kParts) * C::kBTileBytes;
-      } else {
-        int ba = rot + (t_b - n_hint);
-        if (ba >= nB) ba -= nB;
-        src = atiles + size_t(ba) * C::kBTileBytes;
-      }
-      mbar_arrive_expect_tx(b_full + s, C::kBBytes);
-      bulk_g2s(smem + C::kOffB + s * C::kBBytes, src, C::kBBytes, b_full + s, pol_b);
-    };
-    int r_it = 0, r_b = me;  // next tile to load: (voxel-tile iteration, position)
-    auto advance = [&](int& a_it, int& a_b, int by) {
-      a_b += by;
-      while (a_b >= T) {
-        a_b -= T;
-        ++a_it;
-      }
-    };
-    if constexpr (!PAIR) {
-      for (int s0 = me; s0 < C::kStages && uint32_t(s0) < total; s0 += kParts) {
-        if (elect_one()) load_tile(r_it, r_b, s0);
-        __syncwarp();
-        advance(r_it, r_b, kParts);
-      }
-    }
-    int p_st = 0;      // stage of this issuer's previous tile
-    uint32_t p_ph = 0;  // and the b_empty parity of its MMA
     int tb = me;    // completion barrier kk % kTBars
     int itk = -1;
     uint32_t vt_end = 0;  // first tile index of the next voxel tile
@@ -1355,13 +1318,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
         if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait_cluster(b_full + st, ph);
       } else {
-        if (kk >= uint32_t(kParts) && kk - kParts + C::kStages < total) {
-          // refill the previous tile's stage with tile kk - 3 + kStages
-          mbar_wait(b_empty + p_st, p_ph);
-          if (elect_one()) load_tile(r_it, r_b, p_st);
-          __syncwarp();
-          advance(r_it, r_b, kParts);
-        }
         mbar_wait(acc_free + sacc, aph);
         if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait(b_full + st, ph);
@@ -1400,8 +1356,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
         CBB_STAMP(1, kk);
       }
       __syncwarp();
-      p_st = st;
-      p_ph = ph;
       sacc += kParts;
       if (sacc >= C::kAcc) sacc -= C::kAcc;
       tb += kParts;
