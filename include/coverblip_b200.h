@@ -64,7 +64,8 @@ enum {
   CBB_ALGO_TCGEN05 = 1,     /* fp16 operands, fp16 accumulators (2s < 64) */
   CBB_ALGO_FFMA = 2,        /* fp32 FFMA screen */
   CBB_ALGO_EXHAUSTIVE = 3,  /* fp64 scan of every atom */
-  CBB_ALGO_TCGEN05_SPLIT = 4 /* hi/lo fp16 operands, fp32 accumulators (s <= 21) */
+  CBB_ALGO_TCGEN05_SPLIT = 4, /* hi/lo fp16 operands, fp32 accumulators (s <= 21) */
+  CBB_ALGO_TCGEN05_HI32 = 5  /* fp16 operands, fp32 accumulators (2s < 64) */
 };
 
 int cbb_abi_version(void);

@@ -23,7 +23,7 @@ c_vp = ctypes.c_void_p
 
 ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED, ERR_CUFFT = 1, 2, 3, 4
 
-ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3, "tcgen05_split": 4}
+ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3, "tcgen05_split": 4, "tcgen05_hi32": 5}
 
 
 class DictView(ctypes.Structure):

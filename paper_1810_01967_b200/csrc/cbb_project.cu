@@ -586,7 +586,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       const double fhi = f16_bits_to_double(hi);
       const int e = c * s + k;
       row[e] = hi;
-      if (split) {  // [z_hi | z_lo | z_hi]: z~ = z_hi + z_lo
+      if (split == 1) {  // [z_hi | z_lo | z_hi]: z~ = z_hi + z_lo
         const unsigned short lo = f16_bits_rn(x[c] - fhi);
         const double flo = f16_bits_to_double(lo);
         row[2 * s + e] = lo;
@@ -602,7 +602,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
       }
     }
   }
-  row[split ? 6 * s : 2 * s] = kF16One;  // sentinel column right after the data (< kpad)
+  row[split == 1 ? 6 * s : 2 * s] = kF16One;  // sentinel column right after the data (< kpad)
   for (int c = 0; c < kpad / 8; ++c) {
     uint4 pk;
     pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
@@ -613,7 +613,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   }
   const double sd = bounds[kBScaleD];
   double eb;
-  if (split) {
+  if (split == 1) {
     // s~ = z_hi.d_hi + z_lo.d_hi + z_hi.d_lo = z~.d~ - z_lo.d_lo (z~ = z_hi + z_lo, d~ likewise):
     //   |s~ - s| <= ||scale_v z - z~|| scale_d max||d|| + ||z~|| max||scale_d d - d~||
     //             + ||z_lo|| max||d_lo|| + acc * ||A_v|| max||B_j||
@@ -626,9 +626,14 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
          acc_tc * sqrt(2.0 * nhi + nlo) * bounds[kBRowMax] + nq * 0x1p-40;
   } else {
     const double dh = bounds[kBDhMax], delh = bounds[kBDeltaH];
-    const double nq = double(mma_ksteps(s));  // fp16 roundings of nonzero partial sums
-    const double acc_tc = nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
-    eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh + nq * 0x1p-24;
+    const double nq = double(mma_ksteps(s));
+    // fp16 accumulators: one fp16 rounding per issued instruction of a partial sum bounded by
+    // sum|a_k b_k| <= ||z~|| max||d~||; HI32 (fp32 accumulators): the split screen's model,
+    // < 16 truncations below 2^-24 of the largest term + one fp32 rounding per instruction
+    const double acc_tc = split == 2 ? nq * 18.0 * 0x1p-24
+                                     : nq * (0x1p-11 * (1.0 + 0x1p-9) + 0x1p-19);
+    eb = sqrt(eh) * sd * dmax + sqrt(nzh) * delh + acc_tc * sqrt(nzh) * dh +
+         nq * (split == 2 ? 0x1p-40 : 0x1p-24);
   }
   win_tc[v] = __double2float_ru(2.0 * eb * 1.001 + 1e-30);
   if (init_tc) {
@@ -920,11 +925,16 @@ constexpr int kParts = 3;
 // PAIR: the CTAs of a cluster pair run cta_group::2 MMAs (M = 256: each CTA's 128 voxels); every
 // CTA bulk-copies only its half of each atom tile (kBNloc rows), which halves the L2 -> SMEM
 // atom stream that bounds the single-CTA kernel.
-template <int KP, bool SPLIT = false, bool PAIR = false>
+// HI32: the fp16 operand rows of the fp16 screen (2s + 1 columns) with FP32 accumulators: the
+// screen issues the fp16 screen's K-steps but its window is the operand rounding only
+// (~2^-10 |z| instead of ~2^-8): the split screen's fp32 epilogue on 128-atom tiles.
+template <int KP, bool SPLIT = false, bool PAIR = false, bool HI32 = false>
 struct TcCfg {
   static_assert(!SPLIT || KP == 64 || KP == 128, "split tiles are 64 or 128 wide");
+  static_assert(!(SPLIT && HI32), "one operand format");
+  static constexpr bool kF32 = SPLIT || HI32;  // fp32 accumulators, fp32 epilogue
   // 32-atom chunks per tile (split: the tile is one split_rows(KP)-row storage tile)
-  static constexpr int kChunks = SPLIT ? split_rows(KP) / 32 : (KP == 32 ? 5 : 4);
+  static constexpr int kChunks = SPLIT ? split_rows(KP) / 32 : HI32 ? 4 : (KP == 32 ? 5 : 4);
   static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 / 64 (split)
   static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
   static constexpr int kAcc = 3;                             // x BN accumulator columns
@@ -965,7 +975,7 @@ struct TcCfg {
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
   static constexpr int kM = PAIR ? 256 : 128;
-  static constexpr uint32_t kIdesc = SPLIT ? idesc_f16_f32(kM, BN) : idesc_f16_f16(kM, BN);
+  static constexpr uint32_t kIdesc = kF32 ? idesc_f16_f32(kM, BN) : idesc_f16_f16(kM, BN);
   static constexpr int kMinTiles = kParts;  // every part owns >= 1 tile per voxel tile
 };
 
@@ -1168,13 +1178,13 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
   tc_wait_st();
 }
 
-template <int KP, bool SPLIT, bool PAIR>
-__global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
+template <int KP, bool SPLIT, bool PAIR, bool HI32>
+__global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
                  DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta,
                  const uint8_t* __restrict__ hint_tiles, int n_hint) {
-  using C = TcCfg<KP, SPLIT, PAIR>;
+  using C = TcCfg<KP, SPLIT, PAIR, HI32>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
@@ -1431,7 +1441,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
       float runmax_f = active ? init_tc[v] : -INFINITY;
       float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
       const uint32_t kbeg = uint32_t(it) * uint32_t(T), kend = kbeg + uint32_t(T);
-      if constexpr (!SPLIT) {
+      if constexpr (!C::kF32) {
         // fp16 screen: the part owns accumulator stage `part` and completion barrier `part`
         // (kAcc == kTBars == kParts), whose phase flips every tile.  The three parts publish
         // their thresholds per voxel in shared memory, tagged with the voxel-tile iteration:
@@ -1490,7 +1500,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
           if (ba >= nB) ba -= nB;
         }
       } else {
-        // split screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles
+        // split / HI32 screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles
         // are screened in halves and released after the last half is loaded
         for (; kk < kend; kk += kParts) {
           const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
@@ -1535,7 +1545,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR>::kThreads, 1)
       // rescore_kernel merges the parts and rescans the flagged groups in fp64
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(1, it);
       if (live) {
-        const float rm = SPLIT ? runmax_f : __half2float(runmax);
+        const float rm = C::kF32 ? runmax_f : __half2float(runmax);
         const int total = (win >= 0.f) ? cl.finish(rm - win) : 0;
         meta[int64_t(part) * n_pad + v] = make_int2(total, __float_as_int(rm));
       }
@@ -2464,10 +2474,10 @@ static int max_coresident_pairs(K kernel, int threads, int smem) {
   return nc;
 }
 
-template <int KP, bool SPLIT, bool PAIR>
+template <int KP, bool SPLIT, bool PAIR, bool HI32>
 static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                         int grid, int n_vt, cudaStream_t st) {
-  using C = TcCfg<KP, SPLIT, PAIR>;
+  using C = TcCfg<KP, SPLIT, PAIR, HI32>;
   int n_hint = 0;
   if (zs.hint) {  // IPG warm start: the voxel tiles' (pairs') own hint atoms screened first
     const int vox = PAIR ? 2 * C::kVox : C::kVox;
@@ -2493,7 +2503,7 @@ static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const Dic
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 1 : 0;
-  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR>, w.ztiles, n, n_vt,
+  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR, HI32>, w.ztiles, n, n_vt,
                                   (const float*)w.win_tc, (const float*)w.init_tc, dv, w.n_pad,
                                   w.cand, w.meta, (const uint8_t*)w.hint_tiles, n_hint));
   return kOk;
@@ -2538,25 +2548,25 @@ static int launch_tc_dual(const ProjWs& w, int64_t n, const ZSource& zs, const D
   return kOk;
 }
 
-template <int KP, bool SPLIT = false>
+template <int KP, bool SPLIT = false, bool HI32 = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
                      const ProjOut& out, int max_ctas, cudaStream_t st) {
-  using C1 = TcCfg<KP, SPLIT, false>;
-  using C2 = TcCfg<KP, SPLIT, true>;
+  using C1 = TcCfg<KP, SPLIT, false, HI32>;
+  using C2 = TcCfg<KP, SPLIT, true, HI32>;
   static bool attr_set = false;
   static int pairs = 0;
   if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false, HI32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, true>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, true, HI32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmem));
-    pairs = max_coresident_pairs(mf_tc_kernel<KP, SPLIT, true>, C2::kThreads, C2::kSmem);
+    pairs = max_coresident_pairs(mf_tc_kernel<KP, SPLIT, true, HI32>, C2::kThreads, C2::kSmem);
     attr_set = true;
   }
   const int n_vt = int((n + C1::kVox - 1) / C1::kVox);
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if constexpr (!SPLIT) {
+  if constexpr (!SPLIT && !HI32) {
     // dual-voxel-tile screen when every CTA gets at least one voxel-tile pair
     const int n_pt = (n_vt + 1) / 2;
     if (tc_dual_enabled() && n_pt >= grid) return launch_tc_dual<KP>(w, n, zs, dv, grid, n_vt, st);
@@ -2566,8 +2576,8 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
   // at most 5% of the SMs idle, and every CTA gets at least two voxel tiles
   int grid2 = 2 * pairs < grid ? 2 * pairs : grid - grid % 2;
   if (tc_pair_enabled() && grid2 >= 8 && grid2 * 20 >= grid * 19 && n_vt >= 2 * grid2)
-    return launch_tc_as<KP, SPLIT, true>(w, n, zs, dv, grid2, n_vt, st);
-  return launch_tc_as<KP, SPLIT, false>(w, n, zs, dv, grid, n_vt, st);
+    return launch_tc_as<KP, SPLIT, true, HI32>(w, n, zs, dv, grid2, n_vt, st);
+  return launch_tc_as<KP, SPLIT, false, HI32>(w, n, zs, dv, grid, n_vt, st);
 }
 
 template <int S>
@@ -2697,7 +2707,7 @@ int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStr
 // algo: 0 = auto (split tcgen05 for coherent dictionaries with s <= 21, else tcgen05 when
 // 2s < 64, else FFMA / fp64),
 // 1 = tcgen05 (fp16 accumulators), 2 = FFMA, 3 = exhaustive fp64, 4 = split tcgen05 (hi/lo fp16
-// operands, fp32 accumulators, s <= 21)
+// operands, fp32 accumulators, s <= 21), 5 = HI32 tcgen05 (fp16 operands, fp32 accumulators)
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st) {
   if (n < 0) return kErrArgument;
@@ -2715,10 +2725,10 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   const bool tc_ok = (2 * dv.s < 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
   const bool split_ok = tc_ok && dv.s <= kSplitMaxS && dv.atoms_tc2 != nullptr;
   if (algo == 0) algo = (split_ok && dv.prefer_split) ? 4 : tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
-  if (algo == 1 && !tc_ok) return kErrUnsupported;
+  if ((algo == 1 || algo == 5) && !tc_ok) return kErrUnsupported;
   if (algo == 4 && !split_ok) return kErrUnsupported;
-  const bool split = algo == 4;
-  if (split) algo = 1;  // same pipeline, split operand tiles
+  const bool split = algo == 4, hi32 = algo == 5;
+  if (split || hi32) algo = 1;  // same pipeline, other operand tiles / accumulator format
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
   CBB_CUDA_TRY(cudaMemsetAsync(w.heavy_count, 0, sizeof(int), st));
@@ -2728,12 +2738,14 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
         zs, n, n_pad, dv.s, split ? split_kp(dv.s) : dv.kpad, dv.bounds,
         algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
-        algo == 1 ? w.init_tc : nullptr, split ? 1 : 0);
+        algo == 1 ? w.init_tc : nullptr, split ? 1 : hi32 ? 2 : 0);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
     int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, o, max_ctas, st)
                                            : launch_tc<128, true>(w, n, zr, dv, o, max_ctas, st))
+             : hi32 ? (dv.kpad == 32 ? launch_tc<32, false, true>(w, n, zr, dv, o, max_ctas, st)
+                                     : launch_tc<64, false, true>(w, n, zr, dv, o, max_ctas, st))
              : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
                                             : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
                            : dispatch_ffma(w, n, zr, dv, o, st);
