@@ -1248,8 +1248,44 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 0) {
+  if (warp == 0 && !PAIR) {
     // ------------------------------------------------ producer (bulk copies of atom tiles)
+    // Lane 0 alone runs the loop (the other lanes wait at the final barrier): no elect /
+    // reconvergence code per tile.
+    if (lane == 0) {
+      const uint64_t pol_b = policy_evict_last();
+      const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
+      const uint32_t b_full0 = smem_u32(b_full), b_empty0 = smem_u32(b_empty);
+      const uint32_t ring0 = smem_u32(smem + C::kOffB);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < my_vts; ++it) {
+        const int vt = int(blockIdx.x) + it * int(gridDim.x);
+        const uint8_t* hsrc = hint_tiles + size_t(vt) * (n_hint / kParts) * C::kBTileBytes;
+        const uint8_t* asrc = atiles + size_t(rot) * C::kBTileBytes;
+        const uint8_t* aend = atiles + size_t(nB) * C::kBTileBytes;
+        for (int b = 0; b < T; ++b) {
+          mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
+          const uint8_t* src;
+          if (b < n_hint) {
+            src = hsrc + size_t(b / kParts) * C::kBTileBytes;
+          } else {
+            src = asrc;
+            asrc += C::kBTileBytes;
+            if (asrc == aend) asrc = atiles;
+          }
+          mbar_arrive_expect_tx_addr(b_full0 + 8 * st, C::kBBytes);
+          bulk_g2s_addr(ring0 + st * C::kBBytes, src, C::kBBytes, b_full0 + 8 * st, pol_b);
+          CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
+          if (++st == C::kStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------ PAIR producer (half of every atom tile)
     const uint64_t pol_b = policy_evict_last();
     const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
     int st = 0;

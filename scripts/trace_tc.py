@@ -34,6 +34,8 @@ print("epi: part period (2 -> next 2)      ", med(t[ks + 3, 2] - t[ks, 2]))
 print("commit -> t_full ready (1->2)       ", med(t[ks, 2] - t[ks, 1]))
 print("release(k-3) -> issuer ready (3->0) ", med(t[ks, 0] - t[ks - 3, 3]))
 print("producer issue(k) -> issuer ready   ", med(t[ks, 0] - t[ks, 7]))
+KS = int(os.environ.get("TRACE_STAGES", "9"))
+print("commit(k) -> producer issue(k+S)    ", med(t[ks + KS, 7] - t[ks, 1]), "(S = %d)" % KS)
 print("tile period (issuer ready k -> k+1) ", med(t[ks + 1, 0] - t[ks, 0]))
 print("frac of part time waiting           ", med((t[ks, 2] - t[ks, 5]) / (t[ks + 3, 2] - t[ks, 2])))
 vt = np.zeros(256 * 4, dtype=np.int64)
