@@ -32,8 +32,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st);
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st);
 int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st);
-int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile, int b_tile,
-                    float* out, cudaStream_t st);
+int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int s, int a_tile,
+                    int b_tile, float* out, cudaStream_t st);
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr, cudaStream_t st);
 int trace_dump(long long* host, int count);
 int scaled_rows(const DictView& dv, int64_t offset, const int64_t* idx, const double* gamma,
@@ -207,7 +207,8 @@ int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_ti
   if (int rc = check_view(dict)) return rc;
   if (2 * dict->s >= 64) return kErrUnsupported;
   // voxel tiles sit at the start of the projection workspace
-  return tc_debug_scores(workspace, dict->atoms_tc, dict->kpad, a_tile, b_tile, out, S(stream));
+  return tc_debug_scores(workspace, dict->atoms_tc, dict->kpad, dict->s, a_tile, b_tile, out,
+                         S(stream));
 }
 
 // development only (not in the public header): per-tile clock stamps of CTA 0

@@ -68,13 +68,17 @@ __host__ __device__ inline uint32_t split_elem_offset(int r, int e, int rows) {
          uint32_t((((e & 63) >> 3) ^ (r & 7)) * 16) + uint32_t(e & 7) * 2u;
 }
 
-// Byte offset of (row r, 16-byte chunk c) inside a 128-row tile.
-__host__ __device__ inline uint32_t tile_chunk_offset(int r, int c, int kpad) {
-  if (kpad == 32) {  // 64 B rows, Swizzle<2,4,3>: chunk bits [4,6) ^= addr bits [7,9)
-    return uint32_t(r) * 64u + uint32_t((c ^ ((r >> 1) & 3)) * 16);
-  }
-  // 128 B rows, Swizzle<3,4,3>: chunk bits [4,7) ^= addr bits [7,10)
-  return uint32_t(r) * 128u + uint32_t((c ^ (r & 7)) * 16);
+// fp16 atom operand storage (non-split screens): the UMMA K-major layout WITHOUT swizzle, i.e.
+// 8-row groups of tc_nc(s) core matrices (8 rows x 16 B each, chunk c = columns [8c, 8c+8)),
+// group after group.  Only the ceil((2s+1)/8) chunks that carry data or the sentinel are stored
+// (s = 10: 48 B per atom instead of 64), and any 8-row-aligned window of rows is one flat bulk
+// copy.  When tc_nc is odd, the last K = 16 step's second core matrix (all-zero voxel columns)
+// reads whatever finite fp16 data follows (the next group's chunk 0, or the zeroed tail of the
+// stage): zero times finite adds nothing.
+__host__ __device__ inline int tc_nc(int s) { return (2 * s + 1 + 7) / 8; }
+// byte offset of (row j, chunk c) from the start of the row sequence (j a multiple of 8 there)
+__host__ __device__ inline size_t atom_chunk_offset(int64_t j, int c, int nc) {
+  return size_t(j >> 3) * size_t(nc) * 128u + size_t(c) * 128u + size_t(j & 7) * 16u;
 }
 
 // ---------------------------------------------------------------- misc device
@@ -191,6 +195,10 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
                : "memory");
+}
+// generic-proxy shared-memory writes become visible to the async proxy (tensor core reads)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -345,6 +353,18 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, int kpa
   d |= uint64_t(1u) << 46;                             // descriptor version (sm_100)
   const uint64_t layout = (kpad == 32) ? 4u /*SWIZZLE_64B*/ : 2u /*SWIZZLE_128B*/;
   d |= layout << 61;
+  return d;
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle (core matrices 8 rows x 16 B): LBO = byte
+// stride between the two core matrices of a K = 16 step, SBO = byte stride between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc_interleave(uint32_t smem_addr, uint32_t lbo,
+                                                         uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1u) << 46;  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
   return d;
 }
 

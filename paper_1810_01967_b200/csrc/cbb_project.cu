@@ -359,19 +359,21 @@ __device__ __forceinline__ double dict_scale(const float* bounds) {
   return ldexp(1.0, -e);
 }
 
-// Pass 2: fp16 UMMA tiles of scale_d * d (pre-swizzled, one bulk copy per 64-atom tile) and
-// their bounds.  2s <= 64 only (tensor-core path).
+// Pass 2: fp16 UMMA rows of scale_d * d in the no-swizzle core-matrix layout (atom_chunk_offset,
+// tc_nc(s) chunks per row) and their bounds.  2s <= 64 only (tensor-core path).
 __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, int64_t d_pad,
-                               int s, int kpad, uint8_t* __restrict__ atoms_tc,
+                               int s, uint8_t* __restrict__ atoms_tc,
                                float* __restrict__ bounds) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= d_pad) return;
-  const int tile = int(j / kTileRows), r = int(j % kTileRows);
-  uint8_t* trow = atoms_tc + size_t(tile) * kTileRows * kpad * 2;
+  const int nc = tc_nc(s);
+  auto elem = [&](int e) {
+    return reinterpret_cast<unsigned short*>(atoms_tc + atom_chunk_offset(j, e >> 3, nc) +
+                                             (e & 7) * 2);
+  };
   const int e_sent = 2 * s;  // sentinel right after the data: nq = ceil((2s+1)/16) K-steps
   if (j >= d) {  // zero-padded row of the last tile: sentinel score -65504 for every voxel
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_sent >> 3, kpad) +
-                                       (e_sent & 7) * 2) = kF16MinusMax;
+    *elem(e_sent) = kF16MinusMax;
     return;
   }
   const double sc = dict_scale(bounds);
@@ -382,12 +384,8 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
     const double re = a.x * sc, im = a.y * sc;
     const unsigned short hre = f16_bits_rn(re), him = f16_bits_rn(im);
     const double fre = f16_bits_to_double(hre), fim = f16_bits_to_double(him);
-    // element e -> 16B chunk e/8, offset (e%8)*2 bytes
-    const int e_re = k, e_im = s + k;
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_re >> 3, kpad) +
-                                       (e_re & 7) * 2) = hre;
-    *reinterpret_cast<unsigned short*>(trow + tile_chunk_offset(r, e_im >> 3, kpad) +
-                                       (e_im & 7) * 2) = him;
+    *elem(k) = hre;
+    *elem(s + k) = him;
     nrm_h += fre * fre + fim * fim;
     del += (re - fre) * (re - fre) + (im - fim) * (im - fim);
   }
@@ -944,8 +942,10 @@ struct TcCfg {
   static constexpr int kBNloc = PAIR ? BN / 2 : BN;          // atom rows in this CTA's SMEM
   static constexpr int kRowBytes = (KP < 64 ? KP : 64) * 2;   // bytes per row of a K block
   static constexpr int kBlk = KP <= 64 ? 1 : KP / 64;         // K blocks per tile
-  static constexpr int kBTileBytes = BN * KP * 2;             // one atom tile in global memory
-  static constexpr int kBBytes = kBNloc * KP * 2;             // its part in this CTA
+  // split tiles in global memory / this CTA's part (= the ring's stage stride); the fp16 screens
+  // copy only tc_nc(s) 16-byte chunks per row (tile_bytes / copy_bytes in the kernel)
+  static constexpr int kBTileBytes = BN * KP * 2;
+  static constexpr int kBBytes = kBNloc * KP * 2;
   static_assert(kBNloc % 8 == 0, "8-row swizzle groups");
 #ifdef CBB_RING_KB
   static constexpr int kRing = CBB_RING_KB * 1024;
@@ -1200,6 +1200,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t d = dv.d;
   const int nB = int((d + BN - 1) / BN);
+  // atom tile bytes in global memory and this CTA's copy of it: the fp16 screens store
+  // tc_nc(s) chunks per row (no-swizzle layout), the split screen full swizzled K rows
+  const int nc = tc_nc(dv.s);
+  const uint32_t tile_bytes = SPLIT ? uint32_t(C::kBTileBytes) : uint32_t(BN * nc * 16);
+  const uint32_t copy_bytes = SPLIT ? uint32_t(C::kBBytes) : uint32_t(C::kBNloc * nc * 16);
   // PAIR: the two CTAs (ranks 0 = leader, 1) of a cluster stream the same atom tiles in lockstep
   // (same rotation, same number of voxel tiles: the surplus ones are dead, every row v >= n).
   // The leader's issuers run the pair's MMAs; the odd CTA's epilogue and producer signal the
@@ -1242,6 +1247,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   // and would only contribute -inf)
   for (int i = threadIdx.x; i < 4 * C::kVox; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem + C::kOffPthr)[i] = 0xFFFFFC00u;
+  if constexpr (!SPLIT) {  // finite (zero) stage tails: see atom_chunk_offset
+    for (int i = threadIdx.x; i < C::kStages * C::kBBytes / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem + C::kOffB)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive
@@ -1250,37 +1260,45 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
 
   if (warp == 0 && !PAIR) {
     // ------------------------------------------------ producer (bulk copies of atom tiles)
-    // Lane 0 alone runs the loop (the other lanes wait at the final barrier): no elect /
-    // reconvergence code per tile.
-    if (lane == 0) {
+    // kParts lanes, lane p copies the tiles k = p (mod kParts) (kStages % kParts == 0: it owns
+    // the stages p, p + kParts, ...).  A cp.async.bulk blocks its thread ~140 clk and the
+    // empty-barrier wait ~150 clk (scripts/ubench_bulk.cu): one thread streams a tile per
+    // ~390 clk, three lanes one per ~175 clk, against ~160 clk of MMA per tile.
+    if (lane < kParts) {
       const uint64_t pol_b = policy_evict_last();
       const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
       const uint32_t b_full0 = smem_u32(b_full), b_empty0 = smem_u32(b_empty);
       const uint32_t ring0 = smem_u32(smem + C::kOffB);
-      int st = 0;
+      int st = lane;
       uint32_t ph = 0;
-      for (int it = 0; it < my_vts; ++it) {
-        const int vt = int(blockIdx.x) + it * int(gridDim.x);
-        const uint8_t* hsrc = hint_tiles + size_t(vt) * (n_hint / kParts) * C::kBTileBytes;
-        const uint8_t* asrc = atiles + size_t(rot) * C::kBTileBytes;
-        const uint8_t* aend = atiles + size_t(nB) * C::kBTileBytes;
-        for (int b = 0; b < T; ++b) {
-          mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
-          const uint8_t* src;
-          if (b < n_hint) {
-            src = hsrc + size_t(b / kParts) * C::kBTileBytes;
-          } else {
-            src = asrc;
-            asrc += C::kBTileBytes;
-            if (asrc == aend) asrc = atiles;
-          }
-          mbar_arrive_expect_tx_addr(b_full0 + 8 * st, C::kBBytes);
-          bulk_g2s_addr(ring0 + st * C::kBBytes, src, C::kBBytes, b_full0 + 8 * st, pol_b);
-          CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
-          if (++st == C::kStages) {
-            st = 0;
-            ph ^= 1u;
-          }
+      int it = 0, b = lane;  // voxel-tile iteration and tile index inside it
+      while (b >= T) {
+        b -= T;
+        ++it;
+      }
+      for (uint32_t kk = uint32_t(lane); kk < total; kk += kParts) {
+        mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
+        const uint8_t* src;
+        if (b < n_hint) {
+          const int vt = int(blockIdx.x) + it * int(gridDim.x);
+          src = hint_tiles + (size_t(vt) * (n_hint / kParts) + b / kParts) * tile_bytes;
+        } else {
+          int ba = rot + b - n_hint;
+          if (ba >= nB) ba -= nB;
+          src = atiles + size_t(ba) * tile_bytes;
+        }
+        mbar_arrive_expect_tx_addr(b_full0 + 8 * st, copy_bytes);
+        bulk_g2s_addr(ring0 + st * C::kBBytes, src, copy_bytes, b_full0 + 8 * st, pol_b);
+        CBB_STAMP(7, kk);
+        st += kParts;
+        if (st >= C::kStages) {
+          st -= C::kStages;
+          ph ^= 1u;
+        }
+        b += kParts;
+        while (b >= T) {
+          b -= T;
+          ++it;
         }
       }
     }
@@ -1301,16 +1319,20 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           const int hvt = hg < n_hg ? hg : n_hg - 1;  // dead voxel tiles reuse a valid hint
           const uint8_t* src =
               b < n_hint
-                  ? hint_tiles + (size_t(hvt) * (n_hint / kParts) + b / kParts) * C::kBTileBytes
-                  : atiles + size_t(ba) * C::kBTileBytes;
+                  ? hint_tiles + (size_t(hvt) * (n_hint / kParts) + b / kParts) * tile_bytes
+                  : atiles + size_t(ba) * tile_bytes;
           uint8_t* dst = smem + C::kOffB + st * C::kBBytes;
-          mbar_arrive_expect_tx(b_full + st, C::kBBytes);
+          mbar_arrive_expect_tx(b_full + st, copy_bytes);
           // this CTA's rows [crank * kBNloc, +kBNloc) of every K block
+          if constexpr (SPLIT) {
 #pragma unroll
-          for (int kb = 0; kb < C::kBlk; ++kb)
-            bulk_g2s(dst + kb * C::kBNloc * C::kRowBytes,
-                     src + (kb * BN + crank * C::kBNloc) * C::kRowBytes,
-                     uint32_t(C::kBNloc * C::kRowBytes), b_full + st, pol_b);
+            for (int kb = 0; kb < C::kBlk; ++kb)
+              bulk_g2s(dst + kb * C::kBNloc * C::kRowBytes,
+                       src + (kb * BN + crank * C::kBNloc) * C::kRowBytes,
+                       uint32_t(C::kBNloc * C::kRowBytes), b_full + st, pol_b);
+          } else {
+            bulk_g2s(dst, src + crank * copy_bytes, copy_bytes, b_full + st, pol_b);
+          }
           CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
         }
         __syncwarp();
@@ -1376,17 +1398,17 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq) {
-          // K-major operand: K blocks of 64 elements (128 B rows) follow each other, kBNloc
-          // rows each
-          const uint64_t bdesc = umma_desc_kmajor(
-              b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128, KP < 64 ? KP : 64);
+          // split: K blocks of 64 elements (128 B swizzled rows) follow each other, kBNloc rows
+          // each; fp16: no-swizzle core matrices, K step kq = chunks 2kq, 2kq + 1
+          const uint64_t bdesc =
+              SPLIT ? umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128, 64) +
+                          uint64_t(2 * (kq & 3))
+                    : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
           if (kq < nks) {
             if constexpr (PAIR)
-              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)),
-                             C::kIdesc, kq > 0 ? 1u : 0u);
+              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
             else
-              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc + uint64_t(2 * (kq & 3)),
-                            C::kIdesc, kq > 0 ? 1u : 0u);
+              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
           }
         }
         if constexpr (PAIR) {  // both CTAs' barriers
@@ -1686,6 +1708,11 @@ __global__ void __launch_bounds__(TcDual<KP>::kThreads, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   for (int i = threadIdx.x; i < 2 * 4 * C::kVox; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem + C::kOffPthr)[i] = 0xFFFFFC00u;
+  for (int i = threadIdx.x; i < C::kStages * C::kBBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem + C::kOffB)[i] = make_uint4(0, 0, 0, 0);  // finite tails
+  fence_proxy_async_smem();
+  const int nc = tc_nc(dv.s);
+  const uint32_t tile_bytes = uint32_t(BN * nc * 16);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1703,10 +1730,10 @@ __global__ void __launch_bounds__(TcDual<KP>::kThreads, 1)
         mbar_wait(b_empty + st, ph ^ 1u);
         if (elect_one()) {
           const uint8_t* src =
-              b < n_hint ? hint_tiles + (size_t(pt) * (n_hint / kParts) + b / kParts) * C::kBBytes
-                         : dv.atoms_tc + size_t(ba) * C::kBBytes;
-          mbar_arrive_expect_tx(b_full + st, C::kBBytes);
-          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, C::kBBytes, b_full + st, pol_b);
+              b < n_hint ? hint_tiles + (size_t(pt) * (n_hint / kParts) + b / kParts) * tile_bytes
+                         : dv.atoms_tc + size_t(ba) * tile_bytes;
+          mbar_arrive_expect_tx(b_full + st, tile_bytes);
+          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, tile_bytes, b_full + st, pol_b);
         }
         __syncwarp();
         if (b >= n_hint && ++ba == nB) ba = 0;
@@ -1740,8 +1767,7 @@ __global__ void __launch_bounds__(TcDual<KP>::kThreads, 1)
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq) {
           const uint64_t bdesc =
-              umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * BN * 128, KP < 64 ? KP : 64) +
-              uint64_t(2 * (kq & 3));
+              umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
           if (kq < nks) {
 #pragma unroll
             for (int vv = 0; vv < 2; ++vv)
@@ -2157,8 +2183,9 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
 template <int KP>
 __global__ void __launch_bounds__(128, 1)
     tc_debug_scores_kernel(const uint8_t* __restrict__ zrows, const uint8_t* __restrict__ atiles,
-                           int a_tile, int b_tile, float* __restrict__ out) {
-  constexpr int kTileBytes = kTileRows * KP * 2;
+                           int nc, int a_tile, int b_tile, float* __restrict__ out) {
+  constexpr int kTileBytes = kTileRows * KP * 2;  // SMEM buffer (>= the stored tile, zero tail)
+  const uint32_t tbytes = uint32_t(kTileRows * nc * 16);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kTileBytes);
@@ -2170,6 +2197,9 @@ __global__ void __launch_bounds__(128, 1)
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc(holder, 256);
+  for (int i = threadIdx.x; i < kTileBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -2181,13 +2211,13 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(bar, kTileBytes);
-    bulk_g2s(smem, atiles + size_t(b_tile) * kTileBytes, kTileBytes, bar, policy_evict_first());
+    mbar_arrive_expect_tx(bar, tbytes);
+    bulk_g2s(smem, atiles + size_t(b_tile) * tbytes, tbytes, bar, policy_evict_first());
     mbar_wait(bar, 0);
     tc_fence_after();
-    const uint64_t bd = umma_desc_kmajor(smem_u32(smem), KP);
-    for (int k = 0; k < KP / 16; ++k)
-      tc_mma_f16_ts(tbase, tbase + a_col + k * 8, bd + uint64_t(2 * k),
+    for (int k = 0; k < KP / 16; ++k)  // every K step (those past the data multiply zeros)
+      tc_mma_f16_ts(tbase, tbase + a_col + k * 8,
+                    umma_desc_interleave(smem_u32(smem) + k * 256, 128, nc * 128),
                     idesc_f16_f16(128, 128), k > 0);
     tc_commit(bar + 1);
   }
@@ -2337,7 +2367,7 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   if (2 * s < 64) {  // tensor-core operand tiles (+ sentinel column)
     const int64_t d_pad = int64_t(v.n_btiles + 2) * kTileRows;
     prep_tc_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
-        v.atoms64, d, d_pad, s, v.kpad, const_cast<uint8_t*>(v.atoms_tc),
+        v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc),
         const_cast<float*>(v.bounds));
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -2448,7 +2478,8 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
                                                          const uint8_t* __restrict__ atiles,
                                                          int kp, int split, int bn, int nh,
                                                          uint8_t* __restrict__ out) {
-  const int cpr = kp / 8;  // 16-byte chunks per row
+  // 16-byte chunks per row: split rows kp / 8; fp16 rows tc_nc(s), passed as kp = 8 * nc
+  const int cpr = kp / 8;
   const int64_t per_vt = int64_t(nh) * bn * cpr;
   const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= per_vt * n_vt) return;
@@ -2468,8 +2499,8 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
     src = size_t(j / rows) * rows * kp * 2 + split_elem_offset(int(j % rows), 8 * c, rows);
     dst = (size_t(vt) * nh + hb) * bn * kp * 2 + split_elem_offset(rr, 8 * c, bn);
   } else {
-    src = size_t(j / kTileRows) * kTileRows * kp * 2 + tile_chunk_offset(int(j % kTileRows), c, kp);
-    dst = (size_t(vt) * nh + hb) * bn * kp * 2 + tile_chunk_offset(rr, c, kp);
+    src = atom_chunk_offset(j, c, cpr);
+    dst = (size_t(vt) * nh + hb) * bn * cpr * 16 + atom_chunk_offset(rr, c, cpr);
   }
   *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(atiles + src);
 }
@@ -2519,9 +2550,10 @@ static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const Dic
     const int vox = PAIR ? 2 * C::kVox : C::kVox;
     const int n_g = int((n + vox - 1) / vox);
     const int nh = (vox + C::BN - 1) / C::BN;
-    const int64_t chunks = int64_t(n_g) * nh * C::BN * (KP / 8);
+    const int kw = SPLIT ? KP : 8 * tc_nc(dv.s);  // row width (fp16 elements) as stored
+    const int64_t chunks = int64_t(n_g) * nh * C::BN * (kw / 8);
     hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_g, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, KP, SPLIT ? 1 : 0, C::BN,
+        zs.hint, n, dv.d, n_g, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, kw, SPLIT ? 1 : 0, C::BN,
         nh, w.hint_tiles);
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -2571,9 +2603,9 @@ static int launch_tc_dual(const ProjWs& w, int64_t n, const ZSource& zs, const D
     const int vox = 2 * C::kVox;
     const int n_g = int((n + vox - 1) / vox);
     const int nh = (vox + C::BN - 1) / C::BN;
-    const int64_t chunks = int64_t(n_g) * nh * C::BN * (KP / 8);
+    const int64_t chunks = int64_t(n_g) * nh * C::BN * tc_nc(dv.s);
     hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_g, vox, dv.atoms_tc, KP, 0, C::BN, nh, w.hint_tiles);
+        zs.hint, n, dv.d, n_g, vox, dv.atoms_tc, 8 * tc_nc(dv.s), 0, C::BN, nh, w.hint_tiles);
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     n_hint = kParts * nh;
@@ -2836,22 +2868,23 @@ int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStre
   return kOk;
 }
 
-int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int a_tile, int b_tile,
-                    float* out, cudaStream_t st) {
+int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int s, int a_tile,
+                    int b_tile, float* out, cudaStream_t st) {
   const int tile_bytes = kTileRows * kpad * 2;
   const int smem = tile_bytes + 64 + 1024;
+  const int nc = tc_nc(s);
   if (kpad == 32) {
     CBB_CUDA_TRY(cudaFuncSetAttribute(tc_debug_scores_kernel<32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     tc_debug_scores_kernel<32><<<1, 128, smem, st>>>(static_cast<const uint8_t*>(ztiles),
-                                                      static_cast<const uint8_t*>(atiles), a_tile,
-                                                      b_tile, out);
+                                                      static_cast<const uint8_t*>(atiles), nc,
+                                                      a_tile, b_tile, out);
   } else {
     CBB_CUDA_TRY(cudaFuncSetAttribute(tc_debug_scores_kernel<64>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     tc_debug_scores_kernel<64><<<1, 128, smem, st>>>(static_cast<const uint8_t*>(ztiles),
-                                                      static_cast<const uint8_t*>(atiles), a_tile,
-                                                      b_tile, out);
+                                                      static_cast<const uint8_t*>(atiles), nc,
+                                                      a_tile, b_tile, out);
   }
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;

@@ -29,7 +29,8 @@ struct DictView {
   int32_t n_btiles;    // ceil(d / 128)
   const double2* atoms64;      // d x s   complex128 (exact rescoring)
   const float* atoms32;        // d x 2*s_pad planar fp32 [re.., im..]
-  const uint8_t* atoms_tc;     // n_btiles x 128 rows x kpad fp16 (atoms * scale), swizzled
+  const uint8_t* atoms_tc;     // fp16 rows of atoms * scale: tc_nc(s) 16-byte chunks per row,
+                               // no-swizzle core-matrix layout (atom_chunk_offset)
   const float* bounds;         // kB* slots below
   const uint8_t* atoms_tc2;    // split-operand tiles (s <= kSplitMaxS, else null): swizzled
                                // rows of split_kp(s) fp16 [d_hi | d_hi | d_lo | sentinel]
