@@ -1365,14 +1365,20 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     const int nks = SPLIT ? split_ksteps(dv.s) : mma_ksteps(dv.s);
     const uint32_t b_base = smem_u32(smem + C::kOffB);
     static_assert(C::kAcc == kParts, "issuer i always fills accumulator stage i");
+#ifdef CBB_NISS
+    constexpr int kIss = CBB_NISS;  // development: issuer warps (kParts % kIss == 0)
+#else
+    constexpr int kIss = kParts;
+#endif
+    static_assert(kParts % kIss == 0, "issuers share the stages evenly");
     int sacc = me;  // accumulator stage kk % kAcc
-    uint32_t aph = 1;  // acc_free parity: the first use of each stage passes at once
+    uint32_t aphm = (1u << C::kAcc) - 1u;  // acc_free parity per stage: first use passes at once
     int tb = me;    // completion barrier kk % kTBars
     int itk = -1;
     uint32_t vt_end = 0;  // first tile index of the next voxel tile
     int st = me;
     uint32_t ph = 0;
-    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
+    for (uint32_t kk = uint32_t(me); me < kIss && kk < total; kk += kIss) {
       if (kk >= vt_end) {  // first tile of this issuer in a new voxel tile: wait for its A
         ++itk;
         vt_end += uint32_t(T);
@@ -1381,54 +1387,61 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         else
           mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
       }
+      // operands of this tile's MMAs, computed before the waits (off the release -> MMA path)
+      const uint32_t a_tm = tbase + uint32_t(C::kAColOff + ((itk & 1) * C::kACols));
+      const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
+      uint64_t bdesc[KP / 16];
+#pragma unroll
+      for (int kq = 0; kq < KP / 16; ++kq)
+        // split: K blocks of 64 elements (128 B swizzled rows) follow each other, kBNloc rows
+        // each; fp16: no-swizzle core matrices, K step kq = chunks 2kq, 2kq + 1
+        bdesc[kq] = SPLIT ? umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128,
+                                             64) +
+                                uint64_t(2 * (kq & 3))
+                          : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
+      // the atom tile usually landed long before the accumulator stage is released: test it
+      // first, so the release -> MMA hop is a single barrier wait
       if constexpr (PAIR) {
-        mbar_wait_cluster(acc_free + sacc, aph);
-        if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait_cluster(b_full + st, ph);
+        mbar_wait_cluster(acc_free + sacc, (aphm >> sacc) & 1u);
       } else {
-        mbar_wait(acc_free + sacc, aph);
-        if (lane == 0) CBB_STAMP(4, kk);
         mbar_wait(b_full + st, ph);
+        mbar_wait(acc_free + sacc, (aphm >> sacc) & 1u);
       }
-      aph ^= 1u;
+      if (lane == 0) CBB_STAMP(4, kk);
+      aphm ^= 1u << sacc;
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
       if (elect_one()) {
-        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kACols);
-        const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq) {
-          // split: K blocks of 64 elements (128 B swizzled rows) follow each other, kBNloc rows
-          // each; fp16: no-swizzle core matrices, K step kq = chunks 2kq, 2kq + 1
-          const uint64_t bdesc =
-              SPLIT ? umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128, 64) +
-                          uint64_t(2 * (kq & 3))
-                    : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
           if (kq < nks) {
             if constexpr (PAIR)
-              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
+              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], C::kIdesc, kq > 0 ? 1u : 0u);
             else
-              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
+              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], C::kIdesc, kq > 0 ? 1u : 0u);
           }
         }
+        CBB_STAMP(1, kk);
         if constexpr (PAIR) {  // both CTAs' barriers
           tc_commit2_mc(b_empty + st, 3);
           tc_commit2_mc(t_full + tb, 3);
-          if (kk + kParts >= vt_end) tc_commit2_mc(a_empty + (itk & 1), 3);
+          if (kk + kIss >= vt_end)
+            for (int r = 0; r < kParts / kIss; ++r) tc_commit2_mc(a_empty + (itk & 1), 3);
         } else {
           tc_commit(b_empty + st);
           tc_commit(t_full + tb);
           // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
-          if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
+          if (kk + kIss >= vt_end)
+            for (int r = 0; r < kParts / kIss; ++r) tc_commit(a_empty + (itk & 1));
         }
-        CBB_STAMP(1, kk);
       }
       __syncwarp();
-      sacc += kParts;
+      sacc += kIss;
       if (sacc >= C::kAcc) sacc -= C::kAcc;
-      tb += kParts;
+      tb += kIss;
       if (tb >= C::kTBars) tb -= C::kTBars;
-      st += kParts;
+      st += kIss;
       if (st >= C::kStages) {
         st -= C::kStages;
         ph ^= 1u;
