@@ -1406,7 +1406,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         mbar_wait_cluster(acc_free + sacc, (aphm >> sacc) & 1u);
       } else {
         mbar_wait(b_full + st, ph);
+#ifdef CBB_SPIN_ISS
+        mbar_wait_spin(acc_free + sacc, (aphm >> sacc) & 1u);
+#else
         mbar_wait(acc_free + sacc, (aphm >> sacc) & 1u);
+#endif
       }
       if (lane == 0) CBB_STAMP(4, kk);
       aphm ^= 1u << sacc;
@@ -1525,7 +1529,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         uint32_t r[16 * C::kChunks];
         auto consume = [&]() {
           if (q == 0 && lane == 0) CBB_STAMP(5, kk);
+#ifdef CBB_SPIN_EPI
+          mbar_wait_spin(t_full + part, ph);
+#else
           mbar_wait(t_full + part, ph);
+#endif
           tc_fence_after();
           if (q == 0 && lane == 0) CBB_STAMP(2, kk);
           __syncwarp();
