@@ -448,7 +448,10 @@ def run_ours(args, rank, world, local_rank):
                                     f"(Re<z,d> only); {flops:.3e} flops per launch",
                      "kernel_ms": kmean,
                      "padded_k_ceiling": 20 / 32,
-                     "traffic": (traffic or {}).get("dram_bytes_per_launch")},
+                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     # ncu --set full capture of the same kernel (profiles/roofline_traffic.json)
+                     "ncu_tensor_pipe_active_pct": (traffic or {}).get("tensor_pipe_active_pct"),
+                     "ncu_report": (traffic or {}).get("report")},
         "e2e": {"value": macs_per_step() * world * e2e_steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": N_VOX * S * 16,
                 "d2h_bytes_per_step": N_VOX * (8 + 8 + S * 16),

@@ -80,6 +80,9 @@ def full(rep, out, traffic_json, cmd):
          "dram_bytes_read": num("dram__bytes_read.sum"),
          "dram_bytes_write": num("dram__bytes_write.sum")}
     t["dram_bytes_per_launch"] = t["dram_bytes_read"] + t["dram_bytes_write"]
+    t["tensor_pipe_active_pct"] = num(
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
+    t["issue_active_pct"] = num("smsp__issue_active.avg.pct_of_peak_sustained_active")
     with open(traffic_json, "w") as fh:
         json.dump(t, fh, indent=1)
     print(t)
