@@ -123,7 +123,6 @@ def project_cone_exact(Z, dictionary, *, algo: str = "auto") -> ConeProjection:
 
 
 _PIPELINE_MIN = 1 << 16
-_PIPELINE_CHUNK = 1 << 17
 _streams: dict = {}
 
 
@@ -132,6 +131,29 @@ def _pipe_streams(dev):
     if key not in _streams:
         _streams[key] = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
     return _streams[key]
+
+
+def _pipeline_bounds(n: int, dev):
+    """Chunk boundaries of the pipelined call, in units of one voxel tile per SM (so every chunk
+    fills the persistent screen's grid evenly): 1, 2, 4 units first and 4, 2, 1 last, so the
+    first upload and the last download that nothing overlaps stay short; 8 units in between."""
+    unit = 128 * torch.cuda.get_device_properties(dev).multi_processor_count
+    total = -(-n // unit)
+    if total <= 16:
+        sizes = [1] * total if total <= 4 else [max(1, total // 4)] * 4
+    else:
+        mid = total - 14
+        sizes = [1, 2, 4] + [8] * (mid // 8) + ([mid % 8] if mid % 8 else []) + [4, 2, 1]
+    bounds, lo = [], 0
+    for k in sizes:
+        if lo >= n:
+            break
+        hi = min(n, lo + k * unit)
+        bounds.append((lo, hi))
+        lo = hi
+    if lo < n:
+        bounds.append((lo, n))
+    return bounds
 
 
 def _project_pipelined(zh: torch.Tensor, dd: DeviceDictionary, algo: str, dev):
@@ -149,9 +171,7 @@ def _project_pipelined(zh: torch.Tensor, dd: DeviceDictionary, algo: str, dev):
     hidx = torch.empty(n, dtype=torch.int64, pin_memory=True)
     hgam = torch.empty(n, dtype=torch.float64, pin_memory=True)
     hproj = torch.empty((n, s), dtype=torch.complex128, pin_memory=True)
-    chunk = _PIPELINE_CHUNK
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
+    for lo, hi in _pipeline_bounds(n, dev):
         e_in = torch.cuda.Event()
         with torch.cuda.stream(s_in):
             zt[lo:hi].copy_(zh[lo:hi], non_blocking=True)
