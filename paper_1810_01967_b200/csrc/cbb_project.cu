@@ -916,6 +916,14 @@ __device__ long long g_trace_vt[256 * 4];  // per voxel tile of CTA 0: loop star
 // b_empty -> producer, a_full -> issuers, a_empty -> part 0.
 // Atom tiles are visited in a per-CTA rotated order to spread L2 traffic.
 constexpr int kParts = 3;
+// Small projections split the dictionary into up to kMaxSplit contiguous tile ranges (work units
+// = voxel tile x range) so that all SMs get an even share; each range reports its own kParts
+// candidate lists.  Only projections of at most kSplitMaxN voxels reserve the extra lists.
+constexpr int kMaxSplit = 4;
+constexpr int64_t kSplitMaxN = int64_t(1) << 17;
+// 128-row storage tiles after the last atom: sentinel rows that complete the last BN-row tile
+// of every range (up to kMaxSplit - 1 extra BN-row tiles)
+constexpr int kPadTiles = 8;
 
 // SPLIT: hi/lo fp16 operands with fp32 accumulators: KP = 64 -> 128-atom tiles (N = 128 MMAs;
 // measured faster than 64-atom tiles with six stages), screened in two 64-register halves;
@@ -1178,13 +1186,17 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
   tc_wait_st();
 }
 
-template <int KP, bool SPLIT, bool PAIR, bool HI32>
+// RANGES: the dictionary is split into nsplit_arg atom ranges (small projections); without it the
+// range arithmetic folds away (nsplit = 1)
+template <int KP, bool SPLIT, bool PAIR, bool HI32, bool RANGES = false>
 __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
                  DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta,
-                 const uint8_t* __restrict__ hint_tiles, int n_hint) {
+                 const uint8_t* __restrict__ hint_tiles, int n_hint, int nsplit_arg) {
   using C = TcCfg<KP, SPLIT, PAIR, HI32>;
+  static_assert(!(PAIR && RANGES), "CTA pairs screen the whole dictionary");
+  const int nsplit = RANGES ? nsplit_arg : 1;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024_smem(smem_raw);
@@ -1200,6 +1212,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t d = dv.d;
   const int nB = int((d + BN - 1) / BN);
+  // work unit u (the CTA's units are u = blockIdx.x + it * gridDim.x): voxel tile u / nsplit,
+  // atom tiles [h nBh, (h + 1) nBh) with h = u % nsplit (the last range runs into sentinel
+  // tiles when nsplit does not divide nB; PAIR: nsplit = 1)
+  const int nBh = (nB + nsplit - 1) / nsplit;
   // atom tile bytes in global memory and this CTA's copy of it: the fp16 screens store
   // tc_nc(s) chunks per row (no-swizzle layout), the split screen full swizzled K rows
   const int nc = tc_nc(dv.s);
@@ -1212,12 +1228,12 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   const int crank = PAIR ? int(cluster_ctarank()) : 0;
   const bool leader = crank == 0;
   const int csz = PAIR ? 2 : 1;
-  const int rot = int((int64_t(blockIdx.x / csz) * nB) / (gridDim.x / csz));
+  const int rot = int((int64_t(blockIdx.x / csz) * nBh) / (gridDim.x / csz));
   const int my_vts = PAIR ? (n_vt + int(gridDim.x) - 1) / int(gridDim.x)
-                          : (n_vt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+                          : (n_vt * nsplit - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
   // per voxel tile: n_hint warm-start tiles (the voxel tile's own hint atoms, each hint tile
   // repeated for the kParts parts: tile qt -> hint tile qt / kParts), then the nB atom tiles
-  const int T = nB + n_hint;
+  const int T = nBh + n_hint;
   const uint32_t total = uint32_t(my_vts) * uint32_t(T);  // this CTA's tiles
 
   if (threadIdx.x == 0) {
@@ -1271,21 +1287,31 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       const uint32_t ring0 = smem_u32(smem + C::kOffB);
       int st = lane;
       uint32_t ph = 0;
-      int it = 0, b = lane;  // voxel-tile iteration and tile index inside it
+      int it = 0, b = lane;  // work-unit iteration and tile index inside it
       while (b >= T) {
         b -= T;
         ++it;
       }
+      // per work unit: its atom range's first tile and its voxel tile's hint tiles
+      const uint8_t* abase = nullptr;
+      const uint8_t* hbase = nullptr;
+      int it_set = -1;
       for (uint32_t kk = uint32_t(lane); kk < total; kk += kParts) {
+        if (it != it_set) {
+          const int u = int(blockIdx.x) + it * int(gridDim.x);
+          const int vt = u / nsplit;
+          abase = atiles + size_t(u - vt * nsplit) * nBh * tile_bytes;
+          hbase = hint_tiles + size_t(vt) * (n_hint / kParts) * tile_bytes;
+          it_set = it;
+        }
         mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
         const uint8_t* src;
         if (b < n_hint) {
-          const int vt = int(blockIdx.x) + it * int(gridDim.x);
-          src = hint_tiles + (size_t(vt) * (n_hint / kParts) + b / kParts) * tile_bytes;
+          src = hbase + size_t(b / kParts) * tile_bytes;
         } else {
           int ba = rot + b - n_hint;
-          if (ba >= nB) ba -= nB;
-          src = atiles + size_t(ba) * tile_bytes;
+          if (ba >= nBh) ba -= nBh;
+          src = abase + size_t(ba) * tile_bytes;
         }
         mbar_arrive_expect_tx_addr(b_full0 + 8 * st, copy_bytes);
         bulk_g2s_addr(ring0 + st * C::kBBytes, src, copy_bytes, b_full0 + 8 * st, pol_b);
@@ -1476,7 +1502,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
 
     // ---- A for the first voxel tile
     if (part == 0 && my_vts > 0) {
-      const int64_t v0 = int64_t(blockIdx.x) * C::kVox + row;
+      const int64_t v0 = int64_t(int(blockIdx.x) / nsplit) * C::kVox + row;
       stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
       tc_fence_before();
       __syncwarp();
@@ -1488,7 +1514,9 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     int tb = part;                 // its completion barrier kk % kTBars, phase (kk / kTBars) & 1
     uint32_t ph = 0;
     for (int it = 0; it < my_vts; ++it) {
-      const int vt = int(blockIdx.x) + it * int(gridDim.x);
+      const int u = int(blockIdx.x) + it * int(gridDim.x);
+      const int vt = u / nsplit, hr = u - vt * nsplit;  // voxel tile, atom range
+      const int opart = hr * kParts + part;  // output lists of (atom range, part)
       const int64_t v = int64_t(vt) * C::kVox + row;
       const bool live = v < n;
       // ---- stage the NEXT voxel tile's rows into the other A buffer (one tile ahead)
@@ -1496,7 +1524,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         const int nbuf = (it + 1) & 1;
         mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
-        const int64_t vn = int64_t(vt + int(gridDim.x)) * C::kVox + row;
+        const int64_t vn = int64_t((u + int(gridDim.x)) / nsplit) * C::kVox + row;
         stage_voxel_row<KP>(zrows, vn, vn < n, a_lane + uint32_t(nbuf * C::kACols));
         tc_fence_before();
         __syncwarp();
@@ -1506,7 +1534,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
       HCandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0,
-                   cand + int64_t(part) * kGCap * n_pad + (live ? v : 0), n_pad, 0, false};
+                   cand + int64_t(opart) * kGCap * n_pad + (live ? v : 0), n_pad, 0, false};
       // running max seeded with the warm-start lower bound (-inf without a hint)
       const float init = live ? fmaxf(init_tc[v], -65504.f) : -INFINITY;
       __half runmax = active ? __float2half_rd(init) : __ushort_as_half(0xFC00);
@@ -1561,8 +1589,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           thr = __float2half_rd(__half2float(runmax) - win);
           *my_pub = tag | __half_as_ushort(thr);
         }
-        int ba = rot + int(kk - khint);  // atom tile (rot + qt) % nB, qt = kk - khint
-        if (ba >= nB) ba -= nB;
+        // atom tile hr nBh + (rot + qt) % nBh, qt = kk - khint (absolute index, wraps at bend)
+        int ba = rot + int(kk - khint);
+        if (ba >= nBh) ba -= nBh;
+        ba += hr * nBh;
+        const int bend = hr * nBh + nBh;
         for (; kk < kend; kk += kParts) {
           const uint4 w = lds_v4_volatile(pthr_row);
           consume();
@@ -1576,15 +1607,16 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
 #endif
           if (q == 0 && lane == 0) CBB_STAMP(6, kk);
           ba += kParts;
-          if (ba >= nB) ba -= nB;
+          if (ba >= bend) ba -= nBh;
         }
       } else {
         // split / HI32 screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles
         // are screened in halves and released after the last half is loaded
         for (; kk < kend; kk += kParts) {
           const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
-          int ba = rot + qt;                       // atom tile (rot + qt) % nB
-          if (ba >= nB) ba -= nB;
+          int ba = rot + qt;                       // range tile (rot + qt) % nBh
+          if (ba >= nBh) ba -= nBh;
+          ba += hr * nBh;
           mbar_wait(t_full + tb, ph);
           tc_fence_after();
           constexpr int kRegChunks = C::kChunks < 2 ? C::kChunks : 2;
@@ -1626,7 +1658,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       if (live) {
         const float rm = C::kF32 ? runmax_f : __half2float(runmax);
         const int total = (win >= 0.f) ? cl.finish(rm - win) : 0;
-        meta[int64_t(part) * n_pad + v] = make_int2(total, __float_as_int(rm));
+        meta[int64_t(opart) * n_pad + v] = make_int2(total, __float_as_int(rm));
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(2, it);
     }
@@ -1970,11 +2002,11 @@ __device__ __forceinline__ void rescore_entry(int2 en, const double* zr, const d
 
 // One THREAD per voxel: zero voxels, overflow routing and voxels with <= kFastEntries chunk
 // entries (every incoherent dictionary); heavier voxels go to the warp kernel's list.
-template <int S>
+template <int S, int NP = kParts>
 __global__ void __launch_bounds__(256) rescore_fast_kernel(
     ZSource zs, DictView dv, int64_t n, int64_t n_pad, const float* __restrict__ win_tc,
     const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
-    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list, int fast_entries) {
+    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list, int fast_entries, int nparts) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const float win = win_tc[v];
@@ -1982,13 +2014,18 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     write_winner(out, dv, v, 0, 0.0);
     return;
   }
-  int cnt[kParts];
+  // nparts = kParts x the screen's atom ranges
+  // NP (compile time) >= nparts part lists
+  int cnt[NP];
   float gmax = -INFINITY;
   bool ovf = !(win >= 0.f);
+  int entries = 0;
 #pragma unroll
-  for (int p = 0; p < kParts; ++p) {
+  for (int p = 0; p < NP; ++p) {
+    if (p >= nparts) break;
     const int2 m = meta[int64_t(p) * n_pad + v];
     cnt[p] = m.x;
+    entries += m.x;
     ovf |= m.x < 0;
     gmax = fmaxf(gmax, __int_as_float(m.y));
   }
@@ -1997,12 +2034,12 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     return;
   }
   const float thr = gmax - win;
-  bool heavy = fast_entries == 0 || cnt[0] + cnt[1] + cnt[2] > kFastRead;
+  bool heavy = fast_entries == 0 || entries > kFastRead;
   if (!heavy) {  // entries inside the final (cross-part) window
     int live = 0;
 #pragma unroll
-    for (int p = 0; p < kParts; ++p)
-      for (int c = 0; c < cnt[p]; ++c)
+    for (int p = 0; p < NP; ++p)
+      for (int c = 0; p < nparts && c < cnt[p]; ++c)
         live += __int_as_float(cand[(int64_t(p) * kGCap + c) * n_pad + v].y) >= thr;
     heavy = live > fast_entries;
   }
@@ -2020,8 +2057,8 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
   int64_t best = INT64_MAX;
   double bs = -INFINITY;
 #pragma unroll
-  for (int p = 0; p < kParts; ++p)
-    for (int c = 0; c < cnt[p]; ++c) {
+  for (int p = 0; p < NP; ++p)
+    for (int c = 0; p < nparts && c < cnt[p]; ++c) {
       const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
       if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zr, zi, s, dv, best, bs);
     }
@@ -2033,12 +2070,26 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
 }
 
 
-template <int S>
+// entry e of a voxel's concatenated part lists -> (part p, index c in it); unused parts have
+// count 0 (static register indexing, no local memory)
+template <int NP>
+__device__ __forceinline__ void entry_part(int e, const int (&cnt)[NP], int& p, int& c) {
+  p = 0;
+  c = e;
+#pragma unroll
+  for (int q = 0; q + 1 < NP; ++q)
+    if (p == q && c >= cnt[q]) {
+      c -= cnt[q];
+      p = q + 1;
+    }
+}
+
+template <int S, int NP = kParts>
 __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     ZSource zs, DictView dv, int64_t n_pad, const float* __restrict__ win_tc,
     const float* __restrict__ win32, const int2* __restrict__ cand,
     const int2* __restrict__ meta, ProjOut out, int* ovf_count, int64_t* ovf_list,
-    const int* heavy_count, const int64_t* heavy_list) {
+    const int* heavy_count, const int64_t* heavy_list, int nparts) {
   // shared per warp: z (2s doubles), z (2s floats), the atom list, the lanes' fp32 survivors
   extern __shared__ double zsh_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2059,13 +2110,17 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       if (lane == 0) write_winner(out, dv, v, 0, 0.0);
       continue;
     }
-    int cnt[kParts];
+    int cnt[NP];
     float gmax = -INFINITY;
     bool ovf = !(win >= 0.f);
+    int total = 0;
 #pragma unroll
-    for (int p = 0; p < kParts; ++p) {
+    for (int p = 0; p < NP; ++p) {
+      cnt[p] = 0;
+      if (p >= nparts) continue;
       const int2 m = meta[int64_t(p) * n_pad + v];  // same address in every lane: broadcast
       cnt[p] = m.x;
+      total += m.x;
       ovf |= m.x < 0;
       gmax = fmaxf(gmax, __int_as_float(m.y));
     }
@@ -2090,7 +2145,6 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     __syncwarp();
     const float thr = gmax - win;
     const float w32 = win32[v];
-    const int total = cnt[0] + cnt[1] + cnt[2];
     int64_t best = INT64_MAX;
     double bs = -INFINITY;
     // fp32 pre-filter (certified window w32): every lane keeps the atoms within w32 of its own
@@ -2106,8 +2160,8 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       int64_t j0 = 0;
       uint32_t mask = 0;
       if (e < total) {
-        const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
-        const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
+        int p, c;
+        entry_part(e, cnt, p, c);
         const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
         if (__int_as_float(en.y) >= thr) {
           j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
@@ -2170,8 +2224,8 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       for (int e0 = 0; e0 < total; e0 += 32) {
         const int e = e0 + lane;
         if (e < total) {
-          const int p = e < cnt[0] ? 0 : (e < cnt[0] + cnt[1] ? 1 : 2);
-          const int c = e - (p == 0 ? 0 : (p == 1 ? cnt[0] : cnt[0] + cnt[1]));
+          int p, c;
+          entry_part(e, cnt, p, c);
           const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
           if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zsh, zsh + s, s, dv, best, bs);
         }
@@ -2348,9 +2402,9 @@ size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc,
   size_t b = take(size_t(d) * 2 * sp * 4);
   // + two extra 128-row sentinel tiles: the screening reads BN-row (BN <= 256) windows that
   // may run past the last 128-row tile
-  size_t c = take(size_t(nbt + 2) * kTileRows * kp * 2);
+  size_t c = take(size_t(nbt + kPadTiles) * kTileRows * kp * 2);
   size_t e = take(kBCount * sizeof(float));
-  size_t f = take(s <= kSplitMaxS ? size_t(nbt + 2) * kTileRows * split_kp(s) * 2 : 0);
+  size_t f = take(s <= kSplitMaxS ? size_t(nbt + kPadTiles) * kTileRows * split_kp(s) * 2 : 0);
   if (offtc2) *offtc2 = f;
   if (off64) *off64 = a;
   if (off32) *off32 = b;
@@ -2386,7 +2440,7 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   CBB_CUDA_TRY(cudaGetLastError());
   count_launches(1);
   if (2 * s < 64) {  // tensor-core operand tiles (+ sentinel column)
-    const int64_t d_pad = int64_t(v.n_btiles + 2) * kTileRows;
+    const int64_t d_pad = int64_t(v.n_btiles + kPadTiles) * kTileRows;
     prep_tc_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
         v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc),
         const_cast<float*>(v.bounds));
@@ -2400,7 +2454,7 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
     count_launches(1);
   }
   if (v.atoms_tc2) {  // split-operand tiles (after prep_tc_kernel: it publishes scale_d)
-    const int64_t d_pad = int64_t(v.n_btiles + 2) * kTileRows;
+    const int64_t d_pad = int64_t(v.n_btiles + kPadTiles) * kTileRows;
     prep_tc2_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
         v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc2), const_cast<float*>(v.bounds));
     CBB_CUDA_TRY(cudaGetLastError());
@@ -2453,8 +2507,9 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   ProjWs w{};
   w.n_pad = n_vt * kVoxPad;
   w.ztiles = take(size_t(n_vt) * kVoxPad * kp * 2);  // first: cbb_debug_tc_scores reads it
-  w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * kGCap * sizeof(int2)));
-  w.meta = reinterpret_cast<int2*>(take(size_t(w.n_pad) * kParts * sizeof(int2)));
+  const int parts = kParts * (n <= kSplitMaxN ? kMaxSplit : 1);  // see launch_tc
+  w.cand = reinterpret_cast<int2*>(take(size_t(w.n_pad) * parts * kGCap * sizeof(int2)));
+  w.meta = reinterpret_cast<int2*>(take(size_t(w.n_pad) * parts * sizeof(int2)));
   w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.init_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
@@ -2562,9 +2617,9 @@ static int max_coresident_pairs(K kernel, int threads, int smem) {
   return nc;
 }
 
-template <int KP, bool SPLIT, bool PAIR, bool HI32>
+template <int KP, bool SPLIT, bool PAIR, bool HI32, bool RANGES = false>
 static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                        int grid, int n_vt, cudaStream_t st) {
+                        int grid, int n_vt, cudaStream_t st, int nsplit = 1) {
   using C = TcCfg<KP, SPLIT, PAIR, HI32>;
   int n_hint = 0;
   if (zs.hint) {  // IPG warm start: the voxel tiles' (pairs') own hint atoms screened first
@@ -2592,9 +2647,10 @@ static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const Dic
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 1 : 0;
-  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR, HI32>, w.ztiles, n, n_vt,
+  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR, HI32, RANGES>, w.ztiles, n,
+                                  n_vt,
                                   (const float*)w.win_tc, (const float*)w.init_tc, dv, w.n_pad,
-                                  w.cand, w.meta, (const uint8_t*)w.hint_tiles, n_hint));
+                                  w.cand, w.meta, (const uint8_t*)w.hint_tiles, n_hint, nsplit));
   return kOk;
 }
 
@@ -2639,13 +2695,16 @@ static int launch_tc_dual(const ProjWs& w, int64_t n, const ZSource& zs, const D
 
 template <int KP, bool SPLIT = false, bool HI32 = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                     const ProjOut& out, int max_ctas, cudaStream_t st) {
+                     const ProjOut& out, int max_ctas, cudaStream_t st, int* nsplit_out) {
+  *nsplit_out = 1;
   using C1 = TcCfg<KP, SPLIT, false, HI32>;
   using C2 = TcCfg<KP, SPLIT, true, HI32>;
   static bool attr_set = false;
   static int pairs = 0;
   if (!attr_set) {
     CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false, HI32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
+    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false, HI32, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
     CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, true, HI32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmem));
@@ -2659,6 +2718,28 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
     // dual-voxel-tile screen when every CTA gets at least one voxel-tile pair
     const int n_pt = (n_vt + 1) / 2;
     if (tc_dual_enabled() && n_pt >= grid) return launch_tc_dual<KP>(w, n, zs, dv, grid, n_vt, st);
+  }
+  // atom ranges: small projections (at most kSplitMaxN voxels) split the dictionary so the
+  // work units (voxel tile x range) cover the SMs evenly: the smallest nsplit minimising
+  // ceil(n_vt nsplit / grid) / nsplit, every range keeping >= 2 tiles per part
+  if (n <= kSplitMaxN) {
+    const int nB = int((dv.d + C1::BN - 1) / C1::BN);
+    int best = 1;
+    double best_t = double((n_vt + grid - 1) / grid);
+    for (int ns = 2; ns <= kMaxSplit; ++ns) {
+      if ((nB + ns - 1) / ns < 2 * kParts) break;
+      const double t = double((int64_t(n_vt) * ns + grid - 1) / grid) / ns;
+      if (t < best_t * 0.97) {
+        best = ns;
+        best_t = t;
+      }
+    }
+    if (best > 1) {
+      *nsplit_out = best;
+      const int units = n_vt * best;
+      return launch_tc_as<KP, SPLIT, false, HI32, true>(w, n, zs, dv, units < grid ? units : grid,
+                                                        n_vt, st, best);
+    }
   }
   if (grid > n_vt) grid = n_vt;
   // CTA pairs halve the atom stream; used when every pair is co-resident (persistent kernel),
@@ -2762,28 +2843,35 @@ static int launch_exhaustive_list(int64_t n, const ZSource& zs, const DictView& 
   return kOk;
 }
 
-template <int S>
-static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
-                          const ProjOut& o, cudaStream_t st) {
+template <int S, int NP>
+static int launch_rescore_np(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
+                          const ProjOut& o, cudaStream_t st, int nparts) {
   // small projections: too few threads for the thread-per-voxel path to hide L2 latency, every
   // voxel goes to the warp kernel
   const int fast = n >= int64_t(num_sms()) * 256 ? kFastEntries : 0;
-  rescore_fast_kernel<S><<<int((n + 255) / 256), 256, 0, st>>>(
+  rescore_fast_kernel<S, NP><<<int((n + 255) / 256), 256, 0, st>>>(
       zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
-      w.heavy_list, fast);
+      w.heavy_list, fast, nparts);
   CBB_CUDA_TRY(cudaGetLastError());
   const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) +
                                                2 * dv.s_pad * sizeof(float) +
                                                kWarpAtoms * sizeof(int) +
                                                32 * kLaneSurv * sizeof(int2));
   if (shm > 48 * 1024)
-    CBB_CUDA_TRY(cudaFuncSetAttribute(rescore_warp_kernel<S>,
+    CBB_CUDA_TRY(cudaFuncSetAttribute(rescore_warp_kernel<S, NP>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
-  rescore_warp_kernel<S><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
+  rescore_warp_kernel<S, NP><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
       zr, dv, w.n_pad, w.win_tc, w.win32, w.cand, w.meta, o, w.ovf_count, w.ovf_list,
-      w.heavy_count, w.heavy_list);
+      w.heavy_count, w.heavy_list, nparts);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
+}
+
+template <int S>
+static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
+                          const ProjOut& o, cudaStream_t st, int nparts) {
+  return nparts == kParts ? launch_rescore_np<S, kParts>(w, n, zr, dv, o, st, nparts)
+                          : launch_rescore_np<S, kParts * kMaxSplit>(w, n, zr, dv, o, st, nparts);
 }
 
 int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStream_t st) {
@@ -2831,17 +2919,19 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     timing_mark(0, st);
-    int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, o, max_ctas, st)
-                                           : launch_tc<128, true>(w, n, zr, dv, o, max_ctas, st))
-             : hi32 ? (dv.kpad == 32 ? launch_tc<32, false, true>(w, n, zr, dv, o, max_ctas, st)
-                                     : launch_tc<64, false, true>(w, n, zr, dv, o, max_ctas, st))
-             : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st)
-                                            : launch_tc<64>(w, n, zr, dv, o, max_ctas, st))
+    int nsplit = 1;  // atom ranges of the screen (candidate lists: kParts per range)
+    int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, o, max_ctas, st, &nsplit)
+                                           : launch_tc<128, true>(w, n, zr, dv, o, max_ctas, st, &nsplit))
+             : hi32 ? (dv.kpad == 32 ? launch_tc<32, false, true>(w, n, zr, dv, o, max_ctas, st, &nsplit)
+                                     : launch_tc<64, false, true>(w, n, zr, dv, o, max_ctas, st, &nsplit))
+             : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st, &nsplit)
+                                            : launch_tc<64>(w, n, zr, dv, o, max_ctas, st, &nsplit))
                            : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
     timing_mark(1, st);
     if (algo == 1) {
-      CBB_DISPATCH_S(dv.s_pad, rc = launch_rescore<S_>(w, n, zr, dv, o, st); break);
+      CBB_DISPATCH_S(dv.s_pad, rc = launch_rescore<S_>(w, n, zr, dv, o, st, kParts * nsplit);
+                     break);
       if (rc) return rc;
       count_launches(2);
     }
