@@ -48,6 +48,19 @@ __device__ __forceinline__ double block_sum_256(double v, double* sh) {
   return r;
 }
 
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(256) finish_sum(const double* __restrict__ partial, int np,
                                                   double* __restrict__ out) {
   __shared__ double sh[256];
@@ -197,6 +210,66 @@ __global__ void __launch_bounds__(256) gather_s_kernel(const float2* __restrict_
   }
   if (partial) {
     double r = block_sum_256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+  }
+}
+
+// Location-major form of gather_s_kernel (same products, same FMA order, so the same y values):
+// one thread per k-space location w reads its channel vector KT[(ci*n + w)*s + 0..s) once and
+// emits every pattern sample of w (CSR, ascending e = t*m + i).  A location is sampled by
+// L*m/n frames on average (cfg2: 62, cfg4: 31), so the channel reads, which sample-major order
+// repeats for every sample (cfg4: 80 B of a 335 MB array per sample, from HBM), fall by that
+// factor; the 8-byte output writes scatter instead.  The norm / residual partial sums run over
+// a fixed location partition (deterministic).
+constexpr int kLocThreads = 512;  // 2 blocks x 512 threads per SM: all kRedBlocks resident
+template <int S>
+__global__ void __launch_bounds__(kLocThreads) gather_loc_kernel(
+    const float2* __restrict__ KT, const int* __restrict__ csr_off,
+    const int64_t* __restrict__ csr_e, int64_t n, int m, int c, int s,
+    const float2* __restrict__ V, float scale, int mode, const float2* __restrict__ Ymeas,
+    const float* __restrict__ w, float2* __restrict__ Y, double* __restrict__ partial) {
+  __shared__ double sh[kLocThreads];
+  const int64_t cm = int64_t(c) * m;
+  double acc = 0.0;
+  for (int64_t wloc = int64_t(blockIdx.x) * kLocThreads + threadIdx.x; wloc < n;
+       wloc += int64_t(gridDim.x) * kLocThreads) {
+    const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
+    for (int ci = 0; ci < c && b < e_end; ++ci) {
+      float2 kr[S];
+      const float2* kb = KT + (int64_t(ci) * n + wloc) * s;
+#pragma unroll
+      for (int k = 0; k < S; ++k) kr[k] = k < s ? kb[k] : make_float2(0.f, 0.f);
+      for (int j = b; j < e_end; ++j) {
+        const int64_t e = csr_e[j];
+        const int64_t t = e / m;
+        const int64_t eo = t * cm + int64_t(ci) * m + (e - t * m);
+        const float2* vt = V + t * s;
+        float yr = 0.f, yi = 0.f;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          if (k < s) {
+            const float2 a = kr[k], bv = vt[k];
+            yr = fmaf(a.x, bv.x, fmaf(a.y, bv.y, yr));   // a * conj(b)
+            yi = fmaf(a.y, bv.x, fmaf(-a.x, bv.y, yi));
+          }
+        }
+        float2 y = make_float2(yr * scale, yi * scale);
+        if (mode == 2) {
+          const float2 ym = Ymeas[eo];
+          y.x -= ym.x;
+          y.y -= ym.y;
+          const float ww = w ? w[eo] : 1.f;
+          acc += double(ww) * (double(y.x) * y.x + double(y.y) * y.y);
+          Y[eo] = make_float2(ww * y.x, ww * y.y);
+        } else {
+          if (mode == 0) Y[eo] = y;
+          acc += double(y.x) * y.x + double(y.y) * y.y;
+        }
+      }
+    }
+  }
+  if (partial) {
+    double r = block_sum<kLocThreads>(acc, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = r;
   }
 }
@@ -566,9 +639,25 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   int mode = 0;
   if (Y == nullptr) mode = 1;
   else if (Ymeas != nullptr) mode = 2;
-  gather_s_kernel<<<kRedBlocks, 256, 0, st>>>(KT, op->pattern, op->n, op->L, op->m, op->c, s, V,
-                                              op->scale, mode, Ymeas, w, Y,
-                                              (mode != 0 || norm_out) ? part : nullptr);
+  double* pp = (mode != 0 || norm_out) ? part : nullptr;
+  // location-major when locations are sampled >= 4 times and there are enough of them to fill
+  // the GPU with threads (cfg0's 4096 locations run faster sample-major)
+  if (int64_t(op->L) * op->m >= 4 * op->n && op->n >= 65536) {
+#define CBB_GLOC(SP)                                                                          \
+  gather_loc_kernel<SP><<<kRedBlocks, kLocThreads, 0, st>>>(KT, op->csr_off, op->csr_e, op->n, op->m,  \
+                                                    op->c, s, V, op->scale, mode, Ymeas, w, Y, pp)
+    if (s <= 4) CBB_GLOC(4);
+    else if (s <= 8) CBB_GLOC(8);
+    else if (s <= 12) CBB_GLOC(12);
+    else if (s <= 16) CBB_GLOC(16);
+    else if (s <= 20) CBB_GLOC(20);
+    else if (s <= 24) CBB_GLOC(24);
+    else CBB_GLOC(32);
+#undef CBB_GLOC
+  } else {
+    gather_s_kernel<<<kRedBlocks, 256, 0, st>>>(KT, op->pattern, op->n, op->L, op->m, op->c, s,
+                                                V, op->scale, mode, Ymeas, w, Y, pp);
+  }
   CBB_CUDA_TRY(cudaGetLastError());
   count_launches(norm_out ? 4 : 3);
   if (norm_out) return finish(part, kRedBlocks, norm_out, st);
