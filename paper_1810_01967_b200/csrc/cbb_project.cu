@@ -1617,8 +1617,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           int ba = rot + qt;                       // range tile (rot + qt) % nBh
           if (ba >= nBh) ba -= nBh;
           ba += hr * nBh;
+          if (q == 0 && lane == 0) CBB_STAMP(5, kk);
           mbar_wait(t_full + tb, ph);
           tc_fence_after();
+          if (q == 0 && lane == 0) CBB_STAMP(2, kk);
           constexpr int kRegChunks = C::kChunks < 2 ? C::kChunks : 2;
           uint32_t r[32 * kRegChunks];
           __syncwarp();
@@ -1634,6 +1636,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) arrive_lead(acc_free + part);
+              if (q == 0 && lane == 0) CBB_STAMP(3, kk);
             }
             if (qt >= 0)
               screen_tile_f32<kRegChunks>(r, int64_t(ba) * BN + 32 * h * kRegChunks, win,
@@ -1642,6 +1645,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
               runmax_f = fmaxf(runmax_f, tile_max_f32<kRegChunks>(r));
           }
           if (qt < 0 && active) thr_f = __fsub_rd(runmax_f, win);  // warm-start tile
+          if (q == 0 && lane == 0) CBB_STAMP(6, kk);
           sacc += kParts;
           if (sacc >= C::kAcc) sacc -= C::kAcc;
           tb += kParts;

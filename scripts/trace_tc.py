@@ -12,7 +12,7 @@ atoms = random_atoms(D, 10, seed=0)
 Z, _ = cone_voxels(atoms, N, seed=1, dtype=np.complex64)
 dd = cb.device_dictionary(atoms); zt = torch.from_numpy(Z).cuda()
 for _ in range(3):
-    project_device(zt, dd, algo="tcgen05", proj_c128=False)
+    project_device(zt, dd, algo=os.environ.get("TRACE_ALGO", "tcgen05"), proj_c128=False)
 torch.cuda.synchronize()
 lib = _lib.load()
 fn = lib.cbb_dev_trace_dump; fn.restype = ctypes.c_int; fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
