@@ -50,7 +50,8 @@ typedef struct cbb_dict_view {
   int32_t n_btiles;   /* ceil(d / 128) */
   const void* atoms64;   /* d x s complex128 */
   const void* atoms32;   /* d x 2*s_pad fp32 planar */
-  const void* atoms_tc;  /* fp16 UMMA tiles (fp16-accumulated screen) */
+  const void* atoms_tc;  /* fp16 UMMA rows of the fp16-accumulated screen: K-major, no swizzle,
+                            8-row groups of ceil((2s+1)/8) 16-byte core matrices */
   const float* bounds;   /* certified error bounds */
   const void* atoms_tc2; /* split hi/lo fp16 UMMA tiles (fp32-accumulated screen), s <= 21 */
   int32_t prefer_split;  /* CBB_ALGO_AUTO uses the split screen: the dictionary is coherent
@@ -120,11 +121,12 @@ int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count
  * chunks (coherent dictionaries) and were rescored warp-cooperatively.  Synchronises. */
 int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,
                                 void* stream);
-/* Bring-up / test hook: prologue only (bf16 voxel tiles + windows in the workspace). */
+/* Bring-up / test hook: prologue only (fp16 voxel rows + windows in the workspace). */
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
                          void* workspace, size_t workspace_bytes, void* stream);
-/* Bring-up / test hook: raw tcgen05 bf16 scores of voxel tile a_tile x atom tile b_tile
- * (128 x 128 fp32, row = voxel) from the workspace voxel tiles. */
+/* Bring-up / test hook: raw tcgen05 scores (fp16 operands, fp16 accumulators) of voxel tile
+ * a_tile x atom rows [128 b_tile, +128), returned as 128 x 128 fp32 (row = voxel), from the
+ * workspace voxel rows. */
 int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_tile,
                         int32_t b_tile, float* out, void* stream);
 
