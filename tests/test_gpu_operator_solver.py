@@ -297,6 +297,57 @@ def test_s_channel_chain_matches_frame_path_3d():
     assert torch.equal(G, G2)
 
 
+def test_location_major_gather_matches_oracle():
+    """n >= 65,536 locations sampled >= 4 times on average: the s-channel forward map runs
+    location-major (gather_loc_kernel), storing and norm-only; same values as the oracle chain
+    A(X~ V^H), here with c = 2 coil maps and random 3-D masks."""
+    from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
+    rng = np.random.default_rng(21)
+    shape, L, s, c = (64, 64, 16), 16, 10, 2
+    n = int(np.prod(shape))
+    m = n // 4                       # L m = 4 n
+    pat = np.stack([rng.choice(n, size=m, replace=False) for _ in range(L)])
+    coils = rng.standard_normal((c, n)) + 1j * rng.standard_normal((c, n))
+    A = make_cartesian_operator(SamplingPattern(pat, shape), coil_maps=coils)
+    V, _ = np.linalg.qr(rng.standard_normal((L, s)) + 1j * rng.standard_normal((L, s)))
+    Xc = rng.standard_normal((n, s)) + 1j * rng.standard_normal((n, s))
+    R = oop.CartesianOperator(pat, shape, coil_maps=coils)
+    dev = A.device
+    Xt = torch.from_numpy(Xc.astype(np.complex64)).to(dev)
+    Vt = torch.from_numpy(V.astype(np.complex64)).to(dev)
+    Y = A.fm_apply_compressed(Xt, Vt)
+    ref = R.apply(Xc @ V.conj().T)
+    assert rel(Y.cpu().numpy().T, ref) <= 1e-5
+    G = A.fm_adjoint_compressed(Y, Vt)
+    assert rel(G.cpu().numpy(), R.adjoint(ref) @ V) <= 1e-5
+    # norm-only mode (the step rule's ||A dX||^2, nothing stored)
+    out = torch.zeros((), dtype=torch.float64, device=dev)
+    A.fm_apply_norm2_compressed(Xt, Vt, out)
+    nref = np.linalg.norm(ref) ** 2
+    assert abs(float(out) - nref) <= 1e-5 * nref
+
+
+def test_large_projection_unsplit_matches_oracle():
+    """More than 2^17 voxels: the screen runs without atom ranges (one range per voxel tile)
+    and with a ragged last voxel tile; indices are the oracle's exact argmax."""
+    import paper_1810_01967_b200 as cb
+    from paper_1810_01967_b200.projection import project_device
+    from paper_1810_01967_b200.workloads import random_atoms, cone_voxels
+    n, d, s = (1 << 17) + 3001, 4096, 10
+    atoms = random_atoms(d, s, seed=5)
+    Z, _ = cone_voxels(atoms, n, seed=6, dtype=np.complex64)
+    dd = cb.device_dictionary(atoms)
+    idx, gam, proj = project_device(torch.from_numpy(Z).cuda(), dd, algo="tcgen05",
+                                    proj_c128=False)
+    idx = idx.cpu().numpy()
+    sc = np.real(Z.astype(np.complex128) @ atoms.conj().T)
+    ref = sc.argmax(1)
+    top = np.sort(sc, axis=1)[:, -2:]
+    near = (top[:, 1] - top[:, 0]) < 1e-5 * np.abs(top[:, 1])
+    bad = (idx != ref) & ~near
+    assert not bad.any(), int(bad.sum())
+
+
 def test_coil_ipg_matches_reference_trace():
     """Compressed exact IPG with c = 2 coil maps vs the reference solve_compressed."""
     from paper_1810_01967_b200.dictionary import CompressedDictionary, Dictionary
