@@ -125,6 +125,10 @@ def ptr(t) -> int | None:
 
 
 def stream_ptr(stream=None) -> int:
+    """cudaStream_t of `stream`, or of the current device's current stream.  The raw-stream
+    query skips torch.cuda.current_stream()'s Python wrapper (~10 us per call, a third of the
+    host time of a latency-bound cfg0 IPG solve)."""
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())

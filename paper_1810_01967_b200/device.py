@@ -32,7 +32,8 @@ def require_cuda(device=None) -> torch.device:
 
 def workspace(nbytes: int, device: torch.device, tag: str = "default") -> torch.Tensor:
     """Grow-only per-(device, tag, stream) scratch buffer."""
-    key = (device.index, tag, torch.cuda.current_stream(device).cuda_stream)
+    idx = device.index if device.index is not None else torch._C._cuda_getDevice()
+    key = (idx, tag, torch._C._cuda_getCurrentRawStream(idx))
     with _ws_lock:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:
