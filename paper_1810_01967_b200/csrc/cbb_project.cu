@@ -977,7 +977,11 @@ struct TcCfg {
   // completion barriers per tile slot k % kTBars (lcm(kAcc, kParts)): every barrier belongs to
   // one stage AND one part, whose waits consume its phases in order (no parity aliasing)
   static constexpr int kTBars = (kAcc % kParts == 0) ? kAcc : kAcc * kParts;
-  static constexpr int kNumBars = 4 + 2 * kStages + kTBars + kAcc;
+  // split screen on 128-atom tiles: each accumulator stage is two 64-column halves with their
+  // own MMAs (N = 64), commits and releases, so the first half refills while the part loads the
+  // second (the 64 fp32 scores of one half fill the part's registers)
+  static constexpr bool kHalves = SPLIT && !PAIR && kChunks == 4;
+  static constexpr int kNumBars = 4 + 2 * kStages + (kHalves ? 2 : 1) * (kTBars + kAcc);
   static_assert(kStages % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
@@ -1207,6 +1211,9 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   uint64_t* b_empty = b_full + C::kStages;
   uint64_t* t_full = b_empty + C::kStages;
   uint64_t* acc_free = t_full + C::kTBars;  // accumulator stage released by its epilogue part
+  // kHalves: second-half barriers (t_full2[tb] / acc_free2[stage]) next to the first-half ones
+  uint64_t* t_full2 = acc_free + C::kAcc;
+  uint64_t* acc_free2 = t_full2 + C::kTBars;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1251,6 +1258,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       mbar_init(b_empty + i, 1);        // the MMAs reading the stage retired
     }
     for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free + i, 4 * csz);
+    if constexpr (C::kHalves) {
+      for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full2 + i, 1);
+      for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free2 + i, 4);
+    }
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -1427,6 +1438,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
                           : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
       // the atom tile usually landed long before the accumulator stage is released: test it
       // first, so the release -> MMA hop is a single barrier wait
+      const uint32_t apar = (aphm >> sacc) & 1u;  // this stage use's release phase
       if constexpr (PAIR) {
         mbar_wait_cluster(b_full + st, ph);
         mbar_wait_cluster(acc_free + sacc, (aphm >> sacc) & 1u);
@@ -1442,7 +1454,33 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       aphm ^= 1u << sacc;
       tc_fence_after();
       if (lane == 0) CBB_STAMP(0, kk);
-      if (elect_one()) {
+      if constexpr (C::kHalves) {
+        // first half (atoms 0..63 of the tile -> columns 0..63), then, once the part has
+        // released the second half, atoms 64..127 -> columns 64..127 (B rows + 64 x 128 B)
+        constexpr uint32_t kIdH = idesc_f16_f32(128, 64);
+        if (elect_one()) {
+#pragma unroll
+          for (int kq = 0; kq < KP / 16; ++kq)
+            if (kq < nks)
+              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], kIdH, kq > 0 ? 1u : 0u);
+          tc_commit(t_full + tb);
+        }
+        __syncwarp();
+        mbar_wait(acc_free2 + sacc, apar);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kq = 0; kq < KP / 16; ++kq)
+            if (kq < nks)
+              tc_mma_f16_ts(d_tm + 64u, a_tm + uint32_t(kq * 8),
+                            bdesc[kq] + uint64_t((64 * 128) >> 4), kIdH, kq > 0 ? 1u : 0u);
+          CBB_STAMP(1, kk);
+          tc_commit(b_empty + st);
+          tc_commit(t_full2 + tb);
+          if (kk + kIss >= vt_end)
+            for (int r = 0; r < kParts / kIss; ++r) tc_commit(a_empty + (itk & 1));
+        }
+      } else if (elect_one()) {
 #pragma unroll
         for (int kq = 0; kq < KP / 16; ++kq) {
           if (kq < nks) {
@@ -1627,12 +1665,22 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
 #pragma unroll
           for (int h = 0; h < C::kChunks / kRegChunks; ++h) {
+            if (C::kHalves && h == 1) {  // second half: its own MMAs and commit
+              mbar_wait(t_full2 + tb, ph);
+              tc_fence_after();
+              __syncwarp();
+            }
 #pragma unroll
             for (int c = 0; c < kRegChunks; ++c)
               tmem_ld32_f32(ta + uint32_t(32 * (h * kRegChunks + c)),
                             *reinterpret_cast<uint32_t(*)[32]>(r + 32 * c));
             tc_wait_ld();
-            if (h + 1 == C::kChunks / kRegChunks) {
+            if (C::kHalves) {  // release this half at once
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(h == 0 ? acc_free + part : acc_free2 + part);
+              if (h == 1 && q == 0 && lane == 0) CBB_STAMP(3, kk);
+            } else if (h + 1 == C::kChunks / kRegChunks) {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) arrive_lead(acc_free + part);

@@ -39,7 +39,7 @@ A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape), dev
 print("op", time.perf_counter() - t, flush=True)
 import os
 prof = os.environ.get("PROBE_PROFILE") == "1"
-for it in ((1,) if prof else (1, iters)):
+for it in ((int(os.environ.get("PROBE_PROF_ITERS", "1")),) if prof else (1, iters)):
     if prof:
         torch.cuda.synchronize()
         torch.cuda.profiler.start()
