@@ -3,7 +3,7 @@
 * Voxel sharding (cfg1): voxels are independent units; every rank projects its own
   contiguous voxel range against the replicated dictionary.  No data-path collective
   (``shard_range`` + ``project_cone_exact``; ``bench.py`` reports weak scaling).
-* Atom sharding (cfg3, D = 2^20 too large to replicate cheaply with its bf16 / fp32 / fp64
+* Atom sharding (cfg3, D = 2^20 too large to replicate cheaply with its fp16 / fp32 / fp64
   copies): every rank screens its dictionary shard (``cbb_project_best``: shard-local exact
   fp64 argmax as a GLOBAL index + its raw score), then the first-index global argmax of
   ``projection.py:62`` is recovered EXACTLY with two collectives over NCCL:

@@ -6,7 +6,7 @@ Reference semantics (``coverblip/projection.py:45-67``): for every voxel row
 ``projected_v = gamma_v * D_j*`` (``:64``); ``cost = n * d`` (``:67``); a shape
 mismatch raises ``ValueError("dimension mismatch: ...")`` (``:53-56``).
 
-B200 path: ``cbb_project_cone_exact`` (tcgen05 bf16 screening with a certified
+B200 path: ``cbb_project_cone_exact`` (tcgen05 fp16 screening with a certified
 window + fp64 rescoring, see ``csrc/cbb_project.cuh``).  numpy inputs return
 numpy outputs with the reference dtypes (int64 / float64 / complex128); torch
 CUDA inputs stay on the device.
