@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define CBB_ABI_VERSION 2
+#define CBB_ABI_VERSION 3
 
 /* Device view of a prepared dictionary (filled by cbb_dict_prepare). */
 typedef struct cbb_dict_view {
@@ -57,6 +57,17 @@ typedef struct cbb_dict_view {
   int32_t prefer_split;  /* CBB_ALGO_AUTO uses the split screen: the dictionary is coherent
                             (its sampled atoms have near-duplicates inside the fp16 window) */
   int32_t reserved;
+  int32_t n_tiles2;      /* split-screen atom tiles */
+  int32_t reserved2;
+  /* coherent dictionaries (prefer_split): the split tiles hold the atoms in a bisection order
+     with per-tile bounds, so IPG projections with a warm-start hint screen only the tiles
+     that may hold a voxel's argmax (results unchanged); NULL otherwise */
+  const int32_t* tc2_atom;  /* split-tile row -> atom index */
+  const int32_t* tc2_pos;   /* atom -> split-tile row */
+  const float* tile_c;      /* per split tile: fp32 centroid (2 s_pad, planar) */
+  const float* tile_r;      /*   and radius */
+  const void* ctr_tc2;      /* the centroids as split-operand tiles (pruning bound pass) */
+  const float* tile_rs;     /* radius * scale_d per centroid */
 } cbb_dict_view;
 
 /* Projection algorithms. */
@@ -65,8 +76,7 @@ enum {
   CBB_ALGO_TCGEN05 = 1,     /* fp16 operands, fp16 accumulators (2s < 64) */
   CBB_ALGO_FFMA = 2,        /* fp32 FFMA screen */
   CBB_ALGO_EXHAUSTIVE = 3,  /* fp64 scan of every atom */
-  CBB_ALGO_TCGEN05_SPLIT = 4, /* hi/lo fp16 operands, fp32 accumulators (s <= 21) */
-  CBB_ALGO_TCGEN05_HI32 = 5  /* fp16 operands, fp32 accumulators (2s < 64) */
+  CBB_ALGO_TCGEN05_SPLIT = 4 /* hi/lo fp16 operands, fp32 accumulators (s <= 21) */
 };
 
 int cbb_abi_version(void);
@@ -89,6 +99,10 @@ int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s
 
 /* ---- exact cone projection (projection.py:45-67) ---- */
 size_t cbb_project_workspace_bytes(int64_t n, int32_t s);
+/* Workspace for projections of n voxels against this dictionary, including the tile-pruning
+ * buffers of the split screen (used by cbb_project_step with a hint; a workspace of
+ * cbb_project_workspace_bytes(n, s) bytes simply screens every tile). */
+size_t cbb_project_workspace_bytes_dict(int64_t n, const cbb_dict_view* dict);
 /* z: n x s complex (c128 if z_c128 else c64).  Outputs (any may be NULL):
  * idx_out int64 (idx_int64=1) or int32, gamma_out fp64, proj_out c128 (proj_c128=1) or c64. */
 int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
@@ -121,6 +135,13 @@ int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count
  * chunks (coherent dictionaries) and were rescored warp-cooperatively.  Synchronises. */
 int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,
                                 void* stream);
+/* Tile-pruning statistics of the last projection on this workspace (sized with
+ * cbb_project_workspace_bytes_dict): listed (voxel tile, atom tile) pairs and all pairs of the
+ * split screen; listed = -1 if that projection screened every tile (or the workspace has no
+ * pruning buffers).  Synchronises. */
+int cbb_project_prune_stats(void* workspace, size_t workspace_bytes, int64_t n,
+                            const cbb_dict_view* dict, int64_t* listed_host, int64_t* total_host,
+                            void* stream);
 /* Bring-up / test hook: prologue only (fp16 voxel rows + windows in the workspace). */
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
                          void* workspace, size_t workspace_bytes, void* stream);

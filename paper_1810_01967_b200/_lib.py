@@ -23,14 +23,16 @@ c_vp = ctypes.c_void_p
 
 ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED, ERR_CUFFT = 1, 2, 3, 4
 
-ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3, "tcgen05_split": 4, "tcgen05_hi32": 5}
+ALGOS = {"auto": 0, "tcgen05": 1, "ffma": 2, "exhaustive": 3, "tcgen05_split": 4}
 
 
 class DictView(ctypes.Structure):
     _fields_ = [("d", c_i64), ("s", c_i32), ("s_pad", c_i32), ("kpad", c_i32),
                 ("n_btiles", c_i32), ("atoms64", c_vp), ("atoms32", c_vp),
                 ("atoms_tc", c_vp), ("bounds", c_vp), ("atoms_tc2", c_vp),
-                ("prefer_split", c_i32), ("reserved", c_i32)]
+                ("prefer_split", c_i32), ("reserved", c_i32), ("n_tiles2", c_i32),
+                ("reserved2", c_i32), ("tc2_atom", c_vp), ("tc2_pos", c_vp), ("tile_c", c_vp),
+                ("tile_r", c_vp), ("ctr_tc2", c_vp), ("tile_rs", c_vp)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/coverblip_b200.h
@@ -44,6 +46,7 @@ SIGNATURES = {
     "cbb_dict_storage_bytes": (c_size, [c_i64, c_i32]),
     "cbb_dict_prepare": (c_int, [c_vp, c_i32, c_i64, c_i32, c_vp, ctypes.POINTER(DictView), c_vp]),
     "cbb_project_workspace_bytes": (c_size, [c_i64, c_i32]),
+    "cbb_project_workspace_bytes_dict": (c_size, [c_i64, ctypes.POINTER(DictView)]),
     "cbb_project_cone_exact": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_i32,
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_step": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, ctypes.POINTER(DictView), c_vp,
@@ -54,6 +57,8 @@ SIGNATURES = {
                                 c_vp]),
     "cbb_project_overflow_counts": (c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "cbb_project_overflow_count": (c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_int), c_vp]),
+    "cbb_project_prune_stats": (c_int, [c_vp, c_size, c_i64, ctypes.POINTER(DictView),
+                                        ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp]),
     "cbb_project_prologue": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_size,
                                      c_vp]),
     "cbb_debug_tc_scores": (c_int, [c_vp, ctypes.POINTER(DictView), c_i32, c_i32, c_vp, c_vp]),

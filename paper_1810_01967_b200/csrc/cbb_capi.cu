@@ -27,10 +27,13 @@ size_t dict_bytes(int64_t d, int s, size_t*, size_t*, size_t*, size_t*, size_t*)
 int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, DictView* view,
                  cudaStream_t st);
 struct ProjWs;
-size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr);
+size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr, int prune_tiles);
+int prune_tiles_of(const DictView& dv);
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st);
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st);
+int project_prune_stats(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView& dv,
+                        int64_t* listed, int64_t* total, cudaStream_t st);
 int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st);
 int tc_debug_scores(const void* ztiles, const void* atiles, int kpad, int s, int a_tile,
                     int b_tile, float* out, cudaStream_t st);
@@ -76,6 +79,13 @@ static DictView to_view(const cbb_dict_view* v) {
   d.bounds = v->bounds;
   d.atoms_tc2 = static_cast<const uint8_t*>(v->atoms_tc2);
   d.prefer_split = v->prefer_split;
+  d.n_tiles2 = v->n_tiles2;
+  d.tc2_atom = v->tc2_atom;
+  d.tc2_pos = v->tc2_pos;
+  d.tile_c = v->tile_c;
+  d.tile_r = v->tile_r;
+  d.ctr_tc2 = static_cast<const uint8_t*>(v->ctr_tc2);
+  d.tile_rs = v->tile_rs;
   return d;
 }
 
@@ -124,11 +134,24 @@ int cbb_dict_prepare(const void* atoms, int32_t atoms_c128, int64_t d, int32_t s
   view_out->atoms_tc2 = v.atoms_tc2;
   view_out->prefer_split = v.prefer_split;
   view_out->reserved = 0;
+  view_out->n_tiles2 = v.n_tiles2;
+  view_out->reserved2 = 0;
+  view_out->tc2_atom = v.tc2_atom;
+  view_out->tc2_pos = v.tc2_pos;
+  view_out->tile_c = v.tile_c;
+  view_out->tile_r = v.tile_r;
+  view_out->ctr_tc2 = v.ctr_tc2;
+  view_out->tile_rs = v.tile_rs;
   return kOk;
 }
 
 size_t cbb_project_workspace_bytes(int64_t n, int32_t s) {
-  return project_ws_bytes(n, s, nullptr, nullptr);
+  return project_ws_bytes(n, s, nullptr, nullptr, 0);
+}
+
+size_t cbb_project_workspace_bytes_dict(int64_t n, const cbb_dict_view* dict) {
+  if (!dict || dict->s <= 0) return 0;
+  return project_ws_bytes(n, dict->s, nullptr, nullptr, prune_tiles_of(to_view(dict)));
 }
 
 int cbb_project_cone_exact(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
@@ -188,6 +211,15 @@ int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count
   return project_overflow_count(workspace, n, s, count_host, S(stream));
 }
 
+int cbb_project_prune_stats(void* workspace, size_t workspace_bytes, int64_t n,
+                            const cbb_dict_view* dict, int64_t* listed_host, int64_t* total_host,
+                            void* stream) {
+  if (int rc = check_view(dict)) return rc;
+  if (!workspace || !listed_host || !total_host) return kErrArgument;
+  return project_prune_stats(workspace, workspace_bytes, n, to_view(dict), listed_host,
+                             total_host, S(stream));
+}
+
 int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,
                                 void* stream) {
   if (!workspace || !counts_host) return kErrArgument;
@@ -197,7 +229,7 @@ int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* 
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
                          void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_view(dict)) return rc;
-  if (workspace_bytes < project_ws_bytes(n, dict->s, nullptr, nullptr)) return kErrArgument;
+  if (workspace_bytes < project_ws_bytes(n, dict->s, nullptr, nullptr, 0)) return kErrArgument;
   ZSource zs{z, z_c128, nullptr, nullptr, 0.f, nullptr, nullptr};
   return prologue_only(zs, n, to_view(dict), workspace, S(stream));
 }

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 
@@ -24,13 +25,16 @@ enum Status : int {
   kErrCufft = 4,
 };
 
-#define CBB_CUDA_TRY(expr)                                  \
-  do {                                                      \
-    cudaError_t _e = (expr);                                \
-    if (_e != cudaSuccess) {                                \
-      cbb::set_last_error(cudaGetErrorString(_e));          \
-      return cbb::kErrCuda;                                 \
-    }                                                       \
+#define CBB_STR2(x) #x
+#define CBB_STR(x) CBB_STR2(x)
+#define CBB_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      cbb::set_last_error((std::string(cudaGetErrorString(_e)) +                  \
+                           " (" __FILE__ ":" CBB_STR(__LINE__) ")").c_str());     \
+      return cbb::kErrCuda;                                                       \
+    }                                                                             \
   } while (0)
 
 void set_last_error(const char* msg);

@@ -18,10 +18,32 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <algorithm>
+#include <atomic>
+#include <utility>
+#include <vector>
+
+#include <cub/cub.cuh>
 
 namespace cbb {
 
 // ============================================================== helpers
+// compile-time width for the fp64 scoring loops (s_pad; 0 = runtime loop for s > 32)
+#define CBB_DISPATCH_S(s_pad, ...)          \
+  switch (s_pad) {                          \
+    case 2: { constexpr int S_ = 2; __VA_ARGS__; }   \
+    case 4: { constexpr int S_ = 4; __VA_ARGS__; }   \
+    case 6: { constexpr int S_ = 6; __VA_ARGS__; }   \
+    case 8: { constexpr int S_ = 8; __VA_ARGS__; }   \
+    case 10: { constexpr int S_ = 10; __VA_ARGS__; } \
+    case 12: { constexpr int S_ = 12; __VA_ARGS__; } \
+    case 16: { constexpr int S_ = 16; __VA_ARGS__; } \
+    case 20: { constexpr int S_ = 20; __VA_ARGS__; } \
+    case 24: { constexpr int S_ = 24; __VA_ARGS__; } \
+    case 32: { constexpr int S_ = 32; __VA_ARGS__; } \
+    default: { constexpr int S_ = 0; __VA_ARGS__; }  \
+  }
+
 __device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
   atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
 }
@@ -397,17 +419,19 @@ __global__ void prep_tc_kernel(const double2* __restrict__ atoms64, int64_t d, i
 // d_hi = fp16(scale_d d), d_lo = fp16(scale_d d - d_hi), K = split_kp(s), 128-byte swizzle,
 // split_rows(K)-row tiles (split_elem_offset).  Padded rows carry -65504 in the sentinel column
 // (their fp32-accumulated score is -65504 for every voxel).
+// perm (coherent dictionaries): row p holds atom perm[p] (bisection order); null: row p = atom p.
 __global__ void prep_tc2_kernel(const double2* __restrict__ atoms64, int64_t d, int64_t d_pad,
-                                int s, uint8_t* __restrict__ atoms_tc2,
-                                float* __restrict__ bounds) {
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= d_pad) return;
+                                int s, const int32_t* __restrict__ perm,
+                                uint8_t* __restrict__ atoms_tc2, float* __restrict__ bounds) {
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= d_pad) return;
   const int kp = split_kp(s), rows = split_rows(kp);
-  const int tile = int(j / rows), r = int(j % rows);
+  const int tile = int(p / rows), r = int(p % rows);
   uint8_t* trow = atoms_tc2 + size_t(tile) * rows * kp * 2;
   auto put = [&](int e, unsigned short h) {
     *reinterpret_cast<unsigned short*>(trow + split_elem_offset(r, e, rows)) = h;
   };
+  const int64_t j = p >= d ? d : (perm ? int64_t(perm[p]) : p);
   if (j >= d) {
     put(6 * s, kF16MinusMax);
     return;
@@ -435,6 +459,42 @@ __global__ void prep_tc2_kernel(const double2* __restrict__ atoms64, int64_t d, 
   atomic_max_nonneg(bounds + kBDeltaS, __double2float_ru(sqrt(del)));
   atomic_max_nonneg(bounds + kBDloMax, __double2float_ru(sqrt(nlo)));
   atomic_max_nonneg(bounds + kBRowMax, __double2float_ru(sqrt(2.0 * nhi + nlo) * (1.0 + 1e-12)));
+}
+
+// Centroid rows of the tile-pruning bound pass: row t = split-operand row of the fp32 centroid c_t
+// (same layout and scale_d as prep_tc2_kernel, no bound updates: the bound pass carries its own
+// margin), rs[t] = ru(scale_d r_t); rows >= nt are sentinel rows (score -65504).
+__global__ void prep_ctr_kernel(const float* __restrict__ cen, const float* __restrict__ rad,
+                                int nt, int rows_alloc, int s, int sp,
+                                const float* __restrict__ bounds, uint8_t* __restrict__ out,
+                                float* __restrict__ rs) {
+  const int t = int(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows_alloc) return;
+  const int kp = split_kp(s), rows = split_rows(kp);
+  uint8_t* trow = out + size_t(t / rows) * rows * kp * 2;
+  const int r = t % rows;
+  auto put = [&](int e, unsigned short h) {
+    *reinterpret_cast<unsigned short*>(trow + split_elem_offset(r, e, rows)) = h;
+  };
+  if (t >= nt) {
+    put(6 * s, kF16MinusMax);
+    rs[t] = 0.f;
+    return;
+  }
+  const double sc = dict_scale(bounds);
+  rs[t] = __double2float_ru(double(rad[t]) * sc);
+  for (int k = 0; k < s; ++k) {
+    const double x[2] = {double(cen[size_t(t) * 2 * sp + k]) * sc,
+                         double(cen[size_t(t) * 2 * sp + sp + k]) * sc};
+    for (int c = 0; c < 2; ++c) {
+      const unsigned short hi = f16_bits_rn(x[c]);
+      const unsigned short lo = f16_bits_rn(x[c] - f16_bits_to_double(hi));
+      const int e = c * s + k;
+      put(e, hi);
+      put(2 * s + e, hi);
+      put(4 * s + e, lo);
+    }
+  }
 }
 
 // Coherence estimate (selects the screen in auto mode): for kCohSamples evenly spaced atoms i,
@@ -491,9 +551,13 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 const float* __restrict__ bounds, uint8_t* __restrict__ ztiles,
                                 float* __restrict__ win_tc, float* __restrict__ win32,
                                 int s_pad, const double2* __restrict__ atoms64,
-                                int64_t d_atoms, float* __restrict__ init_tc, int split) {
+                                int64_t d_atoms, float* __restrict__ init_tc, int split,
+                                float2* __restrict__ lbz) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
+  // tile pruning: (exact hint score rounded down, ||z|| rounded up); zero and non-finite voxels
+  // are decided without the screen (+inf: they need no atom tile)
+  if (lbz && v < n) lbz[v] = make_float2(INFINITY, 0.f);
   // plain row-major fp16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
   uint8_t* trow = ztiles ? ztiles + size_t(v) * kpad * 2 : nullptr;
   if (v >= n) {
@@ -648,6 +712,13 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
         acc = fma(z.y, a[k].y, acc);
       }
       init = __double2float_rd(acc * sv * sd - eb * 1.001);
+      if (lbz) {  // scaled units of the tile-pruning bound pass (see prune_prepare)
+        const double zn_s = sqrt(nz) * sv;
+        lbz[v] = make_float2(__double2float_rd(acc * sv * sd - 0x1p-11 * zn_s * sd * dmax),
+                             __double2float_ru(zn_s));
+      }
+    } else if (lbz) {
+      lbz[v] = make_float2(-INFINITY, __double2float_ru(sqrt(nz) * sv));
     }
     init_tc[v] = init;
   }
@@ -928,38 +999,26 @@ constexpr int kPadTiles = 8;
 // SPLIT: hi/lo fp16 operands with fp32 accumulators: KP = 64 -> 128-atom tiles (N = 128 MMAs;
 // measured faster than 64-atom tiles with six stages), screened in two 64-register halves;
 // KP = 128 -> 64-atom tiles (the 16 KB stages keep a 9-deep ring).
-// PAIR: the CTAs of a cluster pair run cta_group::2 MMAs (M = 256: each CTA's 128 voxels); every
-// CTA bulk-copies only its half of each atom tile (kBNloc rows), which halves the L2 -> SMEM
-// atom stream that bounds the single-CTA kernel.
-// HI32: the fp16 operand rows of the fp16 screen (2s + 1 columns) with FP32 accumulators: the
-// screen issues the fp16 screen's K-steps but its window is the operand rounding only
-// (~2^-10 |z| instead of ~2^-8): the split screen's fp32 epilogue on 128-atom tiles.
-template <int KP, bool SPLIT = false, bool PAIR = false, bool HI32 = false>
+template <int KP, bool SPLIT = false>
 struct TcCfg {
   static_assert(!SPLIT || KP == 64 || KP == 128, "split tiles are 64 or 128 wide");
-  static_assert(!(SPLIT && HI32), "one operand format");
-  static constexpr bool kF32 = SPLIT || HI32;  // fp32 accumulators, fp32 epilogue
+  static constexpr bool kF32 = SPLIT;  // fp32 accumulators, fp32 epilogue
   // 32-atom chunks per tile (split: the tile is one split_rows(KP)-row storage tile)
-  static constexpr int kChunks = SPLIT ? split_rows(KP) / 32 : HI32 ? 4 : (KP == 32 ? 5 : 4);
+  static constexpr int kChunks = SPLIT ? split_rows(KP) / 32 : (KP == 32 ? 5 : 4);
   static constexpr int BN = 32 * kChunks;                    // 160 (KP 32) / 128 / 64 (split)
   static constexpr int kACols = KP / 2;                      // packed fp16 pairs per lane
   static constexpr int kAcc = 3;                             // x BN accumulator columns
   static constexpr int kAccCols = BN;
   static constexpr int kAColOff = kAcc * kAccCols;           // A buffers after the stages
   static_assert(kAColOff + 2 * kACols <= 512, "TMEM budget");
-  static constexpr int kBNloc = PAIR ? BN / 2 : BN;          // atom rows in this CTA's SMEM
   static constexpr int kRowBytes = (KP < 64 ? KP : 64) * 2;   // bytes per row of a K block
   static constexpr int kBlk = KP <= 64 ? 1 : KP / 64;         // K blocks per tile
-  // split tiles in global memory / this CTA's part (= the ring's stage stride); the fp16 screens
-  // copy only tc_nc(s) 16-byte chunks per row (tile_bytes / copy_bytes in the kernel)
+  // split tiles in global memory (= the ring's stage stride); the fp16 screens copy only
+  // tc_nc(s) 16-byte chunks per row (tile_bytes / copy_bytes in the kernel)
   static constexpr int kBTileBytes = BN * KP * 2;
-  static constexpr int kBBytes = kBNloc * KP * 2;
-  static_assert(kBNloc % 8 == 0, "8-row swizzle groups");
-#ifdef CBB_RING_KB
-  static constexpr int kRing = CBB_RING_KB * 1024;
-#else
+  static constexpr int kBBytes = kBTileBytes;
+  static_assert(BN % 8 == 0, "8-row swizzle groups");
   static constexpr int kRing = (KP == 32 ? 96 : 144) * 1024;
-#endif
   static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
   static_assert(kBBytes % 1024 == 0, "stage buffers keep the 1024 B swizzle alignment");
   static constexpr int kStages = (kStagesRaw / kParts) * kParts;
@@ -980,14 +1039,13 @@ struct TcCfg {
   // split screen on 128-atom tiles: each accumulator stage is two 64-column halves with their
   // own MMAs (N = 64), commits and releases, so the first half refills while the part loads the
   // second (the 64 fp32 scores of one half fill the part's registers)
-  static constexpr bool kHalves = SPLIT && !PAIR && kChunks == 4;
+  static constexpr bool kHalves = SPLIT && kChunks == 4;
   static constexpr int kNumBars = 4 + 2 * kStages + (kHalves ? 2 : 1) * (kTBars + kAcc);
   static_assert(kStages % kParts == 0, "barrier ownership");
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
   static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr int kM = PAIR ? 256 : 128;
-  static constexpr uint32_t kIdesc = kF32 ? idesc_f16_f32(kM, BN) : idesc_f16_f16(kM, BN);
+  static constexpr uint32_t kIdesc = kF32 ? idesc_f16_f32(128, BN) : idesc_f16_f16(128, BN);
   static constexpr int kMinTiles = kParts;  // every part owns >= 1 tile per voxel tile
 };
 
@@ -1191,15 +1249,28 @@ __device__ __forceinline__ void stage_voxel_row(const uint8_t* __restrict__ zrow
 }
 
 // RANGES: the dictionary is split into nsplit_arg atom ranges (small projections); without it the
-// range arithmetic folds away (nsplit = 1)
-template <int KP, bool SPLIT, bool PAIR, bool HI32, bool RANGES = false>
-__global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
+// range arithmetic folds away (nsplit = 1).
+// PRUNE (split screen, IPG warm start): the voxel tiles are formed in screen order (voxel vperm[p]
+// at row p % 128 of tile p / 128) and each screens only the atom tiles its prune list holds
+// (prune_kernel: tiles that may contain a voxel's argmax); a work unit (voxel tile, range hr)
+// takes the list slice [pcnt c hr / nsplit, c (hr + 1) / nsplit).
+// BOUND (the pruning pass itself): `dv` holds the split tiles of the atom-tile CENTROIDS; per
+// (voxel, centroid) the epilogue tests the Cauchy-Schwarz bound s~ + zn r >= lb (scaled units,
+// lbz = (lb - margin, zn) per voxel, bnd_rs = r per centroid) and ORs the voxel tile's need bits
+// into bnd_bits[vt][bnd_words] (see prune_prepare).
+template <int KP, bool SPLIT, bool RANGES = false, bool PRUNE = false, bool BOUND = false>
+__global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     mf_tc_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
                  const float* __restrict__ win_tc, const float* __restrict__ init_tc,
                  DictView dv, int64_t n_pad, int2* __restrict__ cand, int2* __restrict__ meta,
-                 const uint8_t* __restrict__ hint_tiles, int n_hint, int nsplit_arg) {
-  using C = TcCfg<KP, SPLIT, PAIR, HI32>;
-  static_assert(!(PAIR && RANGES), "CTA pairs screen the whole dictionary");
+                 const uint8_t* __restrict__ hint_tiles, int n_hint, int nsplit_arg,
+                 const int32_t* __restrict__ vperm, const int* __restrict__ pcnt,
+                 const uint16_t* __restrict__ plist, int plist_stride,
+                 const float2* __restrict__ lbz, const float* __restrict__ bnd_rs,
+                 uint32_t* __restrict__ bnd_bits, int bnd_words) {
+  using C = TcCfg<KP, SPLIT>;
+  static_assert(!PRUNE || SPLIT, "pruned lists index the split tiles");
+  static_assert(!BOUND || (SPLIT && !RANGES && !PRUNE), "bound pass: split tiles, whole list");
   const int nsplit = RANGES ? nsplit_arg : 1;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -1221,55 +1292,65 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   const int nB = int((d + BN - 1) / BN);
   // work unit u (the CTA's units are u = blockIdx.x + it * gridDim.x): voxel tile u / nsplit,
   // atom tiles [h nBh, (h + 1) nBh) with h = u % nsplit (the last range runs into sentinel
-  // tiles when nsplit does not divide nB; PAIR: nsplit = 1)
+  // tiles when nsplit does not divide nB); PRUNE: a slice of the voxel tile's list
   const int nBh = (nB + nsplit - 1) / nsplit;
-  // atom tile bytes in global memory and this CTA's copy of it: the fp16 screens store
-  // tc_nc(s) chunks per row (no-swizzle layout), the split screen full swizzled K rows
+  // atom tile bytes in global memory and the copy: the fp16 screens store tc_nc(s) chunks per
+  // row (no-swizzle layout), the split screen full swizzled K rows
   const int nc = tc_nc(dv.s);
   const uint32_t tile_bytes = SPLIT ? uint32_t(C::kBTileBytes) : uint32_t(BN * nc * 16);
-  const uint32_t copy_bytes = SPLIT ? uint32_t(C::kBBytes) : uint32_t(C::kBNloc * nc * 16);
-  // PAIR: the two CTAs (ranks 0 = leader, 1) of a cluster stream the same atom tiles in lockstep
-  // (same rotation, same number of voxel tiles: the surplus ones are dead, every row v >= n).
-  // The leader's issuers run the pair's MMAs; the odd CTA's epilogue and producer signal the
-  // leader's barriers remotely, its issuer warps relay "my half of tile k landed".
-  const int crank = PAIR ? int(cluster_ctarank()) : 0;
-  const bool leader = crank == 0;
-  const int csz = PAIR ? 2 : 1;
-  const int rot = int((int64_t(blockIdx.x / csz) * nBh) / (gridDim.x / csz));
-  const int my_vts = PAIR ? (n_vt + int(gridDim.x) - 1) / int(gridDim.x)
-                          : (n_vt * nsplit - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
-  // per voxel tile: n_hint warm-start tiles (the voxel tile's own hint atoms, each hint tile
-  // repeated for the kParts parts: tile qt -> hint tile qt / kParts), then the nB atom tiles
-  const int T = nBh + n_hint;
-  const uint32_t total = uint32_t(my_vts) * uint32_t(T);  // this CTA's tiles
+  const uint32_t copy_bytes = SPLIT ? uint32_t(C::kBBytes) : uint32_t(BN * nc * 16);
+  // unpruned screens visit the atom tiles in a per-CTA rotated order (spreads L2 traffic)
+  const int rot = (PRUNE || BOUND) ? 0 : int((int64_t(blockIdx.x) * nBh) / gridDim.x);
+  const int my_vts = (n_vt * nsplit - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  // per work unit: n_hint warm-start tiles (the voxel tile's own hint atoms, each hint tile
+  // repeated for the kParts parts: tile qt -> hint tile qt / kParts), then its atom tiles
+  struct Unit {
+    int vt, hr, lo, len;  // voxel tile, atom range, first list slot / tile, atom tiles
+  };
+  auto unit_of = [&](int it) {
+    Unit x;
+    const int u = int(blockIdx.x) + it * int(gridDim.x);
+    x.vt = u / nsplit;
+    x.hr = u - x.vt * nsplit;
+    if constexpr (PRUNE) {
+      const int c = pcnt[x.vt];
+      x.lo = int((int64_t(c) * x.hr) / nsplit);
+      x.len = int((int64_t(c) * (x.hr + 1)) / nsplit) - x.lo;
+    } else {
+      x.lo = x.hr * nBh;
+      x.len = nBh;
+    }
+    return x;
+  };
+  // voxel of row `row` of voxel tile vt (PRUNE: screen order); n if past the end
+  auto voxel_of = [&](int vt, int row) -> int64_t {
+    const int64_t p = int64_t(vt) * C::kVox + row;
+    if (p >= n) return n;
+    if constexpr (PRUNE || BOUND) return int64_t(vperm[p]);
+    return p;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(a_full + i, 4 * csz);   // the 4 part-0 warps (of both CTAs) stage A
+      mbar_init(a_full + i, 4);         // the 4 part-0 warps stage A
       mbar_init(a_empty + i, kParts);   // each issuer commits after its last tile of a voxel tile
     }
     for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full + i, 1);
-    // b_full: the atom tile landed (producer with tx; PAIR leader: + the odd CTA's relayed "my
-    // half landed").  acc_free: the 4 warps (PAIR: of both CTAs) of the part that read the
-    // accumulator stage released it.  Separate barriers: with one barrier counting both, the
-    // issuer woke ~520 clk after the last release (measured), ~2x the separate waits.
+    // b_full: the atom tile landed (producer with tx).  acc_free: the 4 warps of the part that
+    // read the accumulator stage released it.  Separate barriers: with one barrier counting
+    // both, the issuer woke ~520 clk after the last release (measured), ~2x the separate waits.
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(b_full + i, (PAIR && leader) ? 2 : 1);
+      mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);        // the MMAs reading the stage retired
     }
-    for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free + i, 4 * csz);
+    for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free + i, 4);
     if constexpr (C::kHalves) {
       for (int i = 0; i < C::kTBars; ++i) mbar_init(t_full2 + i, 1);
       for (int i = 0; i < C::kAcc; ++i) mbar_init(acc_free2 + i, 4);
     }
     mbar_fence_init();
   }
-  if (warp == 1) {
-    if constexpr (PAIR)
-      tmem_alloc2(tmem_holder, 512);
-    else
-      tmem_alloc(tmem_holder, 512);
-  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
   // published thresholds: tag 0xffff, -inf (matches no voxel tile a CTA reaches in practice,
   // and would only contribute -inf)
   for (int i = threadIdx.x; i < 4 * C::kVox; i += blockDim.x)
@@ -1281,11 +1362,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 0 && !PAIR) {
+  if (warp == 0) {
     // ------------------------------------------------ producer (bulk copies of atom tiles)
     // kParts lanes, lane p copies the tiles k = p (mod kParts) (kStages % kParts == 0: it owns
     // the stages p, p + kParts, ...).  A cp.async.bulk blocks its thread ~140 clk and the
@@ -1298,102 +1378,34 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       const uint32_t ring0 = smem_u32(smem + C::kOffB);
       int st = lane;
       uint32_t ph = 0;
-      int it = 0, b = lane;  // work-unit iteration and tile index inside it
-      while (b >= T) {
-        b -= T;
-        ++it;
-      }
-      // per work unit: its atom range's first tile and its voxel tile's hint tiles
-      const uint8_t* abase = nullptr;
-      const uint8_t* hbase = nullptr;
-      int it_set = -1;
-      for (uint32_t kk = uint32_t(lane); kk < total; kk += kParts) {
-        if (it != it_set) {
-          const int u = int(blockIdx.x) + it * int(gridDim.x);
-          const int vt = u / nsplit;
-          abase = atiles + size_t(u - vt * nsplit) * nBh * tile_bytes;
-          hbase = hint_tiles + size_t(vt) * (n_hint / kParts) * tile_bytes;
-          it_set = it;
-        }
-        mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
-        const uint8_t* src;
-        if (b < n_hint) {
-          src = hbase + size_t(b / kParts) * tile_bytes;
-        } else {
-          int ba = rot + b - n_hint;
-          if (ba >= nBh) ba -= nBh;
-          src = abase + size_t(ba) * tile_bytes;
-        }
-        mbar_arrive_expect_tx_addr(b_full0 + 8 * st, copy_bytes);
-        bulk_g2s_addr(ring0 + st * C::kBBytes, src, copy_bytes, b_full0 + 8 * st, pol_b);
-        CBB_STAMP(7, kk);
-        st += kParts;
-        if (st >= C::kStages) {
-          st -= C::kStages;
-          ph ^= 1u;
-        }
-        b += kParts;
-        while (b >= T) {
-          b -= T;
-          ++it;
-        }
-      }
-    }
-  } else if (warp == 0) {
-    // ------------------------------------------------ PAIR producer (half of every atom tile)
-    const uint64_t pol_b = policy_evict_last();
-    const uint8_t* atiles = SPLIT ? dv.atoms_tc2 : dv.atoms_tc;
-    int st = 0;
-    uint32_t ph = 0;
-    for (int it = 0; it < my_vts; ++it) {
-      const int vt = int(blockIdx.x) + it * int(gridDim.x);
-      int ba = rot;
-      for (int b = 0; b < T; ++b) {
-        mbar_wait(b_empty + st, ph ^ 1u);
-        if (elect_one()) {
-          // hint tiles belong to the voxel tile (PAIR: to the pair's 256-voxel group)
-          const int hg = PAIR ? vt / 2 : vt, n_hg = PAIR ? (n_vt + 1) / 2 : n_vt;
-          const int hvt = hg < n_hg ? hg : n_hg - 1;  // dead voxel tiles reuse a valid hint
-          const uint8_t* src =
-              b < n_hint
-                  ? hint_tiles + (size_t(hvt) * (n_hint / kParts) + b / kParts) * tile_bytes
-                  : atiles + size_t(ba) * tile_bytes;
-          uint8_t* dst = smem + C::kOffB + st * C::kBBytes;
-          mbar_arrive_expect_tx(b_full + st, copy_bytes);
-          // this CTA's rows [crank * kBNloc, +kBNloc) of every K block
-          if constexpr (SPLIT) {
-#pragma unroll
-            for (int kb = 0; kb < C::kBlk; ++kb)
-              bulk_g2s(dst + kb * C::kBNloc * C::kRowBytes,
-                       src + (kb * BN + crank * C::kBNloc) * C::kRowBytes,
-                       uint32_t(C::kBNloc * C::kRowBytes), b_full + st, pol_b);
+      int b = lane;  // this lane's next tile inside the current work unit
+      for (int it = 0; it < my_vts; ++it) {
+        const Unit un = unit_of(it);
+        const int T = n_hint + un.len;
+        const uint8_t* hbase = hint_tiles + size_t(un.vt) * (n_hint / kParts) * tile_bytes;
+        const uint16_t* lst = PRUNE ? plist + size_t(un.vt) * plist_stride + un.lo : nullptr;
+        for (; b < T; b += kParts) {
+          // list entry loaded before the ring wait (its latency overlaps the wait)
+          int ba;
+          if constexpr (PRUNE) {
+            ba = b >= n_hint ? int(lst[b - n_hint]) : 0;
           } else {
-            bulk_g2s(dst, src + crank * copy_bytes, copy_bytes, b_full + st, pol_b);
+            ba = rot + b - n_hint;
+            if (ba >= nBh) ba -= nBh;
+            ba += un.lo;
           }
-          CBB_STAMP(7, uint32_t(it) * uint32_t(T) + uint32_t(b));
+          mbar_wait_addr(b_empty0 + 8 * st, ph ^ 1u);
+          const uint8_t* src = b < n_hint ? hbase + size_t(b / kParts) * tile_bytes
+                                          : atiles + size_t(ba) * tile_bytes;
+          mbar_arrive_expect_tx_addr(b_full0 + 8 * st, copy_bytes);
+          bulk_g2s_addr(ring0 + st * C::kBBytes, src, copy_bytes, b_full0 + 8 * st, pol_b);
+          st += kParts;
+          if (st >= C::kStages) {
+            st -= C::kStages;
+            ph ^= 1u;
+          }
         }
-        __syncwarp();
-        if (b >= n_hint && ++ba == nB) ba = 0;
-        if (++st == C::kStages) {
-          st = 0;
-          ph ^= 1u;
-        }
-      }
-    }
-  } else if (PAIR && !leader && warp >= 1 && warp <= kParts) {
-    // ------------------------------------------------ PAIR odd CTA: relay "my half landed"
-    const int me = warp - 1;
-    const uint32_t bf_leader = mapa_shared(smem_u32(b_full), 0);
-    int st = me;
-    uint32_t ph = 0;
-    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
-      mbar_wait(b_full + st, ph);
-      if (lane == 0) mbar_arrive_remote(bf_leader + uint32_t(st * 8));
-      __syncwarp();
-      st += kParts;
-      if (st >= C::kStages) {
-        st -= C::kStages;
-        ph ^= 1u;
+        b -= T;
       }
     }
   } else if (warp >= 1 && warp <= kParts) {
@@ -1402,118 +1414,86 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     const int nks = SPLIT ? split_ksteps(dv.s) : mma_ksteps(dv.s);
     const uint32_t b_base = smem_u32(smem + C::kOffB);
     static_assert(C::kAcc == kParts, "issuer i always fills accumulator stage i");
-#ifdef CBB_NISS
-    constexpr int kIss = CBB_NISS;  // development: issuer warps (kParts % kIss == 0)
-#else
-    constexpr int kIss = kParts;
-#endif
-    static_assert(kParts % kIss == 0, "issuers share the stages evenly");
     int sacc = me;  // accumulator stage kk % kAcc
     uint32_t aphm = (1u << C::kAcc) - 1u;  // acc_free parity per stage: first use passes at once
     int tb = me;    // completion barrier kk % kTBars
-    int itk = -1;
-    uint32_t vt_end = 0;  // first tile index of the next voxel tile
     int st = me;
     uint32_t ph = 0;
-    for (uint32_t kk = uint32_t(me); me < kIss && kk < total; kk += kIss) {
-      if (kk >= vt_end) {  // first tile of this issuer in a new voxel tile: wait for its A
-        ++itk;
-        vt_end += uint32_t(T);
-        if constexpr (PAIR)
-          mbar_wait_cluster(a_full + (itk & 1), (itk >> 1) & 1);
-        else
-          mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
-      }
-      // operands of this tile's MMAs, computed before the waits (off the release -> MMA path)
-      const uint32_t a_tm = tbase + uint32_t(C::kAColOff + ((itk & 1) * C::kACols));
-      const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
-      uint64_t bdesc[KP / 16];
+    uint32_t kk = uint32_t(me), kbeg = 0;
+    for (int it = 0; it < my_vts; ++it) {
+      const uint32_t kend = kbeg + uint32_t(n_hint + unit_of(it).len);
+      // every issuer owns >= 1 tile of the unit (T >= kParts): wait for its A operand
+      mbar_wait(a_full + (it & 1), (it >> 1) & 1);
+      for (; kk < kend; kk += kParts) {
+        // operands of this tile's MMAs, computed before the waits (off the release -> MMA path)
+        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + ((it & 1) * C::kACols));
+        const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
+        uint64_t bdesc[KP / 16];
 #pragma unroll
-      for (int kq = 0; kq < KP / 16; ++kq)
-        // split: K blocks of 64 elements (128 B swizzled rows) follow each other, kBNloc rows
-        // each; fp16: no-swizzle core matrices, K step kq = chunks 2kq, 2kq + 1
-        bdesc[kq] = SPLIT ? umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * C::kBNloc * 128,
-                                             64) +
-                                uint64_t(2 * (kq & 3))
-                          : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
-      // the atom tile usually landed long before the accumulator stage is released: test it
-      // first, so the release -> MMA hop is a single barrier wait
-      const uint32_t apar = (aphm >> sacc) & 1u;  // this stage use's release phase
-      if constexpr (PAIR) {
-        mbar_wait_cluster(b_full + st, ph);
-        mbar_wait_cluster(acc_free + sacc, (aphm >> sacc) & 1u);
-      } else {
+        for (int kq = 0; kq < KP / 16; ++kq)
+          // split: K blocks of 64 elements (128 B swizzled rows) follow each other, BN rows
+          // each; fp16: no-swizzle core matrices, K step kq = chunks 2kq, 2kq + 1
+          bdesc[kq] = SPLIT ? umma_desc_kmajor(b_base + st * C::kBBytes + (kq >> 2) * BN * 128, 64) +
+                                  uint64_t(2 * (kq & 3))
+                            : umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
+        const bool last = kk + kParts >= kend;  // this issuer's last tile of the unit
+        // the atom tile usually landed long before the accumulator stage is released: test it
+        // first, so the release -> MMA hop is a single barrier wait
+        const uint32_t apar = (aphm >> sacc) & 1u;  // this stage use's release phase
         mbar_wait(b_full + st, ph);
-#ifdef CBB_SPIN_ISS
-        mbar_wait_spin(acc_free + sacc, (aphm >> sacc) & 1u);
-#else
-        mbar_wait(acc_free + sacc, (aphm >> sacc) & 1u);
-#endif
-      }
-      if (lane == 0) CBB_STAMP(4, kk);
-      aphm ^= 1u << sacc;
-      tc_fence_after();
-      if (lane == 0) CBB_STAMP(0, kk);
-      if constexpr (C::kHalves) {
-        // first half (atoms 0..63 of the tile -> columns 0..63), then, once the part has
-        // released the second half, atoms 64..127 -> columns 64..127 (B rows + 64 x 128 B)
-        constexpr uint32_t kIdH = idesc_f16_f32(128, 64);
-        if (elect_one()) {
-#pragma unroll
-          for (int kq = 0; kq < KP / 16; ++kq)
-            if (kq < nks)
-              tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], kIdH, kq > 0 ? 1u : 0u);
-          tc_commit(t_full + tb);
-        }
-        __syncwarp();
-        mbar_wait(acc_free2 + sacc, apar);
+        mbar_wait(acc_free + sacc, apar);
+        if (lane == 0) CBB_STAMP(4, kk);
+        aphm ^= 1u << sacc;
         tc_fence_after();
-        if (elect_one()) {
+        if (lane == 0) CBB_STAMP(0, kk);
+        if constexpr (C::kHalves) {
+          // first half (atoms 0..63 of the tile -> columns 0..63), then, once the part has
+          // released the second half, atoms 64..127 -> columns 64..127 (B rows + 64 x 128 B)
+          constexpr uint32_t kIdH = idesc_f16_f32(128, 64);
+          if (elect_one()) {
+#pragma unroll
+            for (int kq = 0; kq < KP / 16; ++kq)
+              if (kq < nks)
+                tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], kIdH, kq > 0 ? 1u : 0u);
+            tc_commit(t_full + tb);
+          }
+          __syncwarp();
+          mbar_wait(acc_free2 + sacc, apar);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kq = 0; kq < KP / 16; ++kq)
+              if (kq < nks)
+                tc_mma_f16_ts(d_tm + 64u, a_tm + uint32_t(kq * 8),
+                              bdesc[kq] + uint64_t((64 * 128) >> 4), kIdH, kq > 0 ? 1u : 0u);
+            CBB_STAMP(1, kk);
+            tc_commit(b_empty + st);
+            tc_commit(t_full2 + tb);
+            if (last) tc_commit(a_empty + (it & 1));
+          }
+        } else if (elect_one()) {
 #pragma unroll
           for (int kq = 0; kq < KP / 16; ++kq)
             if (kq < nks)
-              tc_mma_f16_ts(d_tm + 64u, a_tm + uint32_t(kq * 8),
-                            bdesc[kq] + uint64_t((64 * 128) >> 4), kIdH, kq > 0 ? 1u : 0u);
-          CBB_STAMP(1, kk);
-          tc_commit(b_empty + st);
-          tc_commit(t_full2 + tb);
-          if (kk + kIss >= vt_end)
-            for (int r = 0; r < kParts / kIss; ++r) tc_commit(a_empty + (itk & 1));
-        }
-      } else if (elect_one()) {
-#pragma unroll
-        for (int kq = 0; kq < KP / 16; ++kq) {
-          if (kq < nks) {
-            if constexpr (PAIR)
-              tc_mma_f16_ts2(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], C::kIdesc, kq > 0 ? 1u : 0u);
-            else
               tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bdesc[kq], C::kIdesc, kq > 0 ? 1u : 0u);
-          }
-        }
-        CBB_STAMP(1, kk);
-        if constexpr (PAIR) {  // both CTAs' barriers
-          tc_commit2_mc(b_empty + st, 3);
-          tc_commit2_mc(t_full + tb, 3);
-          if (kk + kIss >= vt_end)
-            for (int r = 0; r < kParts / kIss; ++r) tc_commit2_mc(a_empty + (itk & 1), 3);
-        } else {
+          CBB_STAMP(1, kk);
           tc_commit(b_empty + st);
           tc_commit(t_full + tb);
           // this issuer's last tile of the voxel tile: A buffer recyclable once it retires
-          if (kk + kIss >= vt_end)
-            for (int r = 0; r < kParts / kIss; ++r) tc_commit(a_empty + (itk & 1));
+          if (last) tc_commit(a_empty + (it & 1));
+        }
+        __syncwarp();
+        sacc += kParts;
+        if (sacc >= C::kAcc) sacc -= C::kAcc;
+        tb += kParts;
+        if (tb >= C::kTBars) tb -= C::kTBars;
+        st += kParts;
+        if (st >= C::kStages) {
+          st -= C::kStages;
+          ph ^= 1u;
         }
       }
-      __syncwarp();
-      sacc += kIss;
-      if (sacc >= C::kAcc) sacc -= C::kAcc;
-      tb += kIss;
-      if (tb >= C::kTBars) tb -= C::kTBars;
-      st += kIss;
-      if (st >= C::kStages) {
-        st -= C::kStages;
-        ph ^= 1u;
-      }
+      kbeg = kend;
     }
   } else if (warp >= C::kFirstEpiWarp) {
     // -------------------------------------------------- epilogue parts
@@ -1528,45 +1508,39 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
     const uint32_t t_lane = tbase + lane_off;
     const uint32_t t_stage = t_lane + uint32_t(part * C::kAccCols);  // fp16: stage == part
     uint32_t* pthr_row = reinterpret_cast<uint32_t*>(smem + C::kOffPthr) + row * 4;
-    // A-staged / stage-released signals go to the leader's barriers (PAIR odd CTA: remotely)
-    const uint32_t lead_delta =
-        (PAIR && !leader) ? mapa_shared(smem_u32(bars), 0) - smem_u32(bars) : 0u;
-    auto arrive_lead = [&](uint64_t* bar) {
-      if (PAIR && !leader)
-        mbar_arrive_remote(smem_u32(bar) + lead_delta);
-      else
-        mbar_arrive(bar);
-    };
 
     // ---- A for the first voxel tile
     if (part == 0 && my_vts > 0) {
-      const int64_t v0 = int64_t(int(blockIdx.x) / nsplit) * C::kVox + row;
+      const int64_t v0 = voxel_of(int(blockIdx.x) / nsplit, row);
       stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_lead(a_full + 0);
+      if (lane == 0) mbar_arrive(a_full + 0);
     }
 
     uint32_t kk = uint32_t(part);  // this part's next tile
     int sacc = part;               // its accumulator stage kk % kAcc
     int tb = part;                 // its completion barrier kk % kTBars, phase (kk / kTBars) & 1
     uint32_t ph = 0;
+    uint32_t kbeg = 0;
     for (int it = 0; it < my_vts; ++it) {
-      const int u = int(blockIdx.x) + it * int(gridDim.x);
-      const int vt = u / nsplit, hr = u - vt * nsplit;  // voxel tile, atom range
+      const Unit un = unit_of(it);
+      const int vt = un.vt, hr = un.hr;
       const int opart = hr * kParts + part;  // output lists of (atom range, part)
-      const int64_t v = int64_t(vt) * C::kVox + row;
+      const int64_t v = voxel_of(vt, row);
       const bool live = v < n;
+      const int T = n_hint + un.len;
+      const uint16_t* lst = PRUNE ? plist + size_t(vt) * plist_stride + un.lo : nullptr;
       // ---- stage the NEXT voxel tile's rows into the other A buffer (one tile ahead)
       if (part == 0 && it + 1 < my_vts) {
         const int nbuf = (it + 1) & 1;
         mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
-        const int64_t vn = int64_t((u + int(gridDim.x)) / nsplit) * C::kVox + row;
+        const int64_t vn = voxel_of((int(blockIdx.x) + (it + 1) * int(gridDim.x)) / nsplit, row);
         stage_voxel_row<KP>(zrows, vn, vn < n, a_lane + uint32_t(nbuf * C::kACols));
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_lead(a_full + nbuf);
+        if (lane == 0) mbar_arrive(a_full + nbuf);
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(0, it);
       const float win = live ? win_tc[v] : -1.f;
@@ -1581,7 +1555,69 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
       // split mode: fp32 running max / threshold (thresholds rounded down)
       float runmax_f = active ? init_tc[v] : -INFINITY;
       float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
-      const uint32_t kbeg = uint32_t(it) * uint32_t(T), kend = kbeg + uint32_t(T);
+      const uint32_t kend = kbeg + uint32_t(T);
+      if constexpr (BOUND) {
+        // per (voxel, centroid): need = fl(zn r + s~) >= lb - margin; a warp ORs its lanes' bits
+        // (the tile's 32-centroid words) into the voxel tile's global need mask
+        const float2 lz = live ? lbz[v] : make_float2(INFINITY, 0.f);
+        uint32_t* vbits = bnd_bits + size_t(vt) * bnd_words;
+        for (; kk < kend; kk += kParts) {
+          const int ba = int(kk - kbeg);  // centroid tile
+          mbar_wait(t_full + tb, ph);
+          tc_fence_after();
+          constexpr int kRegChunks = C::kChunks < 2 ? C::kChunks : 2;
+          uint32_t r[32 * kRegChunks];
+          __syncwarp();
+          const uint32_t ta = t_lane + sacc * uint32_t(C::kAccCols);
+#pragma unroll
+          for (int h = 0; h < C::kChunks / kRegChunks; ++h) {
+            if (C::kHalves && h == 1) {
+              mbar_wait(t_full2 + tb, ph);
+              tc_fence_after();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < kRegChunks; ++c)
+              tmem_ld32_f32(ta + uint32_t(32 * (h * kRegChunks + c)),
+                            *reinterpret_cast<uint32_t(*)[32]>(r + 32 * c));
+            tc_wait_ld();
+            if (C::kHalves || h + 1 == C::kChunks / kRegChunks) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0)
+                mbar_arrive(C::kHalves && h == 1 ? acc_free2 + part : acc_free + part);
+            }
+            const int col0 = ba * BN + 32 * kRegChunks * h;
+            const float4* rs4 = reinterpret_cast<const float4*>(bnd_rs + col0);
+#pragma unroll
+            for (int c = 0; c < kRegChunks; ++c) {
+              uint32_t wbits = 0;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const float4 rr = __ldg(rs4 + (32 * c + i) / 4);
+                wbits |= (fmaf(lz.y, rr.x, __uint_as_float(r[32 * c + i])) >= lz.x ? 1u : 0u) << i;
+                wbits |= (fmaf(lz.y, rr.y, __uint_as_float(r[32 * c + i + 1])) >= lz.x ? 1u : 0u)
+                         << (i + 1);
+                wbits |= (fmaf(lz.y, rr.z, __uint_as_float(r[32 * c + i + 2])) >= lz.x ? 1u : 0u)
+                         << (i + 2);
+                wbits |= (fmaf(lz.y, rr.w, __uint_as_float(r[32 * c + i + 3])) >= lz.x ? 1u : 0u)
+                         << (i + 3);
+              }
+              wbits = __reduce_or_sync(0xffffffffu, wbits);
+              if (lane == 0 && wbits) atomicOr(vbits + (col0 >> 5) + c, wbits);
+            }
+          }
+          sacc += kParts;
+          if (sacc >= C::kAcc) sacc -= C::kAcc;
+          tb += kParts;
+          if (tb >= C::kTBars) {
+            tb -= C::kTBars;
+            ph ^= 1u;
+          }
+        }
+        kbeg = kend;
+        continue;
+      }
       if constexpr (!C::kF32) {
         // fp16 screen: the part owns accumulator stage `part` and completion barrier `part`
         // (kAcc == kTBars == kParts), whose phase flips every tile.  The three parts publish
@@ -1595,11 +1631,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         uint32_t r[16 * C::kChunks];
         auto consume = [&]() {
           if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-#ifdef CBB_SPIN_EPI
-          mbar_wait_spin(t_full + part, ph);
-#else
           mbar_wait(t_full + part, ph);
-#endif
           tc_fence_after();
           if (q == 0 && lane == 0) CBB_STAMP(2, kk);
           __syncwarp();
@@ -1614,7 +1646,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           // early release: the stage may be overwritten by tile kk + kAcc while we screen
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) arrive_lead(acc_free + part);
+          if (lane == 0) mbar_arrive(acc_free + part);
           if (q == 0 && lane == 0) CBB_STAMP(3, kk);
           ph ^= 1u;
         };
@@ -1636,25 +1668,24 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           const uint4 w = lds_v4_volatile(pthr_row);
           consume();
           thr = __hmax(thr, shared_thr(w, tag));
-#if defined(CBB_EPI_EMPTY)  // development timing variants (wrong results)
-          if (r[0] == 0x7fff7fffu) runmax = __hmax(runmax, as_h2(r[1]).x);
-#elif defined(CBB_EPI_NOSLOW)
-          if (__hge(tile_max_f16<C::kChunks>(r), __ushort_as_half(0x7C00))) runmax = thr;
-#else
           screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl, my_pub, tag);
-#endif
           if (q == 0 && lane == 0) CBB_STAMP(6, kk);
           ba += kParts;
           if (ba >= bend) ba -= nBh;
         }
       } else {
-        // split / HI32 screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles
-        // are screened in halves and released after the last half is loaded
+        // split screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles are
+        // screened in halves and released after the last half is loaded
         for (; kk < kend; kk += kParts) {
           const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
-          int ba = rot + qt;                       // range tile (rot + qt) % nBh
-          if (ba >= nBh) ba -= nBh;
-          ba += hr * nBh;
+          int ba;
+          if constexpr (PRUNE) {
+            ba = qt >= 0 ? int(lst[qt]) : 0;       // loaded before the wait
+          } else {
+            ba = rot + qt;                         // range tile (rot + qt) % nBh
+            if (ba >= nBh) ba -= nBh;
+            ba += hr * nBh;
+          }
           if (q == 0 && lane == 0) CBB_STAMP(5, kk);
           mbar_wait(t_full + tb, ph);
           tc_fence_after();
@@ -1683,7 +1714,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
             } else if (h + 1 == C::kChunks / kRegChunks) {
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) arrive_lead(acc_free + part);
+              if (lane == 0) mbar_arrive(acc_free + part);
               if (q == 0 && lane == 0) CBB_STAMP(3, kk);
             }
             if (qt >= 0)
@@ -1703,6 +1734,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
           }
         }
       }
+      kbeg = kend;
       // ---- hand-off (no inter-part barrier): this part's surviving chunk entries are appended
       // to its global list (after any spills); count and running max go to meta.
       // rescore_kernel merges the parts and rescans the flagged groups in fp64
@@ -1713,298 +1745,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT, PAIR, HI32>::kThreads, 1)
         meta[int64_t(opart) * n_pad + v] = make_int2(total, __float_as_int(rm));
       }
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(2, it);
-    }
-  }
-  __syncthreads();
-  if constexpr (PAIR) cluster_sync_all();  // no peer arrives on this CTA's barriers any more
-  if (warp == 1) {
-    tc_fence_after();
-    if constexpr (PAIR)
-      tmem_dealloc2(tbase, 512);
-    else
-      tmem_dealloc(tbase, 512);
-  }
-}
-
-// ============================================================== dual-voxel-tile fp16 screen
-// Measured on cfg1 (1x B200): mf_tc_kernel's skeleton alone (epilogue reduced to wait + load +
-// release) takes 6.5 of its 8.4 ms and 4.5 ms without the atom stream -- the L2 -> SMEM copy of
-// every atom tile for every 128-voxel tile (68.7 GB per projection, ~9 TB/s) is the limiter.
-// This kernel screens TWO voxel tiles (256 voxels) against each streamed 64-atom tile: per tile
-// the issuer runs 2 x ksteps MMAs (M = 128, N = 64, one per voxel tile, A from TMEM) reading the
-// same SMEM stage, so the atom stream per (voxel, atom) pair halves.  Each epilogue thread owns
-// one row of both voxel tiles.  TMEM: 3 stages x [vt0 | vt1] x 64 fp16 accumulator columns + the
-// A double buffer 2 x [vt0 | vt1] x KP/2 = 448 (KP 32) / 512 (KP 64) columns.  Barriers, parts,
-// records, published thresholds and the hand-off are mf_tc_kernel's (fp16 path).
-template <int KP>
-struct TcDual {
-  static constexpr int BN = 64;
-  static constexpr int kChunks = 2;
-  static constexpr int kACols = KP / 2;         // one voxel tile's A columns
-  static constexpr int kABuf = 2 * kACols;      // one A buffer: [vt0 | vt1]
-  static constexpr int kAcc = 3;
-  static constexpr int kAccCols = 2 * BN;       // one stage: [vt0 scores | vt1 scores]
-  static constexpr int kAColOff = kAcc * kAccCols;
-  static_assert(kAColOff + 2 * kABuf <= 512, "TMEM budget");
-  static constexpr int kBBytes = BN * KP * 2;
-  static constexpr int kRing = 72 * 1024;
-  static constexpr int kStagesRaw = kRing / kBBytes > 24 ? 24 : kRing / kBBytes;
-  static constexpr int kStages = (kStagesRaw / kParts) * kParts;
-  static_assert(kStages >= 2 * kAcc, "B ring too shallow");
-  static constexpr int kEpiWarps = 4 * kParts;
-  static constexpr int kFirstEpiWarp = 1 + kParts;
-  static constexpr int kThreads = (kFirstEpiWarp + kEpiWarps) * 32;
-  static constexpr int kVox = 128;
-  static constexpr int kSlots = kVox * kParts * 2;
-  static constexpr int kOffB = 0;
-  static constexpr int kOffCj = kOffB + kStages * kBBytes;
-  static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
-  static constexpr int kOffPthr = kOffCs + kCandCap * kSlots * 4;  // [2][kVox][4] u32
-  static constexpr int kOffBar = kOffPthr + 2 * kVox * 16;
-  static constexpr int kNumBars = 4 + 2 * kStages + kAcc;
-  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
-  static constexpr int kSmem = kOffTmem + 16 + 1024;
-  static_assert(kSmem <= 227 * 1024, "shared memory");
-  static constexpr uint32_t kIdesc = idesc_f16_f16(128, BN);
-};
-
-template <int KP>
-__global__ void __launch_bounds__(TcDual<KP>::kThreads, 1)
-    mf_tc_dual_kernel(const uint8_t* __restrict__ zrows, int64_t n, int n_vt,
-                      const float* __restrict__ win_tc, const float* __restrict__ init_tc,
-                      DictView dv, int64_t n_pad, int2* __restrict__ cand,
-                      int2* __restrict__ meta, const uint8_t* __restrict__ hint_tiles,
-                      int n_hint) {
-  using C = TcDual<KP>;
-  constexpr int BN = C::BN;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024_smem(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 2;
-  uint64_t* b_full = bars + 4;
-  uint64_t* b_empty = b_full + C::kStages;
-  uint64_t* t_full = b_empty + C::kStages;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t d = dv.d;
-  const int nB = int((d + BN - 1) / BN);
-  const int n_pt = (n_vt + 1) / 2;  // voxel-tile pairs (256 voxels)
-  const int rot = int((int64_t(blockIdx.x) * nB) / gridDim.x);
-  const int my_pts = (n_pt - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
-  const int T = nB + n_hint;
-  const uint32_t total = uint32_t(my_pts) * uint32_t(T);
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(a_full + i, 4);
-      mbar_init(a_empty + i, kParts);
-    }
-    for (int i = 0; i < C::kAcc; ++i) mbar_init(t_full + i, 1);
-    for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(b_full + i, 1 + 4);
-      mbar_init(b_empty + i, 1);
-    }
-    for (int i = 0; i < C::kAcc; ++i)
-      for (int w = 0; w < 4; ++w) mbar_arrive(b_full + i);
-    mbar_fence_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_holder, 512);
-  for (int i = threadIdx.x; i < 2 * 4 * C::kVox; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(smem + C::kOffPthr)[i] = 0xFFFFFC00u;
-  for (int i = threadIdx.x; i < C::kStages * C::kBBytes / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(smem + C::kOffB)[i] = make_uint4(0, 0, 0, 0);  // finite tails
-  fence_proxy_async_smem();
-  const int nc = tc_nc(dv.s);
-  const uint32_t tile_bytes = uint32_t(BN * nc * 16);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_holder;
-
-  if (warp == 0) {
-    // ------------------------------------------------ producer (bulk copies of atom tiles)
-    const uint64_t pol_b = policy_evict_last();
-    int st = 0;
-    uint32_t ph = 0;
-    for (int it = 0; it < my_pts; ++it) {
-      const int pt = int(blockIdx.x) + it * int(gridDim.x);
-      int ba = rot;
-      for (int b = 0; b < T; ++b) {
-        mbar_wait(b_empty + st, ph ^ 1u);
-        if (elect_one()) {
-          const uint8_t* src =
-              b < n_hint ? hint_tiles + (size_t(pt) * (n_hint / kParts) + b / kParts) * tile_bytes
-                         : dv.atoms_tc + size_t(ba) * tile_bytes;
-          mbar_arrive_expect_tx(b_full + st, tile_bytes);
-          bulk_g2s(smem + C::kOffB + st * C::kBBytes, src, tile_bytes, b_full + st, pol_b);
-        }
-        __syncwarp();
-        if (b >= n_hint && ++ba == nB) ba = 0;
-        if (++st == C::kStages) {
-          st = 0;
-          ph ^= 1u;
-        }
-      }
-    }
-  } else if (warp >= 1 && warp <= kParts) {
-    // ------------------------------------------------ MMA issuers: 2 voxel tiles per atom tile
-    const int me = warp - 1;
-    const int nks = mma_ksteps(dv.s);
-    const uint32_t b_base = smem_u32(smem + C::kOffB);
-    int sacc = me;
-    int itk = -1;
-    uint32_t vt_end = 0;
-    int st = me;
-    uint32_t ph = 0;
-    for (uint32_t kk = uint32_t(me); kk < total; kk += kParts) {
-      if (kk >= vt_end) {
-        ++itk;
-        vt_end += uint32_t(T);
-        mbar_wait(a_full + (itk & 1), (itk >> 1) & 1);
-      }
-      mbar_wait(b_full + st, ph);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a_tm = tbase + uint32_t(C::kAColOff + (itk & 1) * C::kABuf);
-        const uint32_t d_tm = tbase + uint32_t(sacc * C::kAccCols);
-#pragma unroll
-        for (int kq = 0; kq < KP / 16; ++kq) {
-          const uint64_t bdesc =
-              umma_desc_interleave(b_base + st * C::kBBytes + kq * 256, 128, nc * 128);
-          if (kq < nks) {
-#pragma unroll
-            for (int vv = 0; vv < 2; ++vv)
-              tc_mma_f16_ts(d_tm + uint32_t(vv * BN), a_tm + uint32_t(vv * C::kACols + kq * 8),
-                            bdesc, C::kIdesc, kq > 0 ? 1u : 0u);
-          }
-        }
-        tc_commit(b_empty + st);
-        tc_commit(t_full + sacc);
-        if (kk + kParts >= vt_end) tc_commit(a_empty + (itk & 1));
-      }
-      __syncwarp();
-      st += kParts;
-      if (st >= C::kStages) {
-        st -= C::kStages;
-        ph ^= 1u;
-      }
-    }
-  } else if (warp >= C::kFirstEpiWarp) {
-    // -------------------------------------------------- epilogue parts (one row of each tile)
-    const int e = warp - C::kFirstEpiWarp;
-    const int part = e >> 2, q = warp & 3;
-    const int row = q * 32 + lane;
-    int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
-    float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
-    const uint32_t lane_off = uint32_t(q * 32) << 16;
-    const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
-    const uint32_t t_stage = tbase + lane_off + uint32_t(part * C::kAccCols);
-    uint32_t* pthr0 = reinterpret_cast<uint32_t*>(smem + C::kOffPthr) + row * 4;
-    uint32_t* pthr1 = pthr0 + C::kVox * 4;
-
-    if (part == 0 && my_pts > 0) {
-      const int64_t v0 = int64_t(blockIdx.x) * 2 * C::kVox + row;
-      stage_voxel_row<KP>(zrows, v0, v0 < n, a_lane);
-      stage_voxel_row<KP>(zrows, v0 + C::kVox, v0 + C::kVox < n, a_lane + uint32_t(C::kACols));
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + 0);
-    }
-
-    uint32_t kk = uint32_t(part);
-    uint32_t ph = 0;
-    int rel = part + C::kAcc;
-    uint32_t r[32 * 2];
-    for (int it = 0; it < my_pts; ++it) {
-      const int pt = int(blockIdx.x) + it * int(gridDim.x);
-      const int64_t v0 = int64_t(pt) * 2 * C::kVox + row, v1 = v0 + C::kVox;
-      const bool live0 = v0 < n, live1 = v1 < n;
-      if (part == 0 && it + 1 < my_pts) {
-        const int nbuf = (it + 1) & 1;
-        mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const int64_t vn = int64_t(pt + int(gridDim.x)) * 2 * C::kVox + row;
-        const uint32_t ab = a_lane + uint32_t(nbuf * C::kABuf);
-        stage_voxel_row<KP>(zrows, vn, vn < n, ab);
-        stage_voxel_row<KP>(zrows, vn + C::kVox, vn + C::kVox < n, ab + uint32_t(C::kACols));
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(a_full + nbuf);
-      }
-      const float win0 = live0 ? win_tc[v0] : -1.f, win1 = live1 ? win_tc[v1] : -1.f;
-      bool active0 = live0 && win0 >= 0.f, active1 = live1 && win1 >= 0.f;
-      const int slot0 = (part * 2) * C::kVox + row, slot1 = slot0 + C::kVox;
-      HCandList cl0{cj_base + slot0, cs_base + slot0, C::kSlots, 0,
-                    cand + int64_t(part) * kGCap * n_pad + (live0 ? v0 : 0), n_pad, 0, false};
-      HCandList cl1{cj_base + slot1, cs_base + slot1, C::kSlots, 0,
-                    cand + int64_t(part) * kGCap * n_pad + (live1 ? v1 : 0), n_pad, 0, false};
-      __half runmax0 = active0 ? __float2half_rd(fmaxf(init_tc[v0], -65504.f))
-                               : __ushort_as_half(0xFC00);
-      __half runmax1 = active1 ? __float2half_rd(fmaxf(init_tc[v1], -65504.f))
-                               : __ushort_as_half(0xFC00);
-      __half thr0 = __ushort_as_half(0x7C00), thr1 = __ushort_as_half(0x7C00);
-      const uint32_t tag = (uint32_t(it) & 0xffffu) << 16;
-      const uint32_t kbeg = uint32_t(it) * uint32_t(T), khint = kbeg + uint32_t(n_hint),
-                     kend = kbeg + uint32_t(T);
-      auto consume = [&]() {
-        mbar_wait(t_full + part, ph);
-        tc_fence_after();
-        __syncwarp();
-        tmem_ld32_pack16(t_stage, *reinterpret_cast<uint32_t(*)[32]>(r));
-        tmem_ld32_pack16(t_stage + uint32_t(BN), *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        tc_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_full + rel);
-        ph ^= 1u;
-        rel += kParts;
-        if (rel >= C::kStages) rel -= C::kStages;
-      };
-      for (; kk < khint; kk += kParts) {  // warm-start hint tiles
-        consume();
-        if (active0)
-          runmax0 = __hmax(runmax0, tile_max_f16<2>(*reinterpret_cast<uint32_t(*)[32]>(r)));
-        if (active1)
-          runmax1 = __hmax(runmax1, tile_max_f16<2>(*reinterpret_cast<uint32_t(*)[32]>(r + 32)));
-      }
-      if (active0) {
-        thr0 = __float2half_rd(__half2float(runmax0) - win0);
-        pthr0[part] = tag | __half_as_ushort(thr0);
-      }
-      if (active1) {
-        thr1 = __float2half_rd(__half2float(runmax1) - win1);
-        pthr1[part] = tag | __half_as_ushort(thr1);
-      }
-      int ba = rot + int(kk - khint);
-      if (ba >= nB) ba -= nB;
-      for (; kk < kend; kk += kParts) {
-        const uint4 w0 = lds_v4_volatile(pthr0), w1 = lds_v4_volatile(pthr1);
-        consume();
-        thr0 = __hmax(thr0, shared_thr(w0, tag));
-        thr1 = __hmax(thr1, shared_thr(w1, tag));
-#if defined(CBB_EPI_EMPTY)  // development timing variant (wrong results)
-        if (r[0] == 0x7fff7fffu) runmax0 = __hmax(runmax0, as_h2(r[33]).x);
-#else
-        screen_tile<2>(*reinterpret_cast<uint32_t(*)[32]>(r), int64_t(ba) * BN, win0, runmax0,
-                       thr0, active0, cl0, pthr0 + part, tag);
-        screen_tile<2>(*reinterpret_cast<uint32_t(*)[32]>(r + 32), int64_t(ba) * BN, win1,
-                       runmax1, thr1, active1, cl1, pthr1 + part, tag);
-#endif
-        ba += kParts;
-        if (ba >= nB) ba -= nB;
-      }
-      if (live0) {
-        const float rm = __half2float(runmax0);
-        meta[int64_t(part) * n_pad + v0] =
-            make_int2((win0 >= 0.f) ? cl0.finish(rm - win0) : 0, __float_as_int(rm));
-      }
-      if (live1) {
-        const float rm = __half2float(runmax1);
-        meta[int64_t(part) * n_pad + v1] =
-            make_int2((win1 >= 0.f) ? cl1.finish(rm - win1) : 0, __float_as_int(rm));
-      }
     }
   }
   __syncthreads();
@@ -2030,9 +1770,12 @@ constexpr int kWarpAtoms = 32 * 32;  // per-warp atom list: one round of 32 chun
 constexpr int kLaneSurv = 16;        // per-lane fp32-window survivors (atom, fp32 score)
 
 // Expand one chunk entry and rescore its flagged atoms (chunk mask: 6-atom groups).
+// amap (split screen of a reordered dictionary): record positions -> atom indices (padded
+// positions map to d); ties compare the atom indices.
 template <int S>
 __device__ __forceinline__ void rescore_entry(int2 en, const double* zr, const double* zi,
-                                              int s, const DictView& dv, int64_t& best,
+                                              int s, const DictView& dv,
+                                              const int32_t* __restrict__ amap, int64_t& best,
                                               double& bs) {
   const int64_t j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
   uint32_t mask = uint32_t(en.x) >> kChunkShift;
@@ -2041,8 +1784,11 @@ __device__ __forceinline__ void rescore_entry(int2 en, const double* zr, const d
     mask &= mask - 1;
     const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
     for (int i = lo; i < hi; ++i) {
-      const int64_t j = j0 + i;
-      if (j >= dv.d) break;
+      const int64_t j = amap ? int64_t(amap[j0 + i]) : j0 + i;
+      if (j >= dv.d) {
+        if (amap) continue;
+        break;
+      }
       const double acc = dot_atom<S>(zr, zi, dv.atoms64 + j * s, s);
       if (acc > bs || (acc == bs && j < best)) {
         bs = acc;
@@ -2058,7 +1804,8 @@ template <int S, int NP = kParts>
 __global__ void __launch_bounds__(256) rescore_fast_kernel(
     ZSource zs, DictView dv, int64_t n, int64_t n_pad, const float* __restrict__ win_tc,
     const int2* __restrict__ cand, const int2* __restrict__ meta, ProjOut out, int* ovf_count,
-    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list, int fast_entries, int nparts) {
+    int64_t* ovf_list, int* heavy_count, int64_t* heavy_list, int fast_entries, int nparts,
+    const int32_t* __restrict__ amap) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const float win = win_tc[v];
@@ -2112,7 +1859,7 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
   for (int p = 0; p < NP; ++p)
     for (int c = 0; p < nparts && c < cnt[p]; ++c) {
       const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
-      if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zr, zi, s, dv, best, bs);
+      if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zr, zi, s, dv, amap, best, bs);
     }
   if (best == INT64_MAX) {
     ovf_list[atomicAdd(ovf_count, 1)] = v;
@@ -2141,7 +1888,8 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     ZSource zs, DictView dv, int64_t n_pad, const float* __restrict__ win_tc,
     const float* __restrict__ win32, const int2* __restrict__ cand,
     const int2* __restrict__ meta, ProjOut out, int* ovf_count, int64_t* ovf_list,
-    const int* heavy_count, const int64_t* heavy_list, int nparts) {
+    const int* heavy_count, const int64_t* heavy_list, int nparts,
+    const int32_t* __restrict__ amap) {
   // shared per warp: z (2s doubles), z (2s floats), the atom list, the lanes' fp32 survivors
   extern __shared__ double zsh_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2234,7 +1982,7 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
         const int b = __ffs(mask) - 1;
         mask &= mask - 1;
         const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
-        for (int i = lo; i < hi; ++i) alist[off++] = int(j0 + i);
+        for (int i = lo; i < hi; ++i) alist[off++] = amap ? amap[j0 + i] : int(j0 + i);
       }
       __syncwarp();
       for (int a = lane; a < round_total; a += 32) {
@@ -2279,7 +2027,8 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
           int p, c;
           entry_part(e, cnt, p, c);
           const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
-          if (__int_as_float(en.y) >= thr) rescore_entry<S>(en, zsh, zsh + s, s, dv, best, bs);
+          if (__int_as_float(en.y) >= thr)
+            rescore_entry<S>(en, zsh, zsh + s, s, dv, amap, best, bs);
         }
       }
     }
@@ -2439,50 +2188,218 @@ static int s_pad_for(int s) {
   return -1;
 }
 
-size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc, size_t* offb,
-                  size_t* offtc2) {
+// Storage layout of a prepared dictionary.
+struct DictLayout {
+  size_t a64, a32, tc, bounds, tc2, perm, pos, tile_c, tile_r, ctr_tc2, tile_rs, total;
+  int64_t d_pad;   // rows of the tile copies (whole tiles + sentinel tiles)
+  int n_tiles2, ctr_rows;  // split tiles; rows of the centroid split tiles
+};
+
+static DictLayout dict_layout(int64_t d, int s) {
+  DictLayout L{};
   const int sp = s_pad_for(s) > 0 ? s_pad_for(s) : s;
   const int kp = kpad_for(s);
   const int64_t nbt = (d + kTileRows - 1) / kTileRows;
+  L.d_pad = (nbt + kPadTiles) * kTileRows;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t r = o;
     o += (bytes + 255) & ~size_t(255);
     return r;
   };
-  size_t a = take(size_t(d) * s * 16);
-  size_t b = take(size_t(d) * 2 * sp * 4);
-  // + two extra 128-row sentinel tiles: the screening reads BN-row (BN <= 256) windows that
-  // may run past the last 128-row tile
-  size_t c = take(size_t(nbt + kPadTiles) * kTileRows * kp * 2);
-  size_t e = take(kBCount * sizeof(float));
-  size_t f = take(s <= kSplitMaxS ? size_t(nbt + kPadTiles) * kTileRows * split_kp(s) * 2 : 0);
-  if (offtc2) *offtc2 = f;
-  if (off64) *off64 = a;
-  if (off32) *off32 = b;
-  if (offtc) *offtc = c;
-  if (offb) *offb = e;
-  return o;
+  L.a64 = take(size_t(d) * s * 16);
+  L.a32 = take(size_t(d) * 2 * sp * 4);
+  // + sentinel tiles: the screening reads BN-row (BN <= 256) windows that may run past the last
+  // 128-row tile
+  L.tc = take(size_t(L.d_pad) * kp * 2);
+  L.bounds = take(kBCount * sizeof(float));
+  const bool sp2 = s <= kSplitMaxS;
+  L.tc2 = take(sp2 ? size_t(L.d_pad) * split_kp(s) * 2 : 0);
+  if (sp2) {
+    const int rows = split_rows(split_kp(s));
+    L.n_tiles2 = int((d + rows - 1) / rows);
+    // centroid split tiles: >= kParts whole tiles (the bound pass gives every part a tile)
+    const int ct = (L.n_tiles2 + rows - 1) / rows;
+    L.ctr_rows = (ct > kParts ? ct : kParts) * rows;
+    L.perm = take(size_t(L.d_pad) * 4);
+    L.pos = take(size_t(d) * 4);
+    L.tile_c = take(size_t(L.n_tiles2) * 2 * sp * 4);
+    L.tile_r = take(size_t(L.n_tiles2) * 4);
+    L.ctr_tc2 = take(size_t(L.ctr_rows) * split_kp(s) * 2);
+    L.tile_rs = take(size_t(L.ctr_rows) * 4);
+  }
+  L.total = o;
+  return L;
+}
+
+size_t dict_bytes(int64_t d, int s, size_t* off64, size_t* off32, size_t* offtc, size_t* offb,
+                  size_t* offtc2) {
+  const DictLayout L = dict_layout(d, s);
+  if (offtc2) *offtc2 = L.tc2;
+  if (off64) *off64 = L.a64;
+  if (off32) *off32 = L.a32;
+  if (offtc) *offtc = L.tc;
+  if (offb) *offb = L.bounds;
+  return L.total;
+}
+
+// Bisection order of the atoms (host, once per coherent dictionary): recursive split of the
+// real 2s-vectors [re, im] at the median of their projection on the principal direction (power
+// iteration), the left part a whole number of `leaf`-row tiles, so every split tile holds a
+// compact cluster of atoms (small radius -> effective pruning bounds).  Deterministic.
+static void bisection_order(const std::vector<double>& X, int64_t d, int dim, int leaf,
+                            std::vector<int32_t>& order) {
+  order.resize(size_t(d));
+  for (int64_t i = 0; i < d; ++i) order[size_t(i)] = int32_t(i);
+  std::vector<double> key(static_cast<size_t>(d), 0.0);
+  std::vector<double> mean(static_cast<size_t>(dim)), v(static_cast<size_t>(dim)),
+      w(static_cast<size_t>(dim));
+  std::vector<std::pair<int64_t, int64_t>> stack{{0, d}};
+  while (!stack.empty()) {
+    const int64_t lo = stack.back().first, hi = stack.back().second;
+    stack.pop_back();
+    const int64_t n = hi - lo;
+    if (n <= leaf) continue;
+    std::fill(mean.begin(), mean.end(), 0.0);
+    for (int64_t i = lo; i < hi; ++i) {
+      const double* x = &X[size_t(order[size_t(i)]) * dim];
+      for (int k = 0; k < dim; ++k) mean[size_t(k)] += x[k];
+    }
+    for (int k = 0; k < dim; ++k) mean[size_t(k)] /= double(n);
+    // start: the row farthest from the mean
+    double far = -1.0;
+    int64_t jf = order[size_t(lo)];
+    for (int64_t i = lo; i < hi; ++i) {
+      const double* x = &X[size_t(order[size_t(i)]) * dim];
+      double q = 0.0;
+      for (int k = 0; k < dim; ++k) q += (x[k] - mean[size_t(k)]) * (x[k] - mean[size_t(k)]);
+      if (q > far) {
+        far = q;
+        jf = order[size_t(i)];
+      }
+    }
+    for (int k = 0; k < dim; ++k) v[size_t(k)] = X[size_t(jf) * dim + k] - mean[size_t(k)];
+    for (int iter = 0; iter < 6; ++iter) {
+      double nv = 0.0;
+      for (int k = 0; k < dim; ++k) nv += v[size_t(k)] * v[size_t(k)];
+      if (!(nv > 0.0)) break;
+      std::fill(w.begin(), w.end(), 0.0);
+      for (int64_t i = lo; i < hi; ++i) {
+        const double* x = &X[size_t(order[size_t(i)]) * dim];
+        double p = 0.0;
+        for (int k = 0; k < dim; ++k) p += (x[k] - mean[size_t(k)]) * v[size_t(k)];
+        for (int k = 0; k < dim; ++k) w[size_t(k)] += p * (x[k] - mean[size_t(k)]);
+      }
+      double nw = 0.0;
+      for (int k = 0; k < dim; ++k) nw += w[size_t(k)] * w[size_t(k)];
+      if (!(nw > 0.0)) break;
+      nw = 1.0 / std::sqrt(nw);
+      for (int k = 0; k < dim; ++k) v[size_t(k)] = w[size_t(k)] * nw;
+    }
+    for (int64_t i = lo; i < hi; ++i) {
+      const int32_t j = order[size_t(i)];
+      const double* x = &X[size_t(j) * dim];
+      double p = 0.0;
+      for (int k = 0; k < dim; ++k) p += (x[k] - mean[size_t(k)]) * v[size_t(k)];
+      key[size_t(j)] = p;
+    }
+    const int64_t half = ((n / leaf + 1) / 2) * leaf;  // 0 < half < n for n > leaf
+    std::nth_element(order.begin() + lo, order.begin() + lo + half, order.begin() + hi,
+                     [&](int32_t a, int32_t b) {
+                       return key[size_t(a)] < key[size_t(b)] ||
+                              (key[size_t(a)] == key[size_t(b)] && a < b);
+                     });
+    stack.push_back({lo + half, hi});
+    stack.push_back({lo, lo + half});
+  }
+}
+
+// Centroid (fp32, planar [re | im], zero-padded to s_pad) and radius (>= max ||d_j - c||, fp64
+// rounded up) of the atoms at split-tile rows [cl rows, (cl + 1) rows) (rows < d hold atoms
+// perm[row]).  One warp per cluster.
+template <int S>
+__global__ void __launch_bounds__(128) cluster_bounds_kernel(const double2* __restrict__ atoms64,
+                                                             int64_t d, int s, int sp,
+                                                             const int32_t* __restrict__ perm,
+                                                             int rows, int n_clusters,
+                                                             float* __restrict__ cen,
+                                                             float* __restrict__ rad) {
+  const int cl = int(blockIdx.x) * 4 + int(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (cl >= n_clusters) return;
+  const int64_t p0 = int64_t(cl) * rows, p1 = p0 + rows < d ? p0 + rows : d;
+  double sr[S], si[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) sr[k] = si[k] = 0.0;
+  int cnt = 0;
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
+    const double2* a = atoms64 + int64_t(perm[p]) * s;
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (k < s) {
+        const double2 x = a[k];
+        sr[k] += x.x;
+        si[k] += x.y;
+      }
+    ++cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      sr[k] += __shfl_xor_sync(0xffffffffu, sr[k], o);
+      si[k] += __shfl_xor_sync(0xffffffffu, si[k], o);
+    }
+  }
+  float cr[S], ci[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    cr[k] = (cnt > 0 && k < s) ? float(sr[k] / cnt) : 0.f;
+    ci[k] = (cnt > 0 && k < s) ? float(si[k] / cnt) : 0.f;
+  }
+  double r2 = 0.0;
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
+    const double2* a = atoms64 + int64_t(perm[p]) * s;
+    double q = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (k < s) {
+        const double2 x = a[k];
+        const double er = x.x - double(cr[k]), ei = x.y - double(ci[k]);
+        q += er * er + ei * ei;
+      }
+    r2 = fmax(r2, q);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+  if (lane == 0) {  // sp == S (dispatched on s_pad)
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      cen[size_t(cl) * 2 * sp + k] = cr[k];
+      cen[size_t(cl) * 2 * sp + sp + k] = ci[k];
+    }
+    rad[cl] = __double2float_ru(sqrt(r2) * (1.0 + 0x1p-40));
+  }
 }
 
 int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, DictView* view,
                  cudaStream_t st) {
   if (d <= 0 || s <= 0) return kErrArgument;
-  size_t o64, o32, otc, ob, otc2;
-  const size_t total = dict_bytes(d, s, &o64, &o32, &otc, &ob, &otc2);
+  const DictLayout L = dict_layout(d, s);
   uint8_t* base = static_cast<uint8_t*>(storage);
-  CBB_CUDA_TRY(cudaMemsetAsync(base, 0, total, st));
+  CBB_CUDA_TRY(cudaMemsetAsync(base, 0, L.total, st));
   DictView v{};
   v.d = d;
   v.s = s;
   v.s_pad = s_pad_for(s) > 0 ? s_pad_for(s) : s;
   v.kpad = kpad_for(s);
   v.n_btiles = int((d + kTileRows - 1) / kTileRows);
-  v.atoms64 = reinterpret_cast<double2*>(base + o64);
-  v.atoms32 = reinterpret_cast<float*>(base + o32);
-  v.atoms_tc = base + otc;
-  v.bounds = reinterpret_cast<float*>(base + ob);
-  v.atoms_tc2 = s <= kSplitMaxS ? base + otc2 : nullptr;
+  v.atoms64 = reinterpret_cast<double2*>(base + L.a64);
+  v.atoms32 = reinterpret_cast<float*>(base + L.a32);
+  v.atoms_tc = base + L.tc;
+  v.bounds = reinterpret_cast<float*>(base + L.bounds);
+  v.atoms_tc2 = s <= kSplitMaxS ? base + L.tc2 : nullptr;
+  v.n_tiles2 = L.n_tiles2;
   const int threads = 256;
   const int blocks = int((d + threads - 1) / threads);
   prep_dict_kernel<<<blocks, threads, 0, st>>>(atoms, in128, d, s, v.s_pad,
@@ -2492,9 +2409,8 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   CBB_CUDA_TRY(cudaGetLastError());
   count_launches(1);
   if (2 * s < 64) {  // tensor-core operand tiles (+ sentinel column)
-    const int64_t d_pad = int64_t(v.n_btiles + kPadTiles) * kTileRows;
-    prep_tc_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
-        v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc),
+    prep_tc_kernel<<<int((L.d_pad + threads - 1) / threads), threads, 0, st>>>(
+        v.atoms64, d, L.d_pad, s, const_cast<uint8_t*>(v.atoms_tc),
         const_cast<float*>(v.bounds));
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -2502,13 +2418,6 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
   if (v.s <= 32) {  // coherence estimate for the auto screen choice (planar fp32 copy)
     coherence_kernel<<<kCohSamples, 256, 0, st>>>(v.atoms32, d, s, v.s_pad,
                                                   const_cast<float*>(v.bounds));
-    CBB_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
-  }
-  if (v.atoms_tc2) {  // split-operand tiles (after prep_tc_kernel: it publishes scale_d)
-    const int64_t d_pad = int64_t(v.n_btiles + kPadTiles) * kTileRows;
-    prep_tc2_kernel<<<int((d_pad + threads - 1) / threads), threads, 0, st>>>(
-        v.atoms64, d, d_pad, s, const_cast<uint8_t*>(v.atoms_tc2), const_cast<float*>(v.bounds));
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
   }
@@ -2520,6 +2429,68 @@ int dict_prepare(const void* atoms, int in128, int64_t d, int s, void* storage, 
                                  cudaMemcpyDeviceToHost, st));
     CBB_CUDA_TRY(cudaStreamSynchronize(st));
     v.prefer_split = coh >= 1.0f ? 1 : 0;
+  }
+  const int rows2 = v.atoms_tc2 ? split_rows(split_kp(s)) : 0;
+  if (v.atoms_tc2 && v.prefer_split && v.n_tiles2 <= 65536) {
+    // coherent dictionary: bisection order of the split tiles (host) + pruning bounds
+    std::vector<double2> h(size_t(d) * s);
+    CBB_CUDA_TRY(cudaMemcpyAsync(h.data(), v.atoms64, h.size() * sizeof(double2),
+                                 cudaMemcpyDeviceToHost, st));
+    CBB_CUDA_TRY(cudaStreamSynchronize(st));
+    const int dim = 2 * s;
+    std::vector<double> X(size_t(d) * dim);
+    for (int64_t j = 0; j < d; ++j)
+      for (int k = 0; k < s; ++k) {
+        X[size_t(j) * dim + k] = h[size_t(j) * s + k].x;
+        X[size_t(j) * dim + s + k] = h[size_t(j) * s + k].y;
+      }
+    std::vector<int32_t> order;
+    bisection_order(X, d, dim, rows2, order);
+    std::vector<int32_t> perm(static_cast<size_t>(L.d_pad), int32_t(d));
+    std::vector<int32_t> pos(static_cast<size_t>(d));
+    for (int64_t p = 0; p < d; ++p) {
+      perm[size_t(p)] = order[size_t(p)];
+      pos[size_t(order[size_t(p)])] = int32_t(p);
+    }
+    int32_t* dperm = reinterpret_cast<int32_t*>(base + L.perm);
+    int32_t* dpos = reinterpret_cast<int32_t*>(base + L.pos);
+    CBB_CUDA_TRY(cudaMemcpyAsync(dperm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, st));
+    CBB_CUDA_TRY(cudaMemcpyAsync(dpos, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, st));
+    CBB_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors die at scope exit
+    v.tc2_atom = dperm;
+    v.tc2_pos = dpos;
+    v.tile_c = reinterpret_cast<float*>(base + L.tile_c);
+    v.tile_r = reinterpret_cast<float*>(base + L.tile_r);
+    v.ctr_tc2 = base + L.ctr_tc2;
+    v.tile_rs = reinterpret_cast<float*>(base + L.tile_rs);
+  }
+  if (v.atoms_tc2) {  // split-operand tiles (after prep_tc_kernel: it publishes scale_d)
+    prep_tc2_kernel<<<int((L.d_pad + threads - 1) / threads), threads, 0, st>>>(
+        v.atoms64, d, L.d_pad, s, v.tc2_atom, const_cast<uint8_t*>(v.atoms_tc2),
+        const_cast<float*>(v.bounds));
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+  }
+  if (v.tile_c) {
+    int rc = kOk;
+    CBB_DISPATCH_S(v.s_pad, {
+      if constexpr (S_ > 0) {
+        cluster_bounds_kernel<S_><<<(L.n_tiles2 + 3) / 4, 128, 0, st>>>(
+            v.atoms64, d, s, v.s_pad, v.tc2_atom, rows2, L.n_tiles2,
+            const_cast<float*>(v.tile_c), const_cast<float*>(v.tile_r));
+      } else {
+        rc = kErrUnsupported;
+      }
+      break;
+    });
+    if (rc) return rc;
+    CBB_CUDA_TRY(cudaGetLastError());
+    // the centroids as split-operand rows (the bound pass's B operand) + scaled radii
+    prep_ctr_kernel<<<int((L.ctr_rows + threads - 1) / threads), threads, 0, st>>>(
+        v.tile_c, v.tile_r, L.n_tiles2, L.ctr_rows, s, v.s_pad, v.bounds,
+        const_cast<uint8_t*>(v.ctr_tc2), const_cast<float*>(v.tile_rs));
+    CBB_CUDA_TRY(cudaGetLastError());
+    count_launches(2);
   }
   *view = v;
   return kOk;
@@ -2542,11 +2513,26 @@ struct ProjWs {
   uint8_t* hint_tiles;  // [voxel tile][hint tile] warm-start tiles (IPG)
   double* nd_v;
   double* partial;
+  // tile pruning (split screen with a warm-start hint; only when the workspace was sized for
+  // the dictionary, project_ws_bytes(..., prune_tiles > 0))
+  bool prune;
+  float2* lbz;          // [n] (hint score rounded down, ||z|| rounded up)
+  int32_t* pkeys;       // [n] sort keys (hint atom's split-tile position) and values (voxel)
+  int32_t* pkeys_out;
+  int32_t* pvals;
+  int32_t* vperm;       // [n] screen order: position -> voxel
+  void* sort_tmp;
+  size_t sort_tmp_bytes;
+  int* pcnt;            // [n_vt] listed atom tiles per voxel tile
+  uint16_t* plist;      // [n_vt][prune_tiles] ascending atom-tile lists
+  uint32_t* pbits;      // [n_vt][words] need bits of the bound pass
 };
 constexpr int kReduceBlocks = 256;
 constexpr int kVoxPad = 512;  // voxel tiles are padded to a multiple of the largest TC voxel tile
 
-size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
+// prune_tiles > 0 (the dictionary's split tile count, prune-capable dictionaries only) appends
+// the pruning buffers.
+size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr, int prune_tiles) {
   const int kp = s <= kSplitMaxS ? split_kp(s) : kpad_for(s);  // split rows are wider
   const int64_t n_vt = (n + kVoxPad - 1) / kVoxPad;
   size_t o = 0;
@@ -2581,30 +2567,80 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr) {
   }
   w.nd_v = reinterpret_cast<double*>(take(size_t(n) * 8));
   w.partial = reinterpret_cast<double*>(take(kReduceBlocks * 8));
+  w.prune = prune_tiles > 0 && n > 0 && n < (int64_t(1) << 31) && prune_tiles <= 65536;
+  if (w.prune) {
+    w.lbz = reinterpret_cast<float2*>(take(size_t(n) * 8));
+    w.pkeys = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+    w.pkeys_out = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+    w.pvals = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+    w.vperm = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, int(n), 0, 32);
+    w.sort_tmp_bytes = tb;
+    w.sort_tmp = take(tb);
+    const int64_t vt128 = (n + 127) / 128;
+    w.pcnt = reinterpret_cast<int*>(take(size_t(vt128) * 4));
+    w.plist = reinterpret_cast<uint16_t*>(take(size_t(vt128) * prune_tiles * 2));
+    w.pbits = reinterpret_cast<uint32_t*>(take(size_t(vt128) * ((prune_tiles + 31) / 32 + 4) * 4));
+  }
   if (ws) *ws = w;
   return o;
 }
 
-static int g_num_sms = 0;
+constexpr int kPruneMinTiles = 32;
+constexpr int64_t kPruneMinVoxels = 8192;
+
+// split tiles of a prune-capable dictionary (bisection-ordered, with tile bounds), else 0
+int prune_tiles_of(const DictView& dv) {
+  return (dv.tile_c != nullptr && dv.atoms_tc2 != nullptr) ? dv.n_tiles2 : 0;
+}
+
+// Per-device launch facts (a process may project on several GPUs): SM counts and the one-time
+// dynamic shared-memory opt-ins are keyed by the current device.
+constexpr int kMaxDevices = 64;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
 static int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static std::atomic<int> sms[kMaxDevices];
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return v;
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current device only: one
+// opt-in per (kernel, device), remembered in a per-kernel device bitmask.
+template <auto Kernel>
+static int ensure_smem_attr(int smem) {
+  static std::atomic<uint64_t> done{0};
+  const int dev = current_device();
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    CBB_CUDA_TRY(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  return kOk;
 }
 
 // Warm-start hint tiles: row r of voxel tile vt's hint block = a copy of the storage row of
-// atom hint[vt*128 + r] (the previous IPG winner of that voxel), in the screen's own tile
-// layout (vox voxels per tile group: 128, or 256 for a CTA pair); rows without a valid hint
-// (and rows >= vox of the last tile) copy the first padded
-// row (score -65504 for every voxel).  One thread per 16-byte chunk.
+// atom hint[v] (the previous IPG winner of voxel v = row r of the tile; vperm: screen order),
+// in the screen's own tile layout; apos maps an atom to its split-tile storage row (null:
+// identity).  Rows without a valid hint (and rows past n) copy the first padded row (score
+// -65504 for every voxel).  One thread per 16-byte chunk.
 __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restrict__ hint,
                                                          int64_t n, int64_t d, int n_vt, int vox,
                                                          const uint8_t* __restrict__ atiles,
                                                          int kp, int split, int bn, int nh,
+                                                         const int32_t* __restrict__ vperm,
+                                                         const int32_t* __restrict__ apos,
                                                          uint8_t* __restrict__ out) {
   // 16-byte chunks per row: split rows kp / 8; fp16 rows tc_nc(s), passed as kp = 8 * nc
   const int cpr = kp / 8;
@@ -2614,11 +2650,11 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
   const int vt = int(g / per_vt);
   const int rem = int(g - int64_t(vt) * per_vt);
   const int r = rem / cpr, c = rem - r * cpr;
-  const int64_t v = int64_t(vt) * vox + r;
+  const int64_t p = int64_t(vt) * vox + r;
   int64_t j = d;
-  if (r < vox && v < n) {
-    const int64_t h = hint[v];
-    if (h >= 0 && h < d) j = h;
+  if (r < vox && p < n) {
+    const int64_t h = hint[vperm ? int64_t(vperm[p]) : p];
+    if (h >= 0 && h < d) j = apos ? int64_t(apos[h]) : h;
   }
   size_t src, dst;
   const int hb = r / bn, rr = r - hb * bn;
@@ -2633,144 +2669,157 @@ __global__ void __launch_bounds__(256) hint_tiles_kernel(const int32_t* __restri
   *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(atiles + src);
 }
 
-template <class C>
-constexpr int BN_of() { return C::BN; }
-
-// CTA pairs for the matched-filter screen (cta_group::2, see TcCfg): opt-in with CBB_TC_PAIR=1.
-// Measured on cfg1 (1x B200): 19.1 ms vs 8.4 ms for single CTAs -- the odd CTA's remote stage
-// releases lengthen the refill chain of every accumulator stage (release -> issuer 445 -> 1255
-// clk) by more than the halved atom stream saves.
-static bool tc_pair_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CBB_TC_PAIR");
-    v = (e && atoi(e) == 1) ? 1 : 0;
-  }
-  return v != 0;
-}
-template <class K>
-static int max_coresident_pairs(K kernel, int threads, int smem) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(256u);
-  cfg.blockDim = dim3(unsigned(threads));
-  cfg.dynamicSmemBytes = size_t(smem);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int nc = 0;
-  if (cudaOccupancyMaxActiveClusters(&nc, kernel, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return nc;
+// ------------------------------------------------------------ tile pruning (split screen, IPG)
+// Split tile t (rows [t BN, (t+1) BN) of the bisection-ordered split tiles) has an fp32 centroid
+// c_t and a radius r_t >= max_j ||d_j - c_t||.  Cauchy-Schwarz: Re<z, d_j> <= Re<z, c_t> + ||z|| r_t
+// for every atom of the tile.  The voxel's lower bound lb is its hint atom's exact fp64 score
+// (<= its maximum), so a tile with Re<z, c_t> + ||z|| r_t < lb holds neither the voxel's argmax
+// nor a tie, and a voxel tile screens only the atom tiles some voxel of it may need.
+//
+// (1) Screen order: voxels sorted (stable) by (bucket of lb / (||z|| dmax), split-tile position of
+//     the hint atom): voxel tiles gather voxels whose answers lie in the same region of the
+//     dictionary and whose bounds are equally tight (few weak-bound voxels spoil a tile).
+// (2) The bound pass (mf_tc_kernel<.., BOUND>): the centroids as split tiles on the tensor cores,
+//     s~ = scale_v scale_d Re<z~, c~> with |s~ - scale_v scale_d Re<z, c>| <= 2^-16 ||z~|| (split
+//     operands, fp32 accumulation, DESIGN 4.1b); the prologue stores lb' = rd(scale_v scale_d lb -
+//     2^-11 zn sd dmax) and zn = ru(scale_v ||z||), bnd_rs = ru(scale_d r): the margin covers the
+//     MMA error and the fp32 rounding of fl(zn r + s~) with room to spare.
+// (3) prune_list_kernel: need bits -> ascending tile lists + counts.
+__global__ void prune_keys_kernel(const int32_t* __restrict__ hint, int64_t n, int64_t d,
+                                  const int32_t* __restrict__ apos, const float2* __restrict__ lbz,
+                                  const float* __restrict__ bounds, int32_t pos_range,
+                                  int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t h = hint[v];
+  const float2 l = lbz[v];
+  // bound tightness lb / (||z|| dmax) (scaled units: zn carries scale_v, lb scale_v scale_d)
+  const float ratio = l.x / (l.y * bounds[kBScaleD] * bounds[kBDmax]);
+  const int bucket = ratio >= 0.95f ? 0 : ratio >= 0.8f ? 1 : ratio >= 0.5f ? 2 : 3;
+  keys[v] = bucket * pos_range + ((h >= 0 && h < d) ? apos[h] : pos_range - 1);
+  vals[v] = int32_t(v);
 }
 
-template <int KP, bool SPLIT, bool PAIR, bool HI32, bool RANGES = false>
-static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                        int grid, int n_vt, cudaStream_t st, int nsplit = 1) {
-  using C = TcCfg<KP, SPLIT, PAIR, HI32>;
-  int n_hint = 0;
-  if (zs.hint) {  // IPG warm start: the voxel tiles' (pairs') own hint atoms screened first
-    const int vox = PAIR ? 2 * C::kVox : C::kVox;
-    const int n_g = int((n + vox - 1) / vox);
-    const int nh = (vox + C::BN - 1) / C::BN;
-    const int kw = SPLIT ? KP : 8 * tc_nc(dv.s);  // row width (fp16 elements) as stored
-    const int64_t chunks = int64_t(n_g) * nh * C::BN * (kw / 8);
-    hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_g, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, kw, SPLIT ? 1 : 0, C::BN,
-        nh, w.hint_tiles);
-    CBB_CUDA_TRY(cudaGetLastError());
-    count_launches(1);
-    n_hint = kParts * nh;
+// One warp per voxel tile: ascending list of the needed atom tiles (< n_tiles) and its length.
+__global__ void prune_list_kernel(const uint32_t* __restrict__ bits, int words, int n_tiles,
+                                  int n_vt, int* __restrict__ pcnt, uint16_t* __restrict__ plist,
+                                  int plist_stride) {
+  const int vt = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (vt >= n_vt) return;
+  const uint32_t* b = bits + size_t(vt) * words;
+  uint16_t* out = plist + size_t(vt) * plist_stride;
+  int base = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    uint32_t m = w < words ? b[w] : 0u;
+    if (32 * w + 32 > n_tiles) m &= (32 * w >= n_tiles) ? 0u : ((1u << (n_tiles - 32 * w)) - 1u);
+    const int c = __popc(m);
+    int off = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, off, o);
+      if (lane >= o) off += y;
+    }
+    const int tot = __shfl_sync(0xffffffffu, off, 31);
+    off += base - c;
+    while (m) {
+      out[off++] = uint16_t(32 * w + __ffs(m) - 1);
+      m &= m - 1;
+    }
+    base += tot;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(unsigned(C::kThreads));
-  cfg.dynamicSmemBytes = size_t(C::kSmem);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = PAIR ? 1 : 0;
-  CBB_CUDA_TRY(cudaLaunchKernelEx(&cfg, mf_tc_kernel<KP, SPLIT, PAIR, HI32, RANGES>, w.ztiles, n,
-                                  n_vt,
-                                  (const float*)w.win_tc, (const float*)w.init_tc, dv, w.n_pad,
-                                  w.cand, w.meta, (const uint8_t*)w.hint_tiles, n_hint, nsplit));
-  return kOk;
-}
-
-// Dual-voxel-tile fp16 screen (mf_tc_dual_kernel): opt-in with CBB_TC_DUAL=1 (measured on
-// cfg1 with a dedicated producer warp: 10.5 ms vs 8.5 ms).
-static bool tc_dual_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CBB_TC_DUAL");
-    v = (e && atoi(e) == 1) ? 1 : 0;
-  }
-  return v != 0;
+  if (lane == 0) pcnt[vt] = base;
 }
 
 template <int KP>
-static int launch_tc_dual(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                          int grid, int n_vt, cudaStream_t st) {
-  using C = TcDual<KP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_dual_kernel<KP>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set = true;
-  }
+static int launch_bound(const ProjWs& w, int64_t n, const DictView& dv, cudaStream_t st);
+
+// Screen order + prune lists for an IPG projection with a warm-start hint (PRUNE screens).
+static int prune_prepare(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                         cudaStream_t st) {
+  const int threads = 256;
+  const int32_t pos_range = int32_t(int64_t(dv.n_tiles2) * split_rows(split_kp(dv.s)) + 1);
+  prune_keys_kernel<<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(
+      zs.hint, n, dv.d, dv.tc2_pos, w.lbz, dv.bounds, pos_range, w.pkeys, w.pvals);
+  CBB_CUDA_TRY(cudaGetLastError());
+  int bits = 1;
+  while ((int64_t(1) << bits) <= 4 * int64_t(pos_range)) ++bits;
+  size_t tmp = w.sort_tmp_bytes;
+  CBB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tmp, w.pkeys, w.pkeys_out, w.pvals,
+                                               w.vperm, int(n), 0, bits, st));
+  const int n_vt = int((n + 127) / 128);
+  const int words = (dv.n_tiles2 + 31) / 32 + 4;
+  CBB_CUDA_TRY(cudaMemsetAsync(w.pbits, 0, size_t(n_vt) * words * 4, st));
+  const int rc = split_kp(dv.s) == 64 ? launch_bound<64>(w, n, dv, st)
+                                      : launch_bound<128>(w, n, dv, st);
+  if (rc) return rc;
+  prune_list_kernel<<<unsigned((n_vt + 7) / 8), 256, 0, st>>>(w.pbits, words, dv.n_tiles2, n_vt,
+                                                            w.pcnt, w.plist, dv.n_tiles2);
+  CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(4);  // keys, bound pass, lists (+ the sort's own kernels)
+  return kOk;
+}
+
+template <int KP, bool SPLIT, bool RANGES = false, bool PRUNE = false>
+static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
+                        int grid, int n_vt, cudaStream_t st, int nsplit = 1) {
+  using C = TcCfg<KP, SPLIT>;
+  int rc = ensure_smem_attr<mf_tc_kernel<KP, SPLIT, RANGES, PRUNE>>(C::kSmem);
+  if (rc) return rc;
   int n_hint = 0;
-  if (zs.hint) {  // IPG warm start: each voxel-tile pair's own hint atoms screened first
-    const int vox = 2 * C::kVox;
-    const int n_g = int((n + vox - 1) / vox);
+  if (zs.hint) {  // IPG warm start: the voxel tiles' own hint atoms screened first
+    const int vox = C::kVox;
     const int nh = (vox + C::BN - 1) / C::BN;
-    const int64_t chunks = int64_t(n_g) * nh * C::BN * tc_nc(dv.s);
+    const int kw = SPLIT ? KP : 8 * tc_nc(dv.s);  // row width (fp16 elements) as stored
+    const int64_t chunks = int64_t(n_vt) * nh * C::BN * (kw / 8);
     hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_g, vox, dv.atoms_tc, 8 * tc_nc(dv.s), 0, C::BN, nh, w.hint_tiles);
+        zs.hint, n, dv.d, n_vt, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, kw, SPLIT ? 1 : 0, C::BN,
+        nh, PRUNE ? w.vperm : nullptr, SPLIT ? dv.tc2_pos : nullptr, w.hint_tiles);
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     n_hint = kParts * nh;
   }
-  mf_tc_dual_kernel<KP><<<grid, C::kThreads, C::kSmem, st>>>(
-      w.ztiles, n, n_vt, w.win_tc, w.init_tc, dv, w.n_pad, w.cand, w.meta, w.hint_tiles, n_hint);
+  mf_tc_kernel<KP, SPLIT, RANGES, PRUNE><<<grid, C::kThreads, C::kSmem, st>>>(
+      w.ztiles, n, n_vt, (const float*)w.win_tc, (const float*)w.init_tc, dv, w.n_pad, w.cand,
+      w.meta, (const uint8_t*)w.hint_tiles, n_hint, nsplit, PRUNE ? w.vperm : nullptr,
+      PRUNE ? w.pcnt : nullptr, PRUNE ? w.plist : nullptr, dv.n_tiles2, nullptr, nullptr,
+      nullptr, 0);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
 
-template <int KP, bool SPLIT = false, bool HI32 = false>
+// The bound pass: the centroids' split tiles screened like atom tiles (no hint tiles, no ranges).
+template <int KP>
+static int launch_bound(const ProjWs& w, int64_t n, const DictView& dv, cudaStream_t st) {
+  using C = TcCfg<KP, true>;
+  int rc = ensure_smem_attr<mf_tc_kernel<KP, true, false, false, true>>(C::kSmem);
+  if (rc) return rc;
+  const int n_vt = int((n + C::kVox - 1) / C::kVox);
+  int ctiles = (dv.n_tiles2 + C::BN - 1) / C::BN;
+  if (ctiles < kParts) ctiles = kParts;  // sentinel tiles: every part owns >= 1 tile
+  DictView cv = dv;
+  cv.d = int64_t(ctiles) * C::BN;
+  cv.atoms_tc2 = dv.ctr_tc2;
+  int grid = num_sms();
+  if (grid > n_vt) grid = n_vt;
+  mf_tc_kernel<KP, true, false, false, true><<<grid, C::kThreads, C::kSmem, st>>>(
+      w.ztiles, n, n_vt, (const float*)w.win_tc, (const float*)w.init_tc, cv, w.n_pad, w.cand,
+      w.meta, (const uint8_t*)w.hint_tiles, 0, 1, w.vperm, nullptr, nullptr, 0, w.lbz,
+      dv.tile_rs, w.pbits, (dv.n_tiles2 + 31) / 32 + 4);
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+// prune: PRUNE screen (split tiles, warm-start hint, prune lists prepared by prune_prepare)
+template <int KP, bool SPLIT = false>
 static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictView& dv,
-                     const ProjOut& out, int max_ctas, cudaStream_t st, int* nsplit_out) {
+                     int max_ctas, cudaStream_t st, int* nsplit_out, bool prune) {
   *nsplit_out = 1;
-  using C1 = TcCfg<KP, SPLIT, false, HI32>;
-  using C2 = TcCfg<KP, SPLIT, true, HI32>;
-  static bool attr_set = false;
-  static int pairs = 0;
-  if (!attr_set) {
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false, HI32>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, false, HI32, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmem));
-    CBB_CUDA_TRY(cudaFuncSetAttribute(mf_tc_kernel<KP, SPLIT, true, HI32>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C2::kSmem));
-    pairs = max_coresident_pairs(mf_tc_kernel<KP, SPLIT, true, HI32>, C2::kThreads, C2::kSmem);
-    attr_set = true;
-  }
+  using C1 = TcCfg<KP, SPLIT>;
   const int n_vt = int((n + C1::kVox - 1) / C1::kVox);
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if constexpr (!SPLIT && !HI32) {
-    // dual-voxel-tile screen when every CTA gets at least one voxel-tile pair
-    const int n_pt = (n_vt + 1) / 2;
-    if (tc_dual_enabled() && n_pt >= grid) return launch_tc_dual<KP>(w, n, zs, dv, grid, n_vt, st);
-  }
   // atom ranges: small projections (at most kSplitMaxN voxels) split the dictionary so the
   // work units (voxel tile x range) cover the SMs evenly: the smallest nsplit minimising
   // ceil(n_vt nsplit / grid) / nsplit, every range keeping >= 2 tiles per part
@@ -2789,17 +2838,20 @@ static int launch_tc(const ProjWs& w, int64_t n, const ZSource& zs, const DictVi
     if (best > 1) {
       *nsplit_out = best;
       const int units = n_vt * best;
-      return launch_tc_as<KP, SPLIT, false, HI32, true>(w, n, zs, dv, units < grid ? units : grid,
-                                                        n_vt, st, best);
+      if constexpr (SPLIT) {
+        if (prune)
+          return launch_tc_as<KP, SPLIT, true, true>(w, n, zs, dv, units < grid ? units : grid,
+                                                     n_vt, st, best);
+      }
+      return launch_tc_as<KP, SPLIT, true>(w, n, zs, dv, units < grid ? units : grid, n_vt, st,
+                                           best);
     }
   }
   if (grid > n_vt) grid = n_vt;
-  // CTA pairs halve the atom stream; used when every pair is co-resident (persistent kernel),
-  // at most 5% of the SMs idle, and every CTA gets at least two voxel tiles
-  int grid2 = 2 * pairs < grid ? 2 * pairs : grid - grid % 2;
-  if (tc_pair_enabled() && grid2 >= 8 && grid2 * 20 >= grid * 19 && n_vt >= 2 * grid2)
-    return launch_tc_as<KP, SPLIT, true, HI32>(w, n, zs, dv, grid2, n_vt, st);
-  return launch_tc_as<KP, SPLIT, false, HI32>(w, n, zs, dv, grid, n_vt, st);
+  if constexpr (SPLIT) {
+    if (prune) return launch_tc_as<KP, SPLIT, false, true>(w, n, zs, dv, grid, n_vt, st);
+  }
+  return launch_tc_as<KP, SPLIT>(w, n, zs, dv, grid, n_vt, st);
 }
 
 template <int S>
@@ -2846,22 +2898,6 @@ static int launch_exhaustive_s(int64_t n, const ZSource& zs, const DictView& dv,
   return kOk;
 }
 
-// compile-time width for the fp64 scoring loops (s_pad; 0 = runtime loop for s > 32)
-#define CBB_DISPATCH_S(s_pad, CALL)          \
-  switch (s_pad) {                          \
-    case 2: { constexpr int S_ = 2; CALL; }   \
-    case 4: { constexpr int S_ = 4; CALL; }   \
-    case 6: { constexpr int S_ = 6; CALL; }   \
-    case 8: { constexpr int S_ = 8; CALL; }   \
-    case 10: { constexpr int S_ = 10; CALL; } \
-    case 12: { constexpr int S_ = 12; CALL; } \
-    case 16: { constexpr int S_ = 16; CALL; } \
-    case 20: { constexpr int S_ = 20; CALL; } \
-    case 24: { constexpr int S_ = 24; CALL; } \
-    case 32: { constexpr int S_ = 32; CALL; } \
-    default: { constexpr int S_ = 0; CALL; }  \
-  }
-
 static int launch_exhaustive(int64_t n, const ZSource& zs, const DictView& dv, const int* cnt,
                              const int64_t* list, const ProjOut& out, cudaStream_t st) {
   const int sp = s_pad_for(dv.s);
@@ -2897,13 +2933,13 @@ static int launch_exhaustive_list(int64_t n, const ZSource& zs, const DictView& 
 
 template <int S, int NP>
 static int launch_rescore_np(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
-                          const ProjOut& o, cudaStream_t st, int nparts) {
+                          const ProjOut& o, cudaStream_t st, int nparts, const int32_t* amap) {
   // small projections: too few threads for the thread-per-voxel path to hide L2 latency, every
   // voxel goes to the warp kernel
   const int fast = n >= int64_t(num_sms()) * 256 ? kFastEntries : 0;
   rescore_fast_kernel<S, NP><<<int((n + 255) / 256), 256, 0, st>>>(
       zr, dv, n, w.n_pad, w.win_tc, w.cand, w.meta, o, w.ovf_count, w.ovf_list, w.heavy_count,
-      w.heavy_list, fast, nparts);
+      w.heavy_list, fast, nparts, amap);
   CBB_CUDA_TRY(cudaGetLastError());
   const size_t shm = size_t(kRescoreWarps) * (2 * dv.s * sizeof(double) +
                                                2 * dv.s_pad * sizeof(float) +
@@ -2914,16 +2950,17 @@ static int launch_rescore_np(const ProjWs& w, int64_t n, const ZSource& zr, cons
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
   rescore_warp_kernel<S, NP><<<num_sms() * 8, 32 * kRescoreWarps, shm, st>>>(
       zr, dv, w.n_pad, w.win_tc, w.win32, w.cand, w.meta, o, w.ovf_count, w.ovf_list,
-      w.heavy_count, w.heavy_list, nparts);
+      w.heavy_count, w.heavy_list, nparts, amap);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
 
 template <int S>
 static int launch_rescore(const ProjWs& w, int64_t n, const ZSource& zr, const DictView& dv,
-                          const ProjOut& o, cudaStream_t st, int nparts) {
-  return nparts == kParts ? launch_rescore_np<S, kParts>(w, n, zr, dv, o, st, nparts)
-                          : launch_rescore_np<S, kParts * kMaxSplit>(w, n, zr, dv, o, st, nparts);
+                          const ProjOut& o, cudaStream_t st, int nparts, const int32_t* amap) {
+  return nparts == kParts
+             ? launch_rescore_np<S, kParts>(w, n, zr, dv, o, st, nparts, amap)
+             : launch_rescore_np<S, kParts * kMaxSplit>(w, n, zr, dv, o, st, nparts, amap);
 }
 
 int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStream_t st) {
@@ -2934,14 +2971,15 @@ int reduce_sum(const double* x, int64_t n, double* partial, double* out, cudaStr
 }
 
 // algo: 0 = auto (split tcgen05 for coherent dictionaries with s <= 21, else tcgen05 when
-// 2s < 64, else FFMA / fp64),
-// 1 = tcgen05 (fp16 accumulators), 2 = FFMA, 3 = exhaustive fp64, 4 = split tcgen05 (hi/lo fp16
-// operands, fp32 accumulators, s <= 21), 5 = HI32 tcgen05 (fp16 operands, fp32 accumulators)
+// 2s < 64, else FFMA / fp64), 1 = tcgen05 (fp16 accumulators), 2 = FFMA, 3 = exhaustive fp64,
+// 4 = split tcgen05 (hi/lo fp16 operands, fp32 accumulators, s <= 21).
+// The split screen prunes atom tiles (prune_prepare) when the dictionary is prune-capable, a
+// warm-start hint is given and the workspace was sized for it (cbb_project_workspace_bytes_dict).
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st) {
   if (n < 0) return kErrArgument;
   ProjWs w;
-  const size_t need = project_ws_bytes(n, dv.s, &w, ws_ptr);
+  const size_t need = project_ws_bytes(n, dv.s, &w, ws_ptr, 0);
   if (ws_bytes < need) return kErrArgument;
   if (n == 0) {
     if (nd_sum) CBB_CUDA_TRY(cudaMemsetAsync(nd_sum, 0, sizeof(double), st));
@@ -2954,11 +2992,29 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   const bool tc_ok = (2 * dv.s < 64) && (dv.d <= (int64_t(1) << 25)) && (dv.d > 320);
   const bool split_ok = tc_ok && dv.s <= kSplitMaxS && dv.atoms_tc2 != nullptr;
   if (algo == 0) algo = (split_ok && dv.prefer_split) ? 4 : tc_ok ? 1 : (s_pad_for(dv.s) > 0 ? 2 : 3);
-  if ((algo == 1 || algo == 5) && !tc_ok) return kErrUnsupported;
+  if (algo == 1 && !tc_ok) return kErrUnsupported;
   if (algo == 4 && !split_ok) return kErrUnsupported;
-  const bool split = algo == 4, hi32 = algo == 5;
-  if (split || hi32) algo = 1;  // same pipeline, other operand tiles / accumulator format
+  const bool split = algo == 4;
+  if (split) algo = 1;  // same pipeline, other operand tiles / accumulator format
   if (algo == 2 && s_pad_for(dv.s) < 0) return kErrUnsupported;
+  bool prune = false;
+  {
+    const int pt = prune_tiles_of(dv);
+    if (pt > 0 && ws_bytes >= project_ws_bytes(n, dv.s, nullptr, nullptr, pt)) {
+      ProjWs wp;
+      project_ws_bytes(n, dv.s, &wp, ws_ptr, pt);
+      // small problems are launch-latency bound: the pruning pass (sort, bound pass, lists)
+      // only pays for large dictionaries and voxel counts
+      if (split && zs.hint && wp.prune && dv.n_tiles2 >= kPruneMinTiles && n >= kPruneMinVoxels) {
+        w = wp;
+        prune = true;
+      } else if (wp.prune) {  // mark the statistics of this workspace stale
+        CBB_CUDA_TRY(cudaMemsetAsync(wp.pcnt, 0xff, sizeof(int), st));
+      }
+    }
+  }
+  // records of the split screen hold split-tile positions: the rescoring maps them to atoms
+  const int32_t* amap = split ? dv.tc2_atom : nullptr;
   CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
   CBB_CUDA_TRY(cudaMemsetAsync(w.heavy_count, 0, sizeof(int), st));
   if (algo == 1 || algo == 2) {
@@ -2967,22 +3023,29 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
         zs, n, n_pad, dv.s, split ? split_kp(dv.s) : dv.kpad, dv.bounds,
         algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
-        algo == 1 ? w.init_tc : nullptr, split ? 1 : hi32 ? 2 : 0);
+        algo == 1 ? w.init_tc : nullptr, split ? 1 : 0, prune ? w.lbz : nullptr);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
+    if (zr.x != nullptr) {
+      zr.z = zr.z_out;
+      zr.z128 = 0;
+      zr.x = nullptr;
+    }
+    if (prune) {
+      const int rc = prune_prepare(w, n, zr, dv, st);
+      if (rc) return rc;
+    }
     timing_mark(0, st);
     int nsplit = 1;  // atom ranges of the screen (candidate lists: kParts per range)
-    int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, o, max_ctas, st, &nsplit)
-                                           : launch_tc<128, true>(w, n, zr, dv, o, max_ctas, st, &nsplit))
-             : hi32 ? (dv.kpad == 32 ? launch_tc<32, false, true>(w, n, zr, dv, o, max_ctas, st, &nsplit)
-                                     : launch_tc<64, false, true>(w, n, zr, dv, o, max_ctas, st, &nsplit))
-             : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, o, max_ctas, st, &nsplit)
-                                            : launch_tc<64>(w, n, zr, dv, o, max_ctas, st, &nsplit))
+    int rc = split ? (split_kp(dv.s) == 64 ? launch_tc<64, true>(w, n, zr, dv, max_ctas, st, &nsplit, prune)
+                                           : launch_tc<128, true>(w, n, zr, dv, max_ctas, st, &nsplit, prune))
+             : (algo == 1) ? (dv.kpad == 32 ? launch_tc<32>(w, n, zr, dv, max_ctas, st, &nsplit, false)
+                                            : launch_tc<64>(w, n, zr, dv, max_ctas, st, &nsplit, false))
                            : dispatch_ffma(w, n, zr, dv, o, st);
     if (rc) return rc;
     timing_mark(1, st);
     if (algo == 1) {
-      CBB_DISPATCH_S(dv.s_pad, rc = launch_rescore<S_>(w, n, zr, dv, o, st, kParts * nsplit);
+      CBB_DISPATCH_S(dv.s_pad, rc = launch_rescore<S_>(w, n, zr, dv, o, st, kParts * nsplit, amap);
                      break);
       if (rc) return rc;
       count_launches(2);
@@ -2992,16 +3055,17 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
                                 st);
     if (rc) return rc;
   } else if (algo == 3) {
+    ZSource zr = zs;
     if (zs.x != nullptr) {
       // materialise Z = X - mu G (same fp32 rounding as the prologue)
       const int64_t n_pad = n;
       prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                                dv.bounds, nullptr, nullptr,
                                                                nullptr, dv.s_pad, dv.atoms64,
-                                                               dv.d, nullptr, 0);
+                                                               dv.d, nullptr, 0, nullptr);
       CBB_CUDA_TRY(cudaGetLastError());
     }
-    int rc = launch_exhaustive(n, zs, dv, nullptr, nullptr, o, st);
+    int rc = launch_exhaustive(n, zr, dv, nullptr, nullptr, o, st);
     if (rc) return rc;
     count_launches(zs.x != nullptr ? 2 : 1);
   } else {
@@ -3014,9 +3078,32 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   return kOk;
 }
 
+// Tile-pruning statistics of the last projection on this workspace: listed (voxel tile, atom
+// tile) pairs and all pairs; listed = -1 if that projection did not prune.  Synchronises.
+int project_prune_stats(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView& dv,
+                        int64_t* listed, int64_t* total, cudaStream_t st) {
+  *listed = -1;
+  *total = 0;
+  const int pt = prune_tiles_of(dv);
+  if (pt <= 0 || n <= 0 || ws_bytes < project_ws_bytes(n, dv.s, nullptr, nullptr, pt)) return kOk;
+  ProjWs w;
+  project_ws_bytes(n, dv.s, &w, ws_ptr, pt);
+  if (!w.prune) return kOk;
+  const int64_t n_vt = (n + 127) / 128;
+  std::vector<int> cnt(static_cast<size_t>(n_vt));
+  CBB_CUDA_TRY(cudaMemcpyAsync(cnt.data(), w.pcnt, cnt.size() * 4, cudaMemcpyDeviceToHost, st));
+  CBB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (cnt[0] < 0) return kOk;
+  int64_t sum = 0;
+  for (int c : cnt) sum += c;
+  *listed = sum;
+  *total = n_vt * int64_t(pt);
+  return kOk;
+}
+
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st) {
   ProjWs w;
-  project_ws_bytes(n, s, &w, ws_ptr);
+  project_ws_bytes(n, s, &w, ws_ptr, 0);
   CBB_CUDA_TRY(cudaMemcpyAsync(host_count, w.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   CBB_CUDA_TRY(cudaStreamSynchronize(st));
   return kOk;
@@ -3024,7 +3111,7 @@ int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cuda
 
 int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st) {
   ProjWs w;
-  project_ws_bytes(n, s, &w, ws_ptr);
+  project_ws_bytes(n, s, &w, ws_ptr, 0);
   CBB_CUDA_TRY(cudaMemcpyAsync(host2, w.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   CBB_CUDA_TRY(cudaMemcpyAsync(host2 + 1, w.heavy_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   CBB_CUDA_TRY(cudaStreamSynchronize(st));
@@ -3069,12 +3156,12 @@ int trace_dump(long long*, int) { return kErrUnsupported; }
 int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr,
                   cudaStream_t st) {
   ProjWs w;
-  project_ws_bytes(n, dv.s, &w, ws_ptr);
+  project_ws_bytes(n, dv.s, &w, ws_ptr, 0);
   const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
   prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
                                                              w.win32, dv.s_pad, dv.atoms64, dv.d,
-                                                             w.init_tc, 0);
+                                                             w.init_tc, 0, nullptr);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

@@ -35,6 +35,17 @@ struct DictView {
   const uint8_t* atoms_tc2;    // split-operand tiles (s <= kSplitMaxS, else null): swizzled
                                // rows of split_kp(s) fp16 [d_hi | d_hi | d_lo | sentinel]
   int32_t prefer_split;        // auto mode screens with the split tiles (coherent dictionary)
+  int32_t reserved;
+  int32_t n_tiles2;            // split-screen atom tiles: ceil(d / split_rows(split_kp(s)))
+  int32_t reserved2;
+  // Coherent dictionaries: the split tiles hold the atoms in a bisection order (compact tiles)
+  // with per-tile / per-group bounds for the IPG tile pruning (prune_kernel); null otherwise.
+  const int32_t* tc2_atom;     // split-tile row -> atom index (d for padded rows); null: identity
+  const int32_t* tc2_pos;      // atom -> split-tile row; null: identity
+  const float* tile_c;         // [n_tiles2][2 s_pad] fp32 planar centroid of each split tile
+  const float* tile_r;         // [n_tiles2] radius >= max ||d_j - c|| over the tile's atoms
+  const uint8_t* ctr_tc2;      // the centroids as split-operand tiles (bound pass B operand)
+  const float* tile_rs;        // [n_tiles2 (+ sentinel rows)] radius * scale_d, rounded up
 };
 
 // Bounds slots (all rounded up).  The fp16 tiles hold d~ = fp16(scale_d * d) with scale_d a

@@ -55,7 +55,3 @@ def to_device(arr: np.ndarray, device: torch.device, dtype=None) -> torch.Tensor
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
     t = torch.from_numpy(a)
     return t.to(device, non_blocking=True)
-
-
-def complex_view_as_real_ok(t: torch.Tensor) -> torch.Tensor:
-    return t.contiguous()

@@ -23,6 +23,7 @@ with s << L the n x s coordinates are L/s times smaller than the n x L frame sta
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
@@ -131,7 +132,7 @@ class ShardedIpgState(IpgState):
         self.gam_n = torch.empty(nl, dtype=torch.float64, device=device)
         self.scal = torch.zeros(8, dtype=torch.float64, device=device)
         self.host = torch.zeros(8, dtype=torch.float64, pin_memory=True)
-        self.pws_bytes = lib.cbb_project_workspace_bytes(nl, dim)
+        self.pws_bytes = lib.cbb_project_workspace_bytes_dict(nl, ctypes.byref(self.dd.view))
         self.rws_bytes = lib.cbb_reduce_workspace_bytes()
         self.algo = 0
 

@@ -185,7 +185,8 @@ class IpgState:
         self.gam_n = torch.empty(n, dtype=torch.float64, device=device)
         self.scal = torch.zeros(8, dtype=torch.float64, device=device)  # device scalars
         self.host = torch.zeros(8, dtype=torch.float64, pin_memory=True)
-        self.pws_bytes = lib.cbb_project_workspace_bytes(n, dim)
+        # sized for the dictionary: includes the split screen's tile-pruning buffers
+        self.pws_bytes = lib.cbb_project_workspace_bytes_dict(n, ctypes.byref(self.dd.view))
         self.rws_bytes = lib.cbb_reduce_workspace_bytes()
         self.algo = 0
 

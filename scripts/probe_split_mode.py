@@ -39,7 +39,7 @@ def timeit(Z, dd, algo, reps=3):
     return ev[0].elapsed_time(ev[1]) / reps, out
 
 
-def compare(name, Z, dd, algos=("tcgen05_split", "tcgen05_hi32", "tcgen05")):
+def compare(name, Z, dd, algos=("tcgen05_split", "tcgen05")):
     res = {}
     for a in algos:
         ms, out = timeit(Z, dd, a)
@@ -67,7 +67,7 @@ if "small" in which:
         rng.standard_normal((n, 10)) + 1j * rng.standard_normal((n, 10)))
     dd = device_dictionary(atoms, dev)
     ref = orc.project_cone_exact(Z, atoms)
-    for a in ("tcgen05", "tcgen05_split", "tcgen05_hi32", "ffma"):
+    for a in ("tcgen05", "tcgen05_split", "ffma"):
         got = project_device(torch.from_numpy(Z).to(dev), dd, algo=a)
         gi = got[0].cpu().numpy()
         print(f"small coherent d={len(atoms)} {a:14s} index mismatches vs oracle: "

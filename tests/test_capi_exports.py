@@ -45,7 +45,7 @@ def test_ctypes_binding_covers_header(built):
     from paper_1810_01967_b200 import _lib
     lib = _lib.load()
     assert set(_lib.SIGNATURES) == set(declared())
-    assert lib.cbb_abi_version() == 2
+    assert lib.cbb_abi_version() == 3
     # sizes are pure host arithmetic
     assert lib.cbb_project_workspace_bytes(1 << 20, 10) > (1 << 20) * 64
     assert lib.cbb_dict_storage_bytes(1 << 17, 10) >= (1 << 17) * 10 * 16
