@@ -247,21 +247,27 @@ __device__ __noinline__ int hcand_spill(const int* cj, const float* cs, int stri
   return gcnt;
 }
 
+// The score column of slot `slot` sits kCandCap * STRIDE words after its index column (kOffCs =
+// kOffCj + kCandCap * kSlots * 4), so the list carries one shared pointer; STRIDE and the global
+// stride are compile-time / kernel constants (fewer live registers in the screen's epilogue).
+template <int STRIDE>
 struct HCandList {
-  int* cj;           // shared-memory list, column layout [kCandCap][stride]
-  float* cs;
-  int stride;
+  int* cj;           // shared-memory list, column layout [kCandCap][STRIDE], scores after it
   int cnt;
   int2* gbase;       // global spill list
   int64_t gstride;
   int gcnt;
   bool ovf;
 
+  __device__ __forceinline__ float* cs() const {
+    return reinterpret_cast<float*>(cj + kCandCap * STRIDE);
+  }
+
   __device__ __forceinline__ void insert(int j, float sc, float thr) {
     if (cnt == kCandCap) {
-      cnt = cand_compact(cj, cs, stride, thr);
+      cnt = cand_compact(cj, cs(), STRIDE, thr);
       if (cnt == kCandCap) {
-        const int g = hcand_spill(cj, cs, stride, cnt, gbase, gstride, gcnt, thr);
+        const int g = hcand_spill(cj, cs(), STRIDE, cnt, gbase, gstride, gcnt, thr);
         if (g < 0) {
           ovf = true;
           return;
@@ -270,8 +276,8 @@ struct HCandList {
         cnt = 0;
       }
     }
-    cs[cnt * stride] = sc;
-    cj[cnt * stride] = j;
+    cs()[cnt * STRIDE] = sc;
+    cj[cnt * STRIDE] = j;
     ++cnt;
   }
 
@@ -280,11 +286,11 @@ struct HCandList {
   __device__ __forceinline__ int finish(float thr) {
     if (ovf) return -1;
     for (int c = 0; c < cnt; ++c) {
-      const float x = cs[c * stride];
+      const float x = cs()[c * STRIDE];
       if (x >= thr) {
         if (gcnt == kGCap) gcnt = gcand_compact(gbase, gstride, gcnt, thr);
         if (gcnt == kGCap) return -1;
-        gbase[(gcnt++) * gstride] = make_int2(cj[c * stride], __float_as_int(x));
+        gbase[(gcnt++) * gstride] = make_int2(cj[c * STRIDE], __float_as_int(x));
       }
     }
     return gcnt;
@@ -1030,7 +1036,7 @@ struct TcCfg {
   static constexpr int kSlots = kVox * kParts;
   static constexpr int kOffB = 0;
   static constexpr int kOffCj = kOffB + kStages * kBBytes;
-  static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;
+  static constexpr int kOffCs = kOffCj + kCandCap * kSlots * 4;  // = HCandList::cs()
   static constexpr int kOffPthr = kOffCs + kCandCap * kSlots * 4;  // [kVox][4] u32 thresholds
   static constexpr int kOffBar = kOffPthr + kVox * 16;
   // completion barriers per tile slot k % kTBars (lcm(kAcc, kParts)): every barrier belongs to
@@ -1087,8 +1093,9 @@ __device__ __forceinline__ __half hmax_halves(__half2 m) {
 
 // Record 32-atom chunk (16 packed registers) with max cm: groups g < 5 -> registers
 // 3g..3g+2 (atoms 6g..6g+5), g = 5 -> register 15 (atoms 30, 31).
+template <class CL>
 __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64_t jb, __half thr,
-                                             float thr_f, HCandList& cl) {
+                                             float thr_f, CL& cl) {
   uint32_t mask = __hge(hmax_halves(as_h2(r[15])), thr) ? (1u << 5) : 0u;
 #pragma unroll
   for (int i = 0; i < 5; ++i)
@@ -1099,10 +1106,10 @@ __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64
   cl.insert(pack_chunk(jb, mask), __half2float(cm), thr_f);
 }
 
-template <int NC>
+template <int NC, class CL>
 __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_t jb, float win,
                                             __half& runmax, __half& thr, bool& active,
-                                            HCandList& cl, uint32_t* pub, uint32_t tag) {
+                                            CL& cl, uint32_t* pub, uint32_t tag) {
   // NC independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
   __half2 c[NC];
 #pragma unroll
@@ -1144,8 +1151,9 @@ __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_
 // and one warp vote per tile; records carry the chunk's 6-atom group mask.
 __device__ __forceinline__ float fmax3f(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 
+template <class CL>
 __device__ __forceinline__ void record_chunk_f32(const uint32_t* r, float cm, int64_t jb,
-                                                 float thr, HCandList& cl) {
+                                                 float thr, CL& cl) {
   uint32_t mask = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])) >= thr ? (1u << 5) : 0u;
 #pragma unroll
   for (int g = 0; g < 5; ++g) {
@@ -1158,10 +1166,10 @@ __device__ __forceinline__ void record_chunk_f32(const uint32_t* r, float cm, in
   cl.insert(pack_chunk(jb, mask), cm, thr);
 }
 
-template <int NC>
+template <int NC, class CL>
 __device__ __forceinline__ void screen_tile_f32(const uint32_t (&r)[32 * NC], int64_t jb,
                                                 float win, float& runmax, float& thr,
-                                                bool& active, HCandList& cl) {
+                                                bool& active, CL& cl) {
   float c[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
@@ -1380,7 +1388,16 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       uint32_t ph = 0;
       int b = lane;  // this lane's next tile inside the current work unit
       for (int it = 0; it < my_vts; ++it) {
-        const Unit un = unit_of(it);
+        Unit un;
+        if constexpr (PRUNE) {
+          un = unit_of(it);
+        } else {
+          const int u = int(blockIdx.x) + it * int(gridDim.x);
+          un.vt = u / nsplit;
+          un.hr = u - un.vt * nsplit;
+          un.lo = un.hr * nBh;
+          un.len = nBh;
+        }
         const int T = n_hint + un.len;
         const uint8_t* hbase = hint_tiles + size_t(un.vt) * (n_hint / kParts) * tile_bytes;
         const uint16_t* lst = PRUNE ? plist + size_t(un.vt) * plist_stride + un.lo : nullptr;
@@ -1421,7 +1438,8 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     uint32_t ph = 0;
     uint32_t kk = uint32_t(me), kbeg = 0;
     for (int it = 0; it < my_vts; ++it) {
-      const uint32_t kend = kbeg + uint32_t(n_hint + unit_of(it).len);
+      const uint32_t kend =
+          kbeg + uint32_t(n_hint + (PRUNE ? unit_of(it).len : nBh));
       // every issuer owns >= 1 tile of the unit (T >= kParts): wait for its A operand
       mbar_wait(a_full + (it & 1), (it >> 1) & 1);
       for (; kk < kend; kk += kParts) {
@@ -1502,7 +1520,6 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     const int row = q * 32 + lane;  // voxel row inside the voxel tile (= TMEM lane)
     const int slot = part * C::kVox + row;
     int* cj_base = reinterpret_cast<int*>(smem + C::kOffCj);
-    float* cs_base = reinterpret_cast<float*>(smem + C::kOffCs);
     const uint32_t lane_off = uint32_t(q * 32) << 16;
     const uint32_t a_lane = tbase + lane_off + uint32_t(C::kAColOff);
     const uint32_t t_lane = tbase + lane_off;
@@ -1524,19 +1541,33 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
     uint32_t ph = 0;
     uint32_t kbeg = 0;
     for (int it = 0; it < my_vts; ++it) {
-      const Unit un = unit_of(it);
-      const int vt = un.vt, hr = un.hr;
+      int vt, hr, T;
+      int64_t v;
+      const uint16_t* lst = nullptr;
+      if constexpr (PRUNE || BOUND) {
+        const Unit un = unit_of(it);
+        vt = un.vt;
+        hr = un.hr;
+        T = n_hint + un.len;
+        v = voxel_of(vt, row);
+        if constexpr (PRUNE) lst = plist + size_t(vt) * plist_stride + un.lo;
+      } else {  // fixed-length units, identity voxel order (kept in this form: see DESIGN 4.1)
+        const int u = int(blockIdx.x) + it * int(gridDim.x);
+        vt = u / nsplit;
+        hr = u - vt * nsplit;
+        T = n_hint + nBh;
+        v = int64_t(vt) * C::kVox + row;
+      }
       const int opart = hr * kParts + part;  // output lists of (atom range, part)
-      const int64_t v = voxel_of(vt, row);
       const bool live = v < n;
-      const int T = n_hint + un.len;
-      const uint16_t* lst = PRUNE ? plist + size_t(vt) * plist_stride + un.lo : nullptr;
       // ---- stage the NEXT voxel tile's rows into the other A buffer (one tile ahead)
       if (part == 0 && it + 1 < my_vts) {
         const int nbuf = (it + 1) & 1;
         mbar_wait(a_empty + nbuf, (((it + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
-        const int64_t vn = voxel_of((int(blockIdx.x) + (it + 1) * int(gridDim.x)) / nsplit, row);
+        const int un_next = (int(blockIdx.x) + (it + 1) * int(gridDim.x)) / nsplit;
+        const int64_t vn = (PRUNE || BOUND) ? voxel_of(un_next, row)
+                                            : int64_t(un_next) * C::kVox + row;
         stage_voxel_row<KP>(zrows, vn, vn < n, a_lane + uint32_t(nbuf * C::kACols));
         tc_fence_before();
         __syncwarp();
@@ -1545,8 +1576,9 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       if (part == 0 && q == 0 && lane == 0) CBB_STAMP_VT(0, it);
       const float win = live ? win_tc[v] : -1.f;
       bool active = live && win >= 0.f;
-      HCandList cl{cj_base + slot, cs_base + slot, C::kSlots, 0,
-                   cand + int64_t(opart) * kGCap * n_pad + (live ? v : 0), n_pad, 0, false};
+      HCandList<C::kSlots> cl{cj_base + slot, 0,
+                              cand + int64_t(opart) * kGCap * n_pad + (live ? v : 0), n_pad, 0,
+                              false};
       // running max seeded with the warm-start lower bound (-inf without a hint)
       const float init = live ? fmaxf(init_tc[v], -65504.f) : -INFINITY;
       __half runmax = active ? __float2half_rd(init) : __ushort_as_half(0xFC00);
@@ -1555,14 +1587,16 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
       // split mode: fp32 running max / threshold (thresholds rounded down)
       float runmax_f = active ? init_tc[v] : -INFINITY;
       float thr_f = active ? __fsub_rd(runmax_f, win) : INFINITY;
-      const uint32_t kend = kbeg + uint32_t(T);
+      // first tile of the unit: carried for pruned (variable-length) units, it T otherwise
+      const uint32_t kb = PRUNE ? kbeg : uint32_t(it) * uint32_t(T);
+      const uint32_t kend = kb + uint32_t(T);
       if constexpr (BOUND) {
         // per (voxel, centroid): need = fl(zn r + s~) >= lb - margin; a warp ORs its lanes' bits
         // (the tile's 32-centroid words) into the voxel tile's global need mask
         const float2 lz = live ? lbz[v] : make_float2(INFINITY, 0.f);
         uint32_t* vbits = bnd_bits + size_t(vt) * bnd_words;
         for (; kk < kend; kk += kParts) {
-          const int ba = int(kk - kbeg);  // centroid tile
+          const int ba = int(kk - kb);  // centroid tile
           mbar_wait(t_full + tb, ph);
           tc_fence_after();
           constexpr int kRegChunks = C::kChunks < 2 ? C::kChunks : 2;
@@ -1627,7 +1661,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         static_assert(C::kAcc == kParts && C::kTBars == kParts, "stage = part");
         const uint32_t tag = (uint32_t(it) & 0xffffu) << 16;
         uint32_t* my_pub = pthr_row + part;
-        const uint32_t khint = kbeg + uint32_t(n_hint);
+        const uint32_t khint = kb + uint32_t(n_hint);
         uint32_t r[16 * C::kChunks];
         auto consume = [&]() {
           if (q == 0 && lane == 0) CBB_STAMP(5, kk);
@@ -1677,7 +1711,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         // split screen: fp32 scores, at most two chunks (64 registers) in flight; wider tiles are
         // screened in halves and released after the last half is loaded
         for (; kk < kend; kk += kParts) {
-          const int qt = int(kk - kbeg) - n_hint;  // < 0: warm-start hint tile
+          const int qt = int(kk - kb) - n_hint;  // < 0: warm-start hint tile
           int ba;
           if constexpr (PRUNE) {
             ba = qt >= 0 ? int(lst[qt]) : 0;       // loaded before the wait
