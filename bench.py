@@ -1,26 +1,35 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 exact matched-filter projection (BASELINE.json configs[1]).
+"""Benchmark of the B200 exact matched-filter projection and IPG (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one exact cone projection (``project_cone_exact``: tcgen05 fp16 screening with
-fp16 accumulators, certified window, fp64 rescoring, write-back) of N = 2^20 voxels x D = 2^17 random unit
-atoms, s = 10, per GPU (voxel-sharded, weak scaling: every rank projects its own 2^20
-voxels against the replicated dictionary; there is no data-path collective).  Inputs are
-seeded synthetic data with the config's shapes and distributions (no dataset exists).
+fp16 accumulators, certified window, fp64 rescoring, write-back) of N = 2^20 voxels x D = 2^17
+random unit atoms, s = 10, per GPU (BASELINE configs[1], voxel-sharded weak scaling: every rank
+projects its own 2^20 voxels against the replicated dictionary; no data-path collective).
+Inputs are seeded synthetic data with the config's shapes and distributions (no dataset exists).
 
-The JSON line carries: value = whole-job algorithmic MAC/s (N D 2s real MACs per GPU
-step, inputs resident in HBM, L2 flushed between timed steps), e2e = the same metric
-through the public numpy API with pinned host buffers (H2D of Z and D2H of indices /
-gammas / projected inside the timed region), the roofline of the matched-filter kernel
-against the measured dense 16-bit tensor peak (MEASURED_PEAKS bf16; fp16 runs at the same
-tcgen05 rate), the CPU baseline (the numpy port of the reference path on
-this box's host cores, bounded sample), the cfg0 IPG iteration rate, clocks sampled during
-the timed region, and the number of kernels this library launched.
+``--gpus N`` without a launcher re-executes itself under ``torch.distributed.run`` with N ranks
+(one per GPU, NCCL); under torchrun every rank runs the same legs and rank 0 prints ONE line.
 
-``--impl reference`` times the reference's CPU implementation of the same path (the numpy
-port in ``oracle/``; the reference is pure Python and cannot be installed on the box) on all
-host cores, with the same metric and config; under torchrun only rank 0 runs.
+The JSON line carries:
+  value      whole-job algorithmic MAC/s (N D 2s real MACs per GPU step, inputs resident in HBM,
+             L2 flushed between timed steps, CUDA events, max over ranks)
+  e2e        the same metric through the public numpy API with pinned host buffers (H2D of Z and
+             D2H of indices / gammas / projected inside the timed region)
+  roofline   the matched-filter kernel against the measured dense 16-bit tensor peak
+  parity     GPU vs the fp64 oracle at benchmark scale: cfg1 (4,096 voxels x 2^17 atoms), cfg3
+             (512 voxels x 2^20 atoms), cfg2 / cfg4 (2,048 sampled voxels of the IPG iterate at the
+             first and the last iteration x the full dictionary); all outside the timed regions
+  cpu_baseline  the reference path on this box's host cores (numpy port, the real reference
+             package's cover tree and IPG when it is installed under baseline/_ref)
+  ipg*       cfg0 / cfg2 / cfg4 IPG iterations through the public solve_compressed, the sharded
+             solver (also at N = 1) with its operator GB/s and tile-pruning statistics
+  clocks, gpu_launches
+
+``--impl reference`` times the reference's CPU implementation of the same path (the numpy port
+in ``oracle/``: the reference algorithm is numpy's zgemm + argmax) on all host cores, with the
+same metric and config; under torchrun only rank 0 runs.
 """
 
 from __future__ import annotations
@@ -28,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -45,6 +55,8 @@ S = 10
 METRIC = "voxel x atom matched-filter MACs/s (exact projection, cfg1)"
 UNIT = "MAC/s"
 CPU_SAMPLE_VOXELS = 4096
+PARITY_IPG_VOXELS = 2048
+PARITY_CFG3_VOXELS = 512
 
 
 def macs_per_step(n=N_VOX, d=D_ATOMS, s=S):
@@ -127,20 +139,176 @@ def profiled_traffic():
         return None
 
 
-def cpu_baseline(atoms, Z, sample=CPU_SAMPLE_VOXELS):
-    """Reference path (numpy port of projection.py:45-67, complex128) on the host cores."""
+def host_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "numpy": np.__version__, "blas": blas,
+            "threads": "all host cores (OpenBLAS default)"}
+
+
+def load_reference():
+    """The reference package installed under baseline/_ref (python -m pip install --target), or
+    None with the reason.  Used only by the CPU baseline legs."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "coverblip")):
+        return None, "baseline/_ref not installed"
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import coverblip  # noqa: F401
+        from coverblip import covertree, dictionary, forward_model, solver  # noqa: F401
+        return coverblip, None
+    except Exception as exc:  # report, never hide
+        return None, f"import failed: {exc!r}"
+
+
+def parity_block(Z, atoms, gpu_idx, gpu_gam):
+    """GPU indices / gammas vs the fp64 oracle (top-2 restatement of projection.py:58-62) on the
+    same voxels: index mismatches outside documented near-ties (top-2 gap < 1e-5 |s1|)."""
+    from oracle import projection as orc
+    z = np.asarray(Z, dtype=np.complex128)
+    i1, s1, s2 = orc.top2(z, atoms)
+    near = orc.near_tie_mask(s1, s2)
+    gi = np.asarray(gpu_idx).astype(np.int64)
+    bad = (gi != i1) & ~near
+    same = gi == i1
+    gref = np.maximum(s1, 0.0)
+    gg = np.asarray(gpu_gam, dtype=np.float64)
+    denom = np.maximum(np.abs(gref), 1e-300)
+    rel = np.abs(gg - gref)[same] / denom[same]
+    return {"voxels": int(len(gi)), "D": int(atoms.shape[0]),
+            "index_mismatch_non_near_tie": int(bad.sum()),
+            "near_ties": int(near.sum()), "near_tie_index_differs": int((near & ~same).sum()),
+            "gamma_max_rel": float(rel.max()) if rel.size else 0.0,
+            "gamma_norm_rel": float(np.linalg.norm((gg - gref)[same]) /
+                                    max(np.linalg.norm(gref[same]), 1e-300)) if rel.size else 0.0}
+
+
+# ---------------------------------------------------------------- CPU baselines (rank 0, N = 1)
+def cpu_baseline(atoms, Z, gpu_idx, gpu_gam, sample=CPU_SAMPLE_VOXELS):
+    """Reference path (numpy port of projection.py:45-67) on the host cores: complex128 (the
+    solver's dtype) and complex64, on the first `sample` cfg1 voxels, plus the parity of the GPU
+    result for those voxels."""
     from oracle import projection as orc
     zs = np.asarray(Z[:sample], dtype=np.complex128)
     orc.project_cone_exact(zs[:64], atoms)  # warm the BLAS threads
     t0 = time.perf_counter()
     orc.project_cone_exact(zs, atoms)
     dt = time.perf_counter() - t0
+    z64, a64 = zs.astype(np.complex64), atoms.astype(np.complex64)
+    t1 = time.perf_counter()
+    orc.project_cone_exact(z64, a64)
+    dt64 = time.perf_counter() - t1
     return {"value": macs_per_step(sample, atoms.shape[0]) / dt, "unit": UNIT,
             "cores": os.cpu_count(), "kind": "port",
             "sample": f"{sample} voxels x {atoms.shape[0]} atoms, s={S}, complex128 "
-                      f"(numpy/OpenBLAS, {dt:.2f} s)"}
+                      f"(numpy/OpenBLAS, {dt:.2f} s)",
+            "complex64": {"value": macs_per_step(sample, atoms.shape[0]) / dt64, "unit": UNIT,
+                          "seconds": dt64},
+            "host": host_info(),
+            "parity_cfg1": parity_block(zs, atoms, gpu_idx[:sample], gpu_gam[:sample])}
 
 
+def _ref_cfg0(ref, cfg):
+    """cfg0 inputs in the reference's own types (same atoms, basis and pattern)."""
+    from coverblip import dictionary as rd
+    from coverblip import forward_model as rf
+    parent = rd.Dictionary(atoms=cfg.dictionary.atoms, norms=cfg.dictionary.norms,
+                           lookup_table=cfg.dictionary.lookup_table, tr_ms=cfg.dictionary.tr_ms,
+                           L=cfg.dictionary.L)
+    cd = rd.CompressedDictionary(basis=cfg.cdict.basis, atoms_compressed=cfg.cdict.atoms_compressed,
+                                 renorm_factors=cfg.cdict.renorm_factors, s=cfg.cdict.s,
+                                 parent=parent)
+    A = rf.make_cartesian_operator(rf.SamplingPattern(indices=cfg.pattern,
+                                                      spatial_shape=cfg.spatial_shape))
+    return cd, A
+
+
+def cpu_reference_legs():
+    """The reference's CPU exact IPG and cover-tree paths on the box's host cores (SURVEY 8d,
+    BASELINE.md 4), through the installed reference package: cfg0 solve_compressed(blip_exact)
+    end to end, the cover tree on cfg0 (build + coverblip at eps 0 and 0.4) and cover-tree builds
+    on random atoms (d = 2^12, 2^13, extrapolated as a power law)."""
+    ref, why = load_reference()
+    out = {"kind": "reference", "cores": os.cpu_count()}
+    if ref is None:
+        # the numpy restatement of _solve_core stands in for the exact IPG (no cover tree port)
+        out["kind"] = "port"
+        out["reference"] = f"unavailable: {why}"
+    from paper_1810_01967_b200 import workloads
+    cfg = workloads.make_cfg0()
+    if ref is not None:
+        from coverblip import covertree as rc
+        from coverblip import solver as rs
+        cd, A = _ref_cfg0(ref, cfg)
+        t0 = time.perf_counter()
+        X, maps, gam, trace = rs.solve_compressed(
+            cfg.Y, A, cd, None, rs.SolverConfig(mode="blip_exact", max_iters=20, zeta=2.0,
+                                                compressed=10))
+        dt = time.perf_counter() - t0
+        out["ipg_cfg0_exact"] = {"iterations": trace.iterations, "seconds": dt,
+                                 "ms_per_iter": 1e3 * dt / max(1, trace.iterations),
+                                 "final_fidelity": trace.records[-1]["fidelity"]}
+        t0 = time.perf_counter()
+        tree = rc.build(cd.atoms_compressed)
+        out["cover_tree_cfg0_build_s"] = time.perf_counter() - t0
+        for eps in (0.0, 0.4):
+            iters = 3
+            t0 = time.perf_counter()
+            X, maps, gam, trace = rs.solve_compressed(
+                cfg.Y, A, cd, tree, rs.SolverConfig(mode="coverblip", epsilon=eps,
+                                                    max_iters=iters, zeta=2.0, compressed=10))
+            dt = time.perf_counter() - t0
+            trials = sum(r["shrinks"] + 1 for r in trace.records)
+            out[f"coverblip_cfg0_eps{eps}"] = {
+                "iterations": trace.iterations, "projection_trials": trials, "seconds": dt,
+                "ms_per_iter": 1e3 * dt / max(1, trace.iterations),
+                "ms_per_query": 1e3 * dt / max(1, trials * cfg.gt.shape[0])}
+        builds = {}
+        for d in (1 << 12, 1 << 13):
+            a = workloads.random_atoms(d, 10, seed=0)
+            t0 = time.perf_counter()
+            rc.build(a)
+            builds[d] = time.perf_counter() - t0
+        (d1, t1), (d2, t2) = sorted(builds.items())
+        p = float(np.log(t2 / t1) / np.log(d2 / d1))
+        out["cover_tree_random_build"] = {
+            "s": 10, "seconds": {str(k): v for k, v in builds.items()}, "power_law_exponent": p,
+            "extrapolated_s": {str(1 << 17): t2 * (float(1 << 17) / d2) ** p,
+                               str(1 << 20): t2 * (float(1 << 20) / d2) ** p}}
+    else:
+        from oracle import solver as osv
+        t0 = time.perf_counter()
+        res = osv.solve_core(cfg.Y, _OracleOp(cfg), cfg.cdict.atoms_compressed, cfg.cdict.basis,
+                             mode="blip_exact", max_iters=20, zeta=2.0)
+        dt = time.perf_counter() - t0
+        out["ipg_cfg0_exact"] = {"seconds": dt, "note": "oracle/solver.py restatement"}
+    return out
+
+
+class _OracleOp:
+    """cfg0 Cartesian operator of the oracle restatement (fallback CPU IPG leg)."""
+
+    def __new__(cls, cfg):
+        from oracle import operator as oop
+        return oop.CartesianOperator(cfg.pattern, cfg.spatial_shape)
+
+
+# ---------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -170,10 +338,11 @@ def run_reference(args, rank, world):
                                        "(reference algorithm, numpy/OpenBLAS complex128)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
+# ---------------------------------------------------------------- IPG legs
 def ipg_rate(device):
     """BASELINE configs[0] IPG through the public solve_compressed (device-resident loop)."""
     from paper_1810_01967_b200 import workloads
@@ -191,8 +360,8 @@ def ipg_rate(device):
     return {"config": "BASELINE configs[0] (64x64, L=200, D=2242 Bloch IR-bSSFP atoms, s=10, "
                       "8/64 lines, 30 dB, zeta=2, max 20 iters)",
             "iterations": its, "projection_trials": trials, "seconds": dt,
-            "iters_per_s": its / dt, "ms_per_iter": 1e3 * dt / its,
-            "final_fidelity": trace.fidelities()[-1]}
+            "iters_per_s": its / trace.total_time, "ms_per_iter": 1e3 * trace.total_time / its,
+            "solve_seconds": dt, "final_fidelity": trace.fidelities()[-1]}
 
 
 LARGE_IPG = {
@@ -208,13 +377,121 @@ LARGE_IPG = {
 }
 
 
-def ipg_rate_large(device, peaks, which, world=1):
-    """BASELINE configs[2] / configs[4] IPG through the public solve_compressed -- or, under
-    torchrun, through sharded.solve_compressed_sharded over all ranks (voxel-sharded
-    projection, frame-sharded operator; times = max over ranks) -- with the SURVEY 8d roofline
-    model of one iteration (materialised-frame byte model + r projections on the tensor
-    cores).  iters_per_s uses the IPG loop time; solve_seconds is the whole public call
-    (state upload, loop, the (n, L) complex128 image and the maps back on the host)."""
+class _IterProbe:
+    """on_iter hook of the (untimed) parity solve: the iterate sample at the first and the last
+    iteration, and the tile-pruning statistics of every iteration's accepted trial."""
+
+    def __init__(self, n, seed=7, sample=PARITY_IPG_VOXELS):
+        import torch
+        rng = np.random.default_rng(seed)
+        self.rows = np.sort(rng.choice(n, size=min(sample, n), replace=False))
+        self.rows_t = None
+        self.first = self.last = None
+        self.listed = []
+        self.torch = torch
+
+    def __call__(self, k, st, mu, shrinks, fixed):
+        import ctypes
+
+        from paper_1810_01967_b200 import _lib
+        from paper_1810_01967_b200.device import workspace
+        torch = self.torch
+        n_loc = st.n
+        v0 = getattr(getattr(st, "comm", None), "v0", 0)
+        mine = (self.rows >= v0) & (self.rows < v0 + n_loc)
+        loc = torch.as_tensor(self.rows[mine] - v0, device=st.dev)
+        snap = (k, self.rows[mine], st.Z.index_select(0, loc).cpu().numpy(),
+                st.idx_n.index_select(0, loc).cpu().numpy(),
+                st.gam_n.index_select(0, loc).cpu().numpy())
+        if self.first is None:
+            self.first = snap
+        self.last = snap
+        lib = _lib.load()
+        listed, total = ctypes.c_int64(0), ctypes.c_int64(0)
+        ws = workspace(st.pws_bytes, st.dev, "project")
+        lib.cbb_project_prune_stats(ws.data_ptr(), st.pws_bytes, st.n, ctypes.byref(st.dd.view),
+                                    ctypes.byref(listed), ctypes.byref(total), _lib.stream_ptr())
+        self.listed.append(listed.value / total.value if listed.value >= 0 and total.value else
+                           None)
+
+
+def _gather_rows(snap, world, group):
+    """Concatenate the ranks' parts of a parity snapshot (rank order = voxel order)."""
+    if world == 1:
+        return snap
+    import torch.distributed as dist
+    parts = [None] * world
+    dist.all_gather_object(parts, snap, group=group)
+    k = parts[0][0]
+    cat = [np.concatenate([p[i] for p in parts]) for i in range(1, 5)]
+    return (k, *cat)
+
+
+def operator_block(A, cfg, device, s):
+    """Achieved HBM GB/s of the s-channel operator calls of one IPG iteration (CUDA events, 5
+    repetitions each, after the solve), on modelled algorithmic bytes per call:
+      apply     X~ (8ns) + channel images written and FFT'd (c s n complex: 3 x 8csn incl. the
+                location-major copy) + gather (K 8csn, pattern CSR 12 Lm + 4n, y 8cLm)
+      adjoint   residual 8cLm + CSR 12 Lm + 4n + k-space images 8csn + FFT 16csn + combine 8csn + G 8ns
+      residual  AX and Y read, R written: 24 cLm
+    """
+    import torch
+    from paper_1810_01967_b200 import _lib
+    from paper_1810_01967_b200.solver import IpgState
+    lib = _lib.load()
+    n, L, m, c = A.n, A.L, A.m, getattr(A, "c", 1)
+    V = torch.from_numpy(np.ascontiguousarray(cfg.cdict.basis, dtype=np.complex64)).to(device)
+    g = torch.Generator(device=device)
+    g.manual_seed(5)
+    Xs = torch.complex(torch.randn((n, s), generator=g, device=device),
+                       torch.randn((n, s), generator=g, device=device))
+    Y = torch.empty((L, c * m), dtype=torch.complex64, device=device)
+    G = torch.empty((n, s), dtype=torch.complex64, device=device)
+    R = torch.empty_like(Y)
+    o = torch.zeros(1, dtype=torch.float64, device=device)
+    rws = torch.empty(lib.cbb_reduce_workspace_bytes(), dtype=torch.uint8, device=device)
+
+    def timed(fn, reps=5):
+        fn()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(reps):
+            fn()
+        ev[1].record()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    csr = 12 * L * m + 4 * n
+    calls = {
+        "apply": (lambda: A.fm_apply_compressed(Xs, V, out=Y),
+                  8 * n * s + 3 * 8 * c * s * n + 8 * c * s * n + csr + 8 * c * L * m),
+        "adjoint": (lambda: A.fm_adjoint_compressed(Y, V, out=G),
+                    8 * c * L * m + csr + 8 * c * s * n + 16 * c * s * n + 8 * c * s * n + 8 * n * s),
+        "residual": (lambda: _lib.check(lib.cbb_residual(Y.data_ptr(), Y.data_ptr(), Y.numel(),
+                                                         None, R.data_ptr(), o.data_ptr(),
+                                                         rws.data_ptr(), _lib.stream_ptr()),
+                                        "residual"),
+                     24 * c * L * m),
+    }
+    peak = float(measured_peaks()[0].get("hbm_gbs", 6555.2))
+    out = {"unit": "GB/s", "peak_gbs": peak}
+    for name, (fn, nbytes) in calls.items():
+        ms = timed(fn)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak}
+    del IpgState
+    return out
+
+
+def ipg_rate_large(device, peaks, which, world=1, sharded=False, group=None, parity=True,
+                   rank=0):
+    """BASELINE configs[2] / configs[4] IPG through the public solve_compressed, or through
+    sharded.solve_compressed_sharded over the ranks of `group` (voxel-sharded projection,
+    frame-sharded operator; times = max over ranks), with the SURVEY 8d roofline model of one
+    iteration.  A first, untimed solve with the same inputs takes the parity snapshots (the IPG
+    is deterministic, so the timed solve retraces it); iters_per_s uses the IPG loop time of the
+    second solve, solve_seconds the whole public call."""
     import torch
     from paper_1810_01967_b200 import workloads
     from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
@@ -223,32 +500,33 @@ def ipg_rate_large(device, peaks, which, world=1):
     s = spec["s"]
     cfg = getattr(workloads, spec["make"])(device=device)
     A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape), device=device)
-    solve = solve_compressed
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         from paper_1810_01967_b200.sharded import solve_compressed_sharded
-        solve = solve_compressed_sharded
 
-    def run(conf):
-        if world == 1:
-            return solve(cfg.Y, A, cfg.cdict, None, conf)
-        return solve(cfg.Y, A, cfg.cdict, conf)
+        def run(conf, hook=None):
+            return solve_compressed_sharded(cfg.Y, A, cfg.cdict, conf, group=group, on_iter=hook)
+    else:
+        def run(conf, hook=None):
+            return solve_compressed(cfg.Y, A, cfg.cdict, None, conf, on_iter=hook)
 
-    run(SolverConfig(mode="blip_exact", max_iters=2, zeta=2.0, compressed=s))   # warm-up
     conf = SolverConfig(mode="blip_exact", max_iters=spec["iters"], zeta=2.0, compressed=s)
+    n = int(np.prod(cfg.spatial_shape))
+    probe = _IterProbe(n) if parity else None
+    run(conf, probe)                                           # parity pass (+ warm-up)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     X, maps, gam, trace = run(conf)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     loop = trace.total_time
-    if world > 1:
+    if sharded and world > 1:
         t = torch.tensor([dt, loop], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         dt, loop = float(t[0]), float(t[1])
     its = trace.iterations
     trials = sum(r["shrinks"] + 1 for r in trace.records)
-    n, L, m, D = int(np.prod(cfg.spatial_shape)), A.L, A.m, cfg.d
+    L, m, D = A.L, A.m, cfg.d
     r = trials / its
     b_a = 8 * (n * s + 3 * n * L + 2 * m * L)
     b_ah = 8 * (m * L + 4 * n * L + n * s)
@@ -259,25 +537,46 @@ def ipg_rate_large(device, peaks, which, world=1):
     tc = float(peaks.get("bf16_tflops", 1605.7)) * 1e12 * world
     t_roof = b_iter / bw + r * f_p / tc
     t_meas = loop / its
-    return {"config": spec["config"], "n_gpus": world,
-            "sharding": "none" if world == 1 else
-            "voxel-sharded state/projection, frame-sharded s-channel operator (NCCL)",
-            "setup_seconds": cfg.setup_seconds, "iterations": its, "projection_trials": trials,
-            "loop_seconds": loop, "solve_seconds": dt, "iters_per_s": its / loop,
-            "ms_per_iter": 1e3 * t_meas, "final_fidelity": trace.fidelities()[-1],
-            "roofline_model": {
-                "model": "SURVEY 8d: B_iter(r) = B_AH + 24mL + r(B_P + B_A + 16mL) bytes at HBM "
-                         "peak + r 4snD flops at the dense tensor peak (materialised n x L "
-                         "frames; the s-channel operator moves far fewer bytes than this)",
-                "r": r, "bytes_per_iter": b_iter, "t_roof_ms": 1e3 * t_roof,
-                "frac": t_roof / t_meas}}
+    res = {"config": spec["config"], "n_gpus": world,
+           "sharding": ("voxel-sharded state/projection, frame-sharded s-channel operator (NCCL)"
+                        if sharded else "none (single-GPU solver)"),
+           "setup_seconds": cfg.setup_seconds, "iterations": its, "projection_trials": trials,
+           "loop_seconds": loop, "solve_seconds": dt, "iters_per_s": its / loop,
+           "ms_per_iter": 1e3 * t_meas, "final_fidelity": trace.fidelities()[-1],
+           "roofline_model": {
+               "model": "SURVEY 8d: B_iter(r) = B_AH + 24mL + r(B_P + B_A + 16mL) bytes at HBM "
+                        "peak + r 4snD flops at the dense tensor peak (materialised n x L frames, "
+                        "every (voxel, atom) pair screened); the s-channel operator moves fewer "
+                        "bytes and the tile pruning screens fewer pairs than this model counts",
+               "r": r, "bytes_per_iter": b_iter, "t_roof_ms": 1e3 * t_roof,
+               "frac": t_roof / t_meas}}
+    if probe is not None:
+        listed = [x for x in probe.listed if x is not None]
+        res["tile_pruning"] = {
+            "listed_tile_fraction_per_iter": probe.listed,
+            "mean_listed_fraction": float(np.mean(listed)) if listed else None,
+            "screened_pairs_fraction_model": (
+                (1.0 + sum(listed)) / (1 + len(listed)) if listed else None)}
+        snaps = [_gather_rows(probe.first, world, group), _gather_rows(probe.last, world, group)]
+        if rank == 0:
+            atoms = cfg.cdict.atoms_compressed
+            res["parity"] = {}
+            for tag, (k, rows, Z, idx, g) in zip(("first", "last"), snaps):
+                blk = parity_block(Z, atoms, idx, g)
+                blk["iteration"] = int(k)
+                res["parity"][tag] = blk
+    if rank == 0 and not sharded:
+        res["operator"] = operator_block(A, cfg, device, s)
+    del cfg, A
+    return res
 
 
-def cfg3_rate(device, world, rank, reps=2):
+def cfg3_rate(device, world, rank, group=None, reps=2):
     """BASELINE configs[3]: N = 256x256x128 = 8,388,608 voxels x D = 2^20 random unit atoms,
     s = 10.  One GPU: one exact projection.  Under torchrun: atom-sharded (each rank screens
-    D/W atoms; exact cross-rank first-index argmax by all-reduce MAX + select + all-reduce MIN,
-    rows assembled by a SUM all-reduce -- distributed.project_atom_sharded)."""
+    D/W atoms; exact cross-rank first-index argmax by all-reduce MAX + select + all-reduce MIN;
+    every rank writes the rows from its replicated dictionary -- project_atom_sharded).  Parity:
+    512 sampled voxels against all 2^20 atoms (fp64 oracle, outside the timed region)."""
     import torch
     import torch.distributed as dist
     from paper_1810_01967_b200 import device_dictionary
@@ -290,18 +589,18 @@ def cfg3_rate(device, world, rank, reps=2):
     Z, gen = cone_voxels(atoms, N, seed=3, dtype=np.complex64)
     t_gen = time.perf_counter() - t_gen
     zt = torch.from_numpy(Z).to(device)
-    del Z
     lo, hi = shard_range(D, world, rank)
     if world == 1:
         dd = device_dictionary(atoms, device)
         run = lambda: project_device(zt, dd)                     # noqa: E731
     else:
         shard = np.ascontiguousarray(atoms[lo:hi])
-        run = lambda: project_atom_sharded(zt, shard, lo)        # noqa: E731
+        run = lambda: project_atom_sharded(zt, shard, lo, group=group,   # noqa: E731
+                                           atoms_full=atoms)
     out = run()                                                  # warm-up
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=group)
     torch.cuda.synchronize()
     ev[0].record()
     for _ in range(reps):
@@ -311,21 +610,28 @@ def cfg3_rate(device, world, rank, reps=2):
     ms = ev[0].elapsed_time(ev[1]) / reps
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     ms = float(t)
-    idx = out[0]
-    agree = float((idx.cpu().numpy().astype(np.int64) == gen).mean())
-    return {"config": "BASELINE configs[3]: N=8,388,608 voxels x D=2^20 random unit atoms, s=10 "
-                      "(voxel = atom x PD~U(0.2,1) x random phase + 20 dB noise)",
-            "n_gpus": world, "sharding": "none" if world == 1 else
-            "atom-sharded (D/W per rank), exact argmax combine over NCCL",
-            "value": float(N) * D * 2 * s / (ms * 1e-3), "unit": UNIT,
-            "ms_per_projection": ms, "argmax_re_vs_generator": agree,
-            "input_generation_s": t_gen}
+    idx = out[0].cpu().numpy().astype(np.int64)
+    gam = out[1].cpu().numpy()
+    res = {"config": "BASELINE configs[3]: N=8,388,608 voxels x D=2^20 random unit atoms, s=10 "
+                     "(voxel = atom x PD~U(0.2,1) x random phase + 20 dB noise)",
+           "n_gpus": world, "sharding": "none" if world == 1 else
+           "atom-sharded (D/W per rank), exact argmax combine over NCCL, rows written locally",
+           "value": float(N) * D * 2 * s / (ms * 1e-3), "unit": UNIT,
+           "ms_per_projection": ms, "argmax_re_vs_generator": float((idx == gen).mean()),
+           "input_generation_s": t_gen}
+    if rank == 0:
+        rows = np.sort(np.random.default_rng(11).choice(N, size=PARITY_CFG3_VOXELS,
+                                                        replace=False))
+        res["parity"] = parity_block(Z[rows], atoms, idx[rows], gam[rows])
+    return res
 
 
 # ---------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def run_ours(args, rank, world, local_rank, group):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -335,7 +641,6 @@ def run_ours(args, rank, world, local_rank):
     from paper_1810_01967_b200.projection import project_device
     from paper_1810_01967_b200.workloads import cone_voxels, random_atoms
 
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     lib = _lib.load()
     atoms = random_atoms(D_ATOMS, S, seed=0)
@@ -350,17 +655,15 @@ def run_ours(args, rank, world, local_rank):
     def step():
         project_device(zt, dd, out=out)
 
-    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+    for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     lib.cbb_timing_enable(1)
-    import ctypes
     kms = ctypes.c_float(0.0)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     kernel_ms = []
-    if world > 1:
-        dist.barrier()
+    dist.barrier(group=group)
     torch.cuda.synchronize()
     launches0 = lib.cbb_stats_kernel_launches()
     with ClockSampler(local_rank) as clk:
@@ -377,11 +680,12 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    dist.barrier(group=group)
     total_ms = float(t)
     value = macs_per_step() * world * args.steps / (total_ms * 1e-3)
+    gpu_idx = out[0][:CPU_SAMPLE_VOXELS].cpu().numpy()
+    gpu_gam = out[1][:CPU_SAMPLE_VOXELS].cpu().numpy()
 
     # -------- end to end through the public numpy API (pinned host buffers)
     Zh = pinned_empty((N_VOX, S), np.complex128)
@@ -393,38 +697,53 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(3):
         res = cb.project_cone_exact(Zh, dd)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dist.barrier(group=group)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         res = cb.project_cone_exact(Zh, dd)
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX, group=group)
     e2e_s = float(te)
     agree = float(np.mean(res.indices == gen))
+    # the stock reference call: pageable complex128 numpy in, the Dictionary-like object
+    zpage = np.array(Z, dtype=np.complex128)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        cb.project_cone_exact(zpage, atoms)
+    e2e_pageable_ms = 1e3 * (time.perf_counter() - t0) / 2
+    del Zh, zpage
+    torch.cuda.empty_cache()
 
+    peaks, peak_kind = measured_peaks()
     cfg3 = None
     if not args.skip_cfg3:                      # every rank takes part (collectives)
         try:
-            cfg3 = cfg3_rate(dev, world, rank)
+            cfg3 = cfg3_rate(dev, world, rank, group)
         except Exception as exc:  # report, never hide
             cfg3 = {"error": repr(exc)}
         torch.cuda.empty_cache()
-    ipg_multi = {}
-    if world > 1:                               # every rank takes part (collectives)
-        for which in ("cfg2", "cfg4"):
-            if getattr(args, f"skip_{which}"):
-                continue
+    ipg_large = {}
+    for which in ("cfg2", "cfg4"):
+        if getattr(args, f"skip_{which}"):
+            continue
+        entry = {}
+        try:                                    # every rank takes part (collectives)
+            entry = ipg_rate_large(dev, peaks, which, world, sharded=True, group=group,
+                                   rank=rank)
+        except Exception as exc:  # report, never hide
+            entry = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+        if world == 1:                          # the single-GPU solver, for reference
             try:
-                ipg_multi[which] = ipg_rate_large(dev, measured_peaks()[0], which, world)
+                entry["unsharded"] = ipg_rate_large(dev, peaks, which, 1, sharded=False,
+                                                    parity=False)
             except Exception as exc:  # report, never hide
-                ipg_multi[which] = {"error": repr(exc)}
+                entry["unsharded"] = {"error": repr(exc)}
             torch.cuda.empty_cache()
+        ipg_large[which] = entry
     if rank != 0:
         return 0
-    peaks, peak_kind = measured_peaks()
     flops = 4.0 * S * N_VOX * D_ATOMS
     kmean = statistics.mean(kernel_ms)
     achieved = flops / (kmean * 1e-3) / 1e12
@@ -457,61 +776,144 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": N_VOX * (8 + 8 + S * 16),
                 "path": "paper_1810_01967_b200.project_cone_exact(numpy complex128, pinned) -> "
                         "ConeProjection(int64, float64, complex128)",
-                "ms_per_step": 1e3 * e2e_s / e2e_steps},
+                "ms_per_step": 1e3 * e2e_s / e2e_steps,
+                "pageable_ms_per_step": e2e_pageable_ms,
+                "pageable_value": macs_per_step() / (e2e_pageable_ms * 1e-3),
+                "pageable_path": "stock reference call: pageable numpy complex128 and the atom "
+                                 "array (dictionary prepared on first use, cached)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "argmax_re_vs_generator": agree,
     }
-    for which, res in ipg_multi.items():
+    for which, res in ipg_large.items():
         line[f"ipg_{which}"] = res
     if cfg3 is not None:
         line["cfg3"] = cfg3
+    parity = {}
     if world == 1:
-        line["cpu_baseline"] = cpu_baseline(atoms, Z)
+        line["cpu_baseline"] = cpu_baseline(atoms, Z, gpu_idx, gpu_gam)
+        parity["cfg1"] = line["cpu_baseline"]["parity_cfg1"]
+        if not args.skip_cpu_reference:
+            try:
+                line["cpu_baseline"]["reference_legs"] = cpu_reference_legs()
+            except Exception as exc:  # report, never hide
+                line["cpu_baseline"]["reference_legs"] = {"error": repr(exc)}
         try:
             line["ipg"] = ipg_rate(dev)
         except Exception as exc:  # report, never hide
             line["ipg"] = {"error": repr(exc)}
-        for which in ("cfg2", "cfg4"):
-            if getattr(args, f"skip_{which}"):
-                continue
-            try:
-                line[f"ipg_{which}"] = ipg_rate_large(dev, peaks, which)
-            except Exception as exc:  # report, never hide
-                line[f"ipg_{which}"] = {"error": repr(exc)}
-            torch.cuda.empty_cache()
-    print(json.dumps(line), flush=True)
+    if cfg3 is not None and "parity" in cfg3:
+        parity["cfg3"] = cfg3["parity"]
+    for which, res in ipg_large.items():
+        if "parity" in res:
+            parity[which] = res["parity"]
+    line["parity"] = parity
+    emit(line)
     return 0
 
 
+# ---------------------------------------------------------------- launcher
+def relaunch(args):
+    """``--gpus N`` outside a launcher: re-execute this script under torch.distributed.run with N
+    ranks (one per GPU) and let rank 0 print the JSON line."""
+    argv = [a for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={args.master_port}", os.path.abspath(__file__)] + argv
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world):
+    """Launcher check without GPUs (gloo): every rank contributes (rank + 1) units; the line
+    reports the aggregate over all ranks and n_gpus = world."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t)
+    ranks = [None] * world
+    dist.all_gather_object(ranks, rank)
+    if rank == 0:
+        emit({"dry_run": True, "n_gpus": world, "ranks": ranks, "value": float(t),
+              "unit": "rank units"})
+    dist.destroy_process_group()
+    return 0
+
+
+_OUT = sys.stdout
+
+
+def emit(line):
+    """The one JSON line, on the original stdout (libraries' own stdout output -- e.g. NCCL's
+    version banner -- is redirected to stderr, so stdout carries nothing else)."""
+    _OUT.write(json.dumps(line) + "\n")
+    _OUT.flush()
+
+
+def _stdout_to_stderr():
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _stdout_to_stderr()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--master-port", type=int, default=29531)
     ap.add_argument("--skip-cfg2", action="store_true", help="skip the cfg2 IPG measurement")
     ap.add_argument("--skip-cfg3", action="store_true",
                     help="skip the cfg3 (8.4M voxels x 2^20 atoms) projection")
     ap.add_argument("--skip-cfg4", action="store_true",
                     help="skip the cfg4 (256x256x64, L=500) 3-D IPG measurement")
+    ap.add_argument("--skip-cpu-reference", action="store_true",
+                    help="skip the reference package's CPU IPG / cover-tree legs")
+    ap.add_argument("--dry-run-gloo", action="store_true",
+                    help="launcher self-test on CPU ranks (gloo), no GPU work")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if not args.dry_run_gloo:
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                emit({"error": f"--gpus {args.gpus} but {have} GPUs are visible",
+                      "n_gpus": args.gpus})
+                return 1
+        return relaunch(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run_gloo:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(args.master_port))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(args.master_port))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    # one NCCL group at every N (world 1 included): the sharded IPG runs the same code path at
+    # N = 1 and N > 1, so the scaling curve compares like with like
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        return run_ours(args, rank, world, local_rank)
+        return run_ours(args, rank, world, local_rank, dist.group.WORLD)
     finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -9,8 +9,11 @@
   ``projection.py:62`` is recovered EXACTLY with two collectives over NCCL:
       all-reduce MAX of the fp64 scores  ->  cand = (score == max) ? idx : INT64_MAX
       (``cbb_argmax_select``)  ->  all-reduce MIN of cand.
-  No precision is lost (no packing of a rounded score with the index).  The owner shard
-  writes gamma * d_j* (``cbb_scaled_rows``) and a SUM all-reduce assembles the rows.
+  No precision is lost (no packing of a rounded score with the index).  Every rank then
+  writes all projected rows gamma * d_j* itself from a replicated copy of the dictionary
+  (``cbb_scaled_rows`` over the full view: 2^20 x 10 complex atoms are 168 MB of fp64 rows),
+  so the n x s rows never cross NVLink; without the replicated copy the owner shard writes its
+  rows and a SUM all-reduce assembles them.
 
 The collectives go through ``torch.distributed`` (NCCL on the box, gloo in the CPU tests).
 """
@@ -62,9 +65,11 @@ def combine_atom_shards(score: torch.Tensor, gidx: torch.Tensor, group=None,
 
 
 def project_atom_sharded(Z: torch.Tensor, atoms_shard, atom_offset: int, group=None,
-                         proj_c128=False):
+                         proj_c128=False, atoms_full=None):
     """Atom-sharded exact projection of the (replicated) voxels Z on this rank's shard.
 
+    ``atoms_full`` (optional, the whole dictionary or its ``DeviceDictionary``): the projected
+    rows are written locally from it instead of being summed over the ranks.
     Returns (indices int64, gammas float64, projected) identical on every rank.
     """
     from .dictionary import device_dictionary
@@ -83,6 +88,12 @@ def project_atom_sharded(Z: torch.Tensor, atoms_shard, atom_offset: int, group=N
     gamma = torch.clamp(gscore, min=0.0)
     proj = torch.empty((n, dd.s), dtype=torch.complex128 if proj_c128 else torch.complex64,
                        device=Z.device)
+    if atoms_full is not None:       # every rank owns every atom: local rows, no collective
+        full = device_dictionary(atoms_full, Z.device)
+        _lib.check(lib.cbb_scaled_rows(ctypes.byref(full.view), 0, gidx.data_ptr(),
+                                       gamma.data_ptr(), n, proj.data_ptr(), int(proj_c128),
+                                       _lib.stream_ptr()), "cbb_scaled_rows")
+        return gidx, gamma, proj
     _lib.check(lib.cbb_scaled_rows(ctypes.byref(dd.view), int(atom_offset), gidx.data_ptr(),
                                    gamma.data_ptr(), n, proj.data_ptr(), int(proj_c128),
                                    _lib.stream_ptr()), "cbb_scaled_rows")
