@@ -823,7 +823,7 @@ def relaunch(args):
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    return subprocess.call(cmd, env=env)
+    return subprocess.call(cmd, env=env, stdout=_OUT)   # the ranks' JSON line -> our stdout
 
 
 def dry_run(args, rank, world):
