@@ -154,7 +154,9 @@ int cbb_debug_tc_scores(void* workspace, const cbb_dict_view* dict, int32_t a_ti
 /* ---- Cartesian operator (forward_model.py:123-167) + subspace maps (dictionary.py:116-122) ---- */
 typedef struct cbb_op cbb_op;
 /* spatial dims (ndim 2 or 3), L frames, m samples per frame, pattern (L x m int32 device,
- * flat C-order index per sample).  flags bit 0: identity_transform hook (no DFT). */
+ * flat C-order index per sample).  flags bit 0: identity_transform hook (no DFT).  Builds the
+ * pattern's CSR on the legacy default stream and synchronises that stream; L*m and n must stay
+ * below 2^31 (status 3 otherwise). */
 int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const int32_t* pattern,
                   int32_t flags, cbb_op** out);
 /* Coil sensitivity maps S (forward_model.py:82-113,132-167): c x n complex64 device array
@@ -163,6 +165,9 @@ int cbb_op_create(int32_t ndim, const int32_t* dims, int32_t L, int32_t m, const
 int cbb_op_set_coils(cbb_op* op, int32_t c, const void* coil_maps);
 int cbb_op_destroy(cbb_op* op);
 size_t cbb_op_workspace_bytes(const cbb_op* op);
+/* Workspace of the compressed (s-channel) calls with rank s only: 2 c s n complex64 + partials
+ * (the uncompressed calls need cbb_op_workspace_bytes). */
+size_t cbb_op_workspace_bytes_compressed(const cbb_op* op, int32_t s);
 /* Y = A X.  X: n x L complex64 voxel-major (reference layout); Y: L x m complex64
  * FRAME-major (Y_fm[t][i] = Y_ref[i][t]; the Python shim transposes at the boundary). */
 int cbb_op_apply(cbb_op* op, const void* X, void* Y, void* workspace, void* stream);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "cbb_op_destroy": (c_int, [c_vp]),
     "cbb_op_set_coils": (c_int, [c_vp, c_i32, c_vp]),
     "cbb_op_workspace_bytes": (c_size, [c_vp]),
+    "cbb_op_workspace_bytes_compressed": (c_size, [c_vp, c_i32]),
     "cbb_op_apply": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "cbb_op_adjoint": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "cbb_op_apply_compressed": (c_int, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),

@@ -48,6 +48,7 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int f
 int op_destroy(Op* op);
 int op_set_coils(Op* op, int c, const float2* coils);
 size_t op_ws_bytes(const Op* op);
+size_t op_ws_bytes_compressed(const Op* op, int s);
 int op_apply(Op* op, const float2* X, float2* Y, void* ws, cudaStream_t st);
 int op_adjoint(Op* op, const float2* Y, float2* X, void* ws, cudaStream_t st);
 int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2* Y, void* ws,
@@ -302,6 +303,9 @@ int cbb_op_destroy(cbb_op* op) {
 }
 
 size_t cbb_op_workspace_bytes(const cbb_op* op) { return op ? op_ws_bytes(op->impl) : 0; }
+size_t cbb_op_workspace_bytes_compressed(const cbb_op* op, int32_t s) {
+  return (op && s >= 1) ? op_ws_bytes_compressed(op->impl, s) : 0;
+}
 
 int cbb_op_apply(cbb_op* op, const void* X, void* Y, void* workspace, void* stream) {
   return op_apply(op->impl, static_cast<const float2*>(X), static_cast<float2*>(Y), workspace,

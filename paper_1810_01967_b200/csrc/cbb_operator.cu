@@ -122,6 +122,22 @@ __global__ void __launch_bounds__(256) scatter_kernel(const float2* __restrict__
   }
 }
 
+// Exact e / m for 0 <= e < 2^32, m >= 2: floor(e * ceil(2^64 / m) / 2^64) (the rounding error
+// e (ceil - 2^64/m) / 2^64 < 2^-32 stays below 1/m, the smallest nonzero fractional part).
+struct DivM {
+  uint64_t magic;  // ceil(2^64 / m); 0 for m == 1
+  int m;
+  __host__ static DivM make(int m) {
+    DivM d;
+    d.m = m;
+    d.magic = m > 1 ? ~uint64_t(0) / uint64_t(m) + 1 : 0;
+    return d;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t e) const {
+    return magic ? uint32_t(__umul64hi(uint64_t(e), magic)) : e;
+  }
+};
+
 // ---------------------------------------------------------------- s-channel compressed operator
 // C[(ci*s + k)*n + v] = S_ci[v] * Xc[v*s + k]   (coils == nullptr -> S = 1)
 __global__ void __launch_bounds__(256) channels_kernel(const float2* __restrict__ Xc,
@@ -225,10 +241,11 @@ constexpr int kLocThreads = 512;  // 2 blocks x 512 threads per SM: all kRedBloc
 template <int S>
 __global__ void __launch_bounds__(kLocThreads) gather_loc_kernel(
     const float2* __restrict__ KT, const int* __restrict__ csr_off,
-    const int64_t* __restrict__ csr_e, int64_t n, int m, int c, int s,
+    const int* __restrict__ csr_e, int64_t n, DivM dm, int c, int s,
     const float2* __restrict__ V, float scale, int mode, const float2* __restrict__ Ymeas,
     const float* __restrict__ w, float2* __restrict__ Y, double* __restrict__ partial) {
   __shared__ double sh[kLocThreads];
+  const int m = dm.m;
   const int64_t cm = int64_t(c) * m;
   double acc = 0.0;
   for (int64_t wloc = int64_t(blockIdx.x) * kLocThreads + threadIdx.x; wloc < n;
@@ -240,10 +257,10 @@ __global__ void __launch_bounds__(kLocThreads) gather_loc_kernel(
 #pragma unroll
       for (int k = 0; k < S; ++k) kr[k] = k < s ? kb[k] : make_float2(0.f, 0.f);
       for (int j = b; j < e_end; ++j) {
-        const int64_t e = csr_e[j];
-        const int64_t t = e / m;
-        const int64_t eo = t * cm + int64_t(ci) * m + (e - t * m);
-        const float2* vt = V + t * s;
+        const uint32_t e = uint32_t(csr_e[j]);
+        const uint32_t t = dm.div(e);
+        const int64_t eo = int64_t(t) * cm + int64_t(ci) * m + (e - t * uint32_t(m));
+        const float2* vt = V + int64_t(t) * s;
         float yr = 0.f, yi = 0.f;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -274,6 +291,113 @@ __global__ void __launch_bounds__(kLocThreads) gather_loc_kernel(
   }
 }
 
+// Location-tiled gather (every frame's pattern row sorted ascending): a CTA stages the channel
+// values of W consecutive k-space locations from the channel-planar FFT output into shared
+// memory (one coalesced pass, swizzled against bank conflicts), then for every frame t the
+// samples of those locations are the contiguous segment [seg[t][b], seg[t][b+1]) of row t:
+// pattern reads and y writes are contiguous.  Same products in the same FMA order per sample
+// as gather_s_kernel / gather_loc_kernel (identical y).  Norm / residual partials per CTA over a
+// fixed tile assignment (deterministic).
+__device__ __forceinline__ int tile_swz(int wl) { return wl ^ ((wl >> 4) & 15); }
+
+template <int S>
+__global__ void __launch_bounds__(256) gather_tile_kernel(
+    const float2* __restrict__ C, const int* __restrict__ pat, const int* __restrict__ seg,
+    int nb, int W, int64_t n, int L, int m, int c, int s, const float2* __restrict__ V,
+    float scale, int mode, const float2* __restrict__ Ymeas, const float* __restrict__ w,
+    float2* __restrict__ Y, double* __restrict__ partial) {
+  extern __shared__ float2 kt[];  // [c*s][W], swizzled columns
+  __shared__ double sh[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cm = int64_t(c) * m;
+  double acc = 0.0;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t w0 = int64_t(b) * W;
+    const int wn = int(n - w0 < W ? n - w0 : W);
+    __syncthreads();  // previous tile fully consumed
+    for (int q = 0; q < c * s; ++q)
+      for (int j = threadIdx.x; j < wn; j += blockDim.x)
+        kt[q * W + tile_swz(j)] = C[int64_t(q) * n + w0 + j];
+    __syncthreads();
+    const int* sb = seg + int64_t(b) * L;  // row b: first sample >= b W; row b + 1: the end
+    // warp w takes the frame groups [32 g, 32 g + 32) with g = w (mod 8); lane j fetches the
+    // segment of frame 32 g + j, then the warp walks the group's non-empty segments
+    for (int t0 = 32 * warp; t0 < L; t0 += 32 * 8) {
+      const int tl = t0 + lane;
+      const int my_lo = tl < L ? sb[tl] : 0, my_hi = tl < L ? sb[L + tl] : 0;
+      uint32_t busy = __ballot_sync(0xffffffffu, my_hi > my_lo);
+      while (busy) {
+        const int j = __ffs(busy) - 1;
+        busy &= busy - 1;
+        const int t = t0 + j;
+        const int lo = __shfl_sync(0xffffffffu, my_lo, j), hi = __shfl_sync(0xffffffffu, my_hi, j);
+        float2 vr[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) vr[k] = k < s ? V[int64_t(t) * s + k] : make_float2(0.f, 0.f);
+        for (int i = lo + lane; i < hi; i += 32) {
+          const int sw = tile_swz(pat[int64_t(t) * m + i] - int(w0));
+          for (int ci = 0; ci < c; ++ci) {
+            const float2* kc = kt + ci * s * W + sw;
+            float yr = 0.f, yi = 0.f;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              if (k < s) {
+                const float2 a = kc[k * W], bv = vr[k];
+                yr = fmaf(a.x, bv.x, fmaf(a.y, bv.y, yr));   // a * conj(b)
+                yi = fmaf(a.y, bv.x, fmaf(-a.x, bv.y, yi));
+              }
+            }
+            const int64_t eo = int64_t(t) * cm + int64_t(ci) * m + i;
+            float2 y = make_float2(yr * scale, yi * scale);
+            if (mode == 2) {
+              const float2 ym = Ymeas[eo];
+              y.x -= ym.x;
+              y.y -= ym.y;
+              const float ww = w ? w[eo] : 1.f;
+              acc += double(ww) * (double(y.x) * y.x + double(y.y) * y.y);
+              Y[eo] = make_float2(ww * y.x, ww * y.y);
+            } else {
+              if (mode == 0) Y[eo] = y;
+              acc += double(y.x) * y.x + double(y.y) * y.y;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (partial) {
+    double r = block_sum_256(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+  }
+}
+
+// seg[b][t] = first sample of frame t at a location >= b W (rows sorted ascending), b = 0..nb
+// (row nb = m): tile b's segments are rows b and b + 1, each L contiguous entries
+__global__ void seg_table_kernel(const int* __restrict__ pat, int L, int m, int nb, int W,
+                                 int* __restrict__ seg) {
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= int64_t(L) * (nb + 1)) return;
+  const int b = int(g / L), t = int(g - int64_t(b) * L);
+  const int* row = pat + int64_t(t) * m;
+  const int64_t key = int64_t(b) * W;
+  int lo = 0, hi = m;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (row[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  seg[g] = lo;
+}
+
+// flag = 1 if some frame's pattern row is not strictly ascending
+__global__ void rows_sorted_kernel(const int* __restrict__ pat, int L, int m, int* flag) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(L) * m;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(e % m);
+    if (i + 1 < m && pat[e + 1] <= pat[e]) *flag = 1;
+  }
+}
+
 // K[(ci*s + k)*n + w] = sum over the pattern entries e = t*m + i with Omega_t(i) = w (CSR,
 // ascending e) of R[t][ci*m + i] * V[t*s + k].  One thread per k-space location: each sample of
 // R is read once and feeds all s channel accumulators (registers, S >= s); unsampled locations
@@ -282,23 +406,24 @@ __global__ void __launch_bounds__(kLocThreads) gather_loc_kernel(
 template <int S>
 __global__ void __launch_bounds__(256) kspace_s_kernel(const float2* __restrict__ R,
                                                        const int* __restrict__ csr_off,
-                                                       const int64_t* __restrict__ csr_e,
-                                                       int64_t n, int m, int c, int s,
+                                                       const int* __restrict__ csr_e,
+                                                       int64_t n, DivM dm, int c, int s,
                                                        const float2* __restrict__ V,
                                                        float2* __restrict__ K) {
   const int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (wloc >= n) return;
   const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
+  const int m = dm.m;
   const int64_t cm = int64_t(c) * m;
   for (int ci = 0; ci < c; ++ci) {
     float2 acc[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) acc[k] = make_float2(0.f, 0.f);
     for (int j = b; j < e_end; ++j) {
-      const int64_t e = csr_e[j];
-      const int64_t t = e / m, i = e - t * m;
-      const float2 r = R[t * cm + int64_t(ci) * m + i];
-      const float2* vt = V + t * s;
+      const uint32_t e = uint32_t(csr_e[j]);
+      const uint32_t t = dm.div(e), i = e - t * uint32_t(m);
+      const float2 r = R[int64_t(t) * cm + int64_t(ci) * m + i];
+      const float2* vt = V + int64_t(t) * s;
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         if (k < s) {
@@ -437,7 +562,11 @@ struct Op {
   int chan_batch[4];     // cached plans for batches of c*s channel images
   cufftHandle chan_plan[4];
   int* csr_off;          // n + 1 offsets into csr_e (s-channel adjoint)
-  int64_t* csr_e;        // pattern entries t*m + i sorted by k-space location (stable)
+  int* csr_e;            // pattern entries t*m + i (int32) sorted by k-space location (stable)
+  DivM dm;               // e -> (t, i) = (e / m, e % m)
+  bool rows_sorted;      // every frame's pattern row strictly ascending: location-tiled gather
+  int seg_W[4];          // cached segment tables of the tiled gather, per tile width W
+  int* seg_tab[4];
   float scale;           // 1/sqrt(n) (1 for the identity hook)
   bool identity;         // forward_model.py:95,137,163 identity_transform test hook: skip the DFT
 };
@@ -448,19 +577,29 @@ static int grid_for(int64_t work, int per_block = 256) {
   return int(g > 0 ? g : 1);
 }
 
-// workspace: max(frame stack L*n, 2 x c*32 channel images: planar FFT buffer + its
-// location-major copy) + per-coil reduction partials
+// Workspace.  Uncompressed calls need the (L, n) frame stack; s-channel calls the c*s channel
+// images (planar FFT buffer) and their location-major copy (untiled gather only): 2 c s n.
+// Then the reduction partials (one per CTA of the largest reduction grid).
+static size_t ws_round(size_t b) { return (b + 255) & ~size_t(255); }
+constexpr int kTileBlocks = 2048;  // max CTAs (= partial slots) of the tiled gather
+static size_t ws_partials_bytes(const Op* op) {
+  const size_t slots = size_t(op->c) * kRedBlocks > kTileBlocks ? size_t(op->c) * kRedBlocks
+                                                                 : size_t(kTileBlocks);
+  return slots * sizeof(double) + 256;
+}
 static size_t ws_main_bytes(const Op* op) {
   const size_t frames = size_t(op->L) * op->n * sizeof(float2);
   const size_t chans = size_t(op->c) * 64 * op->n * sizeof(float2);
-  return ((frames > chans ? frames : chans) + 255) & ~size_t(255);
+  return ws_round(frames > chans ? frames : chans);
 }
-size_t op_ws_bytes(const Op* op) {
-  return ws_main_bytes(op) + size_t(op->c) * kRedBlocks * sizeof(double) + 256;
+size_t op_ws_bytes(const Op* op) { return ws_main_bytes(op) + ws_partials_bytes(op); }
+size_t op_ws_bytes_compressed(const Op* op, int s) {
+  return ws_round(size_t(op->c) * 2 * s * op->n * sizeof(float2)) + ws_partials_bytes(op);
 }
 static float2* ws_frames(void* ws) { return static_cast<float2*>(ws); }
-static double* ws_partial(const Op* op, void* ws) {
-  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + ws_main_bytes(op));
+// partials sit after the main area: `main` is the caller's layout (full or compressed)
+static double* ws_partial_at(void* ws, size_t main) {
+  return reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + main);
 }
 
 static int make_plan(const Op* op, int batch, cufftHandle* plan) {
@@ -473,25 +612,37 @@ static int make_plan(const Op* op, int batch, cufftHandle* plan) {
   return kOk;
 }
 
-// CSR of the pattern by k-space location: stable sort of the L*m flat entries by Omega value.
+// CSR of the pattern by k-space location: stable sort of the L*m flat entries (int32) by Omega
+// value, and the row-order check of the tiled gather.  Runs on the legacy default stream (the
+// pattern upload precedes it there) and synchronises that stream only.
 static int build_csr(Op* op) {
   const int64_t total = int64_t(op->L) * op->m;
   int* keys = nullptr;
+  int* flag = nullptr;
+  const cudaStream_t st = 0;
   CBB_CUDA_TRY(cudaMalloc(&op->csr_off, sizeof(int) * size_t(op->n + 1)));
-  CBB_CUDA_TRY(cudaMalloc(&op->csr_e, sizeof(int64_t) * size_t(total)));
+  CBB_CUDA_TRY(cudaMalloc(&op->csr_e, sizeof(int) * size_t(total)));
   CBB_CUDA_TRY(cudaMalloc(&keys, sizeof(int) * size_t(total)));
-  CBB_CUDA_TRY(cudaMemcpy(keys, op->pattern, sizeof(int) * size_t(total),
-                          cudaMemcpyDeviceToDevice));
-  thrust::sequence(thrust::device, op->csr_e, op->csr_e + total);
-  thrust::stable_sort_by_key(thrust::device, keys, keys + total, op->csr_e);
-  thrust::lower_bound(thrust::device, keys, keys + total, thrust::counting_iterator<int>(0),
+  CBB_CUDA_TRY(cudaMalloc(&flag, sizeof(int)));
+  CBB_CUDA_TRY(cudaMemcpyAsync(keys, op->pattern, sizeof(int) * size_t(total),
+                               cudaMemcpyDeviceToDevice, st));
+  CBB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  rows_sorted_kernel<<<grid_for(total), 256, 0, st>>>(op->pattern, op->L, op->m, flag);
+  auto pol = thrust::cuda::par.on(st);
+  thrust::sequence(pol, op->csr_e, op->csr_e + total);
+  thrust::stable_sort_by_key(pol, keys, keys + total, op->csr_e);
+  thrust::lower_bound(pol, keys, keys + total, thrust::counting_iterator<int>(0),
                       thrust::counting_iterator<int>(int(op->n) + 1), op->csr_off);
-  cudaError_t e = cudaDeviceSynchronize();
+  int unsorted = 1;
+  cudaError_t e = cudaMemcpyAsync(&unsorted, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(keys);
+  cudaFree(flag);
   if (e != cudaSuccess) {
     set_last_error(cudaGetErrorString(e));
     return kErrCuda;
   }
+  op->rows_sorted = unsorted == 0;
   return kOk;
 }
 
@@ -508,8 +659,15 @@ int op_create(int ndim, const int* dims, int L, int m, const int* pattern, int f
     op->dims[i] = dims[i];
     op->n *= dims[i];
   }
+  // int32 CSR (offsets and entries t*m + i) and int32 FFT sizes
+  if (int64_t(L) * m >= (int64_t(1) << 31) || op->n >= (int64_t(1) << 31) - 1) {
+    set_last_error("cbb_op_create: L*m and n must stay below 2^31");
+    delete op;
+    return kErrUnsupported;
+  }
   op->L = L;
   op->m = m;
+  op->dm = DivM::make(m);
   op->c = 1;
   op->pattern = pattern;
   op->identity = (flags & 1) != 0;
@@ -538,7 +696,43 @@ int op_destroy(Op* op) {
   }
   if (op->csr_off) cudaFree(op->csr_off);
   if (op->csr_e) cudaFree(op->csr_e);
+  for (int i = 0; i < 4; ++i)
+    if (op->seg_tab[i]) cudaFree(op->seg_tab[i]);
   delete op;
+  return kOk;
+}
+
+// Tile width of the location-tiled gather: the largest power of two (<= 2048, and not far past
+// n) whose c*s planes fit 40 KB of shared memory (several CTAs per SM hide the pattern loads).
+static int tile_width(const Op* op, int s) {
+  int W = 2048;
+  while (W > 32 && (size_t(op->c) * s * W * sizeof(float2) > 40 * 1024 || W / 2 >= op->n)) W >>= 1;
+  return W;
+}
+
+// Segment table of the tiled gather for width W (built once per W, stream-ordered).
+static int seg_table(Op* op, int W, cudaStream_t st, const int** out) {
+  for (int i = 0; i < 4; ++i)
+    if (op->seg_W[i] == W) {
+      *out = op->seg_tab[i];
+      return kOk;
+    }
+  int slot = -1;
+  for (int i = 0; i < 4 && slot < 0; ++i)
+    if (op->seg_W[i] == 0) slot = i;
+  if (slot < 0) {
+    set_last_error("too many distinct tile widths");
+    return kErrUnsupported;
+  }
+  const int nb = int((op->n + W - 1) / W);
+  const int64_t cnt = int64_t(op->L) * (nb + 1);
+  CBB_CUDA_TRY(cudaMalloc(&op->seg_tab[slot], sizeof(int) * size_t(cnt)));
+  seg_table_kernel<<<unsigned((cnt + 255) / 256), 256, 0, st>>>(op->pattern, op->L, op->m, nb,
+                                                                 W, op->seg_tab[slot]);
+  CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  op->seg_W[slot] = W;
+  *out = op->seg_tab[slot];
   return kOk;
 }
 
@@ -631,21 +825,62 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   CBB_CUDA_TRY(cudaGetLastError());
   int rc = fft_channels(op, C, op->c * s, CUFFT_FORWARD, st);
   if (rc) return rc;
-  float2* KT = C + size_t(op->c) * s * op->n;
-  interleave_kernel<<<unsigned((int64_t(op->c) * op->n + 255) / 256), 256, 0, st>>>(
-      C, op->c, s, op->n, KT);
-  CBB_CUDA_TRY(cudaGetLastError());
-  double* part = ws_partial(op, ws);
+  double* part = ws_partial_at(ws, ws_round(size_t(op->c) * 2 * s * op->n * sizeof(float2)));
   int mode = 0;
   if (Y == nullptr) mode = 1;
   else if (Ymeas != nullptr) mode = 2;
   double* pp = (mode != 0 || norm_out) ? part : nullptr;
+  int launches = 2;
+  if (op->rows_sorted && int64_t(op->L) * op->m >= 4 * op->n) {
+    // location-tiled gather straight from the channel-planar FFT output
+    const int W = tile_width(op, s);
+    const int nb = int((op->n + W - 1) / W);
+    const int* seg = nullptr;
+    if ((rc = seg_table(op, W, st, &seg))) return rc;
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int grid = 8 * sms;
+    if (grid > kTileBlocks) grid = kTileBlocks;
+    if (grid > nb) grid = nb;
+    const size_t smem = size_t(op->c) * s * W * sizeof(float2);
+#define CBB_GTILE(SP)                                                                        \
+  do {                                                                                       \
+    gather_tile_kernel<SP><<<grid, 256, smem, st>>>(C, op->pattern, seg, nb, W, op->n, op->L,  \
+                                                    op->m, op->c, s, V, op->scale, mode, Ymeas, \
+                                                    w, Y, pp);                                 \
+  } while (0)
+    if (s <= 4) CBB_GTILE(4);
+    else if (s <= 8) CBB_GTILE(8);
+    else if (s <= 12) CBB_GTILE(12);
+    else if (s <= 16) CBB_GTILE(16);
+    else if (s <= 20) CBB_GTILE(20);
+    else if (s <= 24) CBB_GTILE(24);
+    else CBB_GTILE(32);
+#undef CBB_GTILE
+    CBB_CUDA_TRY(cudaGetLastError());
+    if (norm_out) {
+      count_launches(launches + 1);
+      return finish(part, grid, norm_out, st);
+    }
+    count_launches(launches);
+    return kOk;
+  }
+  float2* KT = C + size_t(op->c) * s * op->n;
+  interleave_kernel<<<unsigned((int64_t(op->c) * op->n + 255) / 256), 256, 0, st>>>(
+      C, op->c, s, op->n, KT);
+  CBB_CUDA_TRY(cudaGetLastError());
+  ++launches;
   // location-major when locations are sampled >= 4 times and there are enough of them to fill
   // the GPU with threads (cfg0's 4096 locations run faster sample-major)
   if (int64_t(op->L) * op->m >= 4 * op->n && op->n >= 65536) {
 #define CBB_GLOC(SP)                                                                          \
-  gather_loc_kernel<SP><<<kRedBlocks, kLocThreads, 0, st>>>(KT, op->csr_off, op->csr_e, op->n, op->m,  \
-                                                    op->c, s, V, op->scale, mode, Ymeas, w, Y, pp)
+  gather_loc_kernel<SP><<<kRedBlocks, kLocThreads, 0, st>>>(KT, op->csr_off, op->csr_e, op->n, \
+                                                            op->dm, op->c, s, V, op->scale,  \
+                                                            mode, Ymeas, w, Y, pp)
     if (s <= 4) CBB_GLOC(4);
     else if (s <= 8) CBB_GLOC(8);
     else if (s <= 12) CBB_GLOC(12);
@@ -659,7 +894,7 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
                                                 V, op->scale, mode, Ymeas, w, Y, pp);
   }
   CBB_CUDA_TRY(cudaGetLastError());
-  count_launches(norm_out ? 4 : 3);
+  count_launches(norm_out ? launches + 1 : launches);
   if (norm_out) return finish(part, kRedBlocks, norm_out, st);
   return kOk;
 }
@@ -672,7 +907,7 @@ int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float
   {
     const unsigned grid = unsigned((op->n + 255) / 256);
 #define CBB_KSPACE(SP)                                                                    \
-  kspace_s_kernel<SP><<<grid, 256, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->m, op->c, s, \
+  kspace_s_kernel<SP><<<grid, 256, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->dm, op->c, s, \
                                             V, K)
     if (s <= 4) CBB_KSPACE(4);
     else if (s <= 8) CBB_KSPACE(8);

@@ -138,6 +138,7 @@ class ForwardOperator:
                 handle, self.c, None if self._coils_dev is None else self._coils_dev.data_ptr()),
                 "cbb_op_set_coils")
             self._ws_bytes = int(lib.cbb_op_workspace_bytes(handle))
+            self._wsbuf = {}    # per-operator workspaces (freed with the operator)
         else:
             if matrix is None:
                 raise ValueError("gaussian operator needs a matrix")
@@ -196,8 +197,17 @@ class ForwardOperator:
         return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.complex64)).to(
             self.device)
 
-    def _ws(self):
-        return workspace(self._ws_bytes, self.device, f"op{id(self)}")
+    def _ws(self, s=None):
+        """This operator's workspace: the frame-stack layout of the uncompressed calls, or the
+        s-channel layout (2 c s n complex64 + partials) of the compressed calls with rank s."""
+        key = "full" if s is None else int(s)
+        nbytes = (self._ws_bytes if s is None else
+                  int(_lib.load().cbb_op_workspace_bytes_compressed(self._op, int(s))))
+        buf = self._wsbuf.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._wsbuf[key] = buf
+        return buf
 
     @property
     def cm(self) -> int:
@@ -236,7 +246,7 @@ class ForwardOperator:
         Y = out if out is not None else torch.empty((self.L, self.cm), dtype=torch.complex64,
                                                     device=self.device)
         _lib.check(_lib.load().cbb_op_apply_compressed(self._op, Xc.data_ptr(), V.data_ptr(), s,
-                                                       Y.data_ptr(), self._ws().data_ptr(),
+                                                       Y.data_ptr(), self._ws(s).data_ptr(),
                                                        _lib.stream_ptr()),
                    "cbb_op_apply_compressed")
         return Y
@@ -250,7 +260,7 @@ class ForwardOperator:
             return _norm2(Y, out)
         _lib.check(_lib.load().cbb_op_apply_norm2_compressed(self._op, Xc.data_ptr(),
                                                              V.data_ptr(), s, out.data_ptr(),
-                                                             self._ws().data_ptr(),
+                                                             self._ws(s).data_ptr(),
                                                              _lib.stream_ptr()),
                    "cbb_op_apply_norm2_compressed")
         return out
@@ -265,7 +275,7 @@ class ForwardOperator:
         G = out if out is not None else torch.empty((self.n, s), dtype=torch.complex64,
                                                     device=self.device)
         _lib.check(_lib.load().cbb_op_adjoint_compressed(self._op, R.data_ptr(), V.data_ptr(), s,
-                                                         G.data_ptr(), self._ws().data_ptr(),
+                                                         G.data_ptr(), self._ws(s).data_ptr(),
                                                          _lib.stream_ptr()),
                    "cbb_op_adjoint_compressed")
         return G
