@@ -148,10 +148,36 @@ __device__ __forceinline__ float dot_atom32(const float* zr, const float* zi,
   return acc;
 }
 
+// np.argmax order on (score, index): NaN is the maximum (the first NaN wins), then the larger
+// score, then the lower index (projection.py:62 on rows with non-finite scores).
+__device__ __forceinline__ bool argmax_better(double a, int64_t ja, double b, int64_t jb) {
+  const bool na = a != a, nb = b != b;
+  if (na || nb) return na && (!nb || ja < jb);
+  return a > b || (a == b && ja < jb);
+}
+
+// Rows with a non-finite component: the reference's score block Re(Z @ D^H) (projection.py:61,
+// numpy -> OpenBLAS zgemm) is NaN for EVERY atom of such a row (the complex kernel multiplies
+// the infinite component by zero parts), so np.argmax returns atom 0; gamma is then
+// _gammas_for's einsum with atom 0 (projection.py:38-42), i.e. the plain fp64 dot.
+template <int S>
+__device__ __forceinline__ bool nonfinite_row(const double* zr, const double* zi, int s) {
+  bool bad = false;
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (k < s) bad |= !isfinite(zr[k]) || !isfinite(zi[k]);
+  } else {
+    for (int k = 0; k < s; ++k) bad |= !isfinite(zr[k]) || !isfinite(zi[k]);
+  }
+  return bad;
+}
+
 __device__ void write_winner(const ProjOut& out, const DictView& dv, int64_t v, int64_t j,
                              double score) {
   const int s = dv.s;
-  const double gamma = score > 0.0 ? score : 0.0;
+  // np.maximum(score, 0) (projection.py:42): NaN propagates
+  const double gamma = score != score ? score : (score > 0.0 ? score : 0.0);
   if (out.idx) {
     if (out.idx64) reinterpret_cast<int64_t*>(out.idx)[v] = j + out.idx_offset;
     else reinterpret_cast<int32_t*>(out.idx)[v] = int32_t(j + out.idx_offset);
@@ -816,15 +842,19 @@ __global__ void __launch_bounds__(256) exhaustive_kernel(ZSource zs, DictView dv
     int64_t best = INT64_MAX;
     for (int64_t j = lane; j < dv.d; j += 32) {
       const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
-      if (acc > bs) { bs = acc; best = j; }
+      if (argmax_better(acc, j, bs, best)) { bs = acc; best = j; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double obs = __shfl_xor_sync(0xffffffffu, bs, o);
       int64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
-      if (obs > bs || (obs == bs && ob < best)) { bs = obs; best = ob; }
+      if (argmax_better(obs, ob, bs, best)) { bs = obs; best = ob; }
     }
-    if (best == INT64_MAX) best = 0;  // all-NaN row: np.argmax returns the first NaN -> 0
+    if (best == INT64_MAX) best = 0;  // empty dictionary slice
+    if (nonfinite_row<S>(zw, zw + s, s)) {  // all-NaN reference scores: atom 0
+      best = 0;
+      bs = dot_atom<S>(zw, zw + s, dv.atoms64, s);
+    }
     if (lane == 0) write_winner(out, dv, v, best, bs);
     __syncwarp();
   }
@@ -902,7 +932,7 @@ __global__ void __launch_bounds__(256) exhaustive_split_kernel(ZSource zs, DictV
     if (__any_sync(0xffffffffu, full)) {
       for (int64_t j = lo + lane; j < hi; j += 32) {
         const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
-        if (acc > bs) { bs = acc; best = j; }
+        if (argmax_better(acc, j, bs, best)) { bs = acc; best = j; }
       }
     } else {
       const float thr32 = gmax32 - w32;
@@ -911,21 +941,21 @@ __global__ void __launch_bounds__(256) exhaustive_split_kernel(ZSource zs, DictV
         if (__int_as_float(e2.y) < thr32) continue;
         const int64_t j = e2.x;
         const double acc = dot_atom<S>(zw, zw + s, dv.atoms64 + j * s, s);
-        if (acc > bs || (acc == bs && j < best)) { bs = acc; best = j; }
+        if (argmax_better(acc, j, bs, best)) { bs = acc; best = j; }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double obs = __shfl_xor_sync(0xffffffffu, bs, o);
       const int64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
-      if (obs > bs || (obs == bs && ob < best)) { bs = obs; best = ob; }
+      if (argmax_better(obs, ob, bs, best)) { bs = obs; best = ob; }
     }
     if (lane == 0) partial[pr] = make_double2(bs, __longlong_as_double(best));
     __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(256) exhaustive_finish_kernel(DictView dv,
+__global__ void __launch_bounds__(256) exhaustive_finish_kernel(ZSource zs, DictView dv,
                                                                 const int* __restrict__ cnt,
                                                                 const int64_t* __restrict__ list,
                                                                 const double2* __restrict__ partial,
@@ -937,10 +967,23 @@ __global__ void __launch_bounds__(256) exhaustive_finish_kernel(DictView dv,
   for (int k = 0; k < kExhSplits; ++k) {
     const double2 p = partial[i * kExhSplits + k];
     const int64_t j = __double_as_longlong(p.y);
-    if (p.x > bs || (p.x == bs && j < best)) { bs = p.x; best = j; }
+    if (argmax_better(p.x, j, bs, best)) { bs = p.x; best = j; }
   }
-  if (best == INT64_MAX) best = 0;  // all-NaN row: np.argmax returns the first NaN -> 0
-  write_winner(out, dv, list[i], best, bs);
+  if (best == INT64_MAX) best = 0;  // empty dictionary
+  const int64_t v = list[i];
+  bool bad = false;
+  double acc = 0.0;
+  for (int k = 0; k < dv.s; ++k) {  // non-finite row: all-NaN reference scores -> atom 0
+    const double2 z = load_z(zs, v, dv.s, k);
+    bad |= !isfinite(z.x) || !isfinite(z.y);
+    acc = fma(z.x, dv.atoms64[k].x, acc);
+    acc = fma(z.y, dv.atoms64[k].y, acc);
+  }
+  if (bad) {
+    best = 0;
+    bs = acc;
+  }
+  write_winner(out, dv, v, best, bs);
 }
 
 #ifdef CBB_TRACE
@@ -2950,7 +2993,7 @@ static int launch_exhaustive_list_s(int64_t n, const ZSource& zs, const DictView
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
   exhaustive_split_kernel<S><<<num_sms() * 8, 256, shm, st>>>(zs, dv, cnt, list, win32, partial);
   CBB_CUDA_TRY(cudaGetLastError());
-  exhaustive_finish_kernel<<<int((n + 255) / 256), 256, 0, st>>>(dv, cnt, list, partial, out);
+  exhaustive_finish_kernel<<<int((n + 255) / 256), 256, 0, st>>>(zs, dv, cnt, list, partial, out);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

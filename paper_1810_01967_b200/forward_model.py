@@ -241,8 +241,12 @@ class ForwardOperator:
         c*s FFTs of the subspace channel images, no (L, n) frame stack)."""
         Xc, V = Xc.contiguous(), V.contiguous()
         s = int(Xc.shape[1])
-        if self.kind == "dense_gaussian" or s > 32:
-            return self.fm_apply(Xc @ V.conj().transpose(0, 1))
+        if self.kind == "dense_gaussian" or s > 32:   # decompress, then the frame path
+            Y = self.fm_apply(Xc @ V.conj().transpose(0, 1))
+            if out is None:
+                return Y
+            out.copy_(Y)
+            return out
         Y = out if out is not None else torch.empty((self.L, self.cm), dtype=torch.complex64,
                                                     device=self.device)
         _lib.check(_lib.load().cbb_op_apply_compressed(self._op, Xc.data_ptr(), V.data_ptr(), s,
@@ -270,8 +274,12 @@ class ForwardOperator:
         deterministic per-channel k-space build, c*s inverse FFTs, coil combine)."""
         R, V = R.contiguous(), V.contiguous()
         s = int(V.shape[1])
-        if self.kind == "dense_gaussian" or s > 32:
-            return self.fm_adjoint(R) @ V
+        if self.kind == "dense_gaussian" or s > 32:   # frame path, then compress
+            G = self.fm_adjoint(R) @ V
+            if out is None:
+                return G
+            out.copy_(G)
+            return out
         G = out if out is not None else torch.empty((self.n, s), dtype=torch.complex64,
                                                     device=self.device)
         _lib.check(_lib.load().cbb_op_adjoint_compressed(self._op, R.data_ptr(), V.data_ptr(), s,

@@ -73,6 +73,7 @@ def project_device(Z: torch.Tensor, dd: DeviceDictionary, *, algo: str = "auto",
         idx, gam, proj = out
     wsb = lib.cbb_project_workspace_bytes(n, s)
     ws = workspace(wsb, dev, "project")
+    _last_ws[dev.index] = (ws, n, s, torch.cuda.current_stream(dev))
     rc = lib.cbb_project_cone_exact(Z.data_ptr() if n else None, int(z128), n,
                                     ctypes.byref(dd.view), idx.data_ptr(),
                                     int(idx.dtype == torch.int64), gam.data_ptr(),
@@ -195,26 +196,32 @@ def _project_pipelined(zh: torch.Tensor, dd: DeviceDictionary, algo: str, dev):
     return hidx, hgam, hproj
 
 
-def overflow_counts(n: int, s: int):
-    """(voxels rescanned exhaustively in fp64, voxels with many tcgen05 candidate chunks that
-    were rescored warp-cooperatively) of the last projection of this shape (diagnostic)."""
-    lib = _lib.load()
+_last_ws: dict = {}   # device index -> (workspace, n, s, stream) of the last project_device call
+
+
+def _last_workspace(n, s):
     dev = require_cuda()
-    wsb = lib.cbb_project_workspace_bytes(n, s)
-    ws = workspace(wsb, dev, "project")
+    rec = _last_ws.get(dev.index)
+    if rec is None:
+        raise ValueError("no projection has run on this device")
+    ws, n0, s0, stream = rec
+    if (n is not None and n != n0) or (s is not None and s != s0):
+        raise ValueError(f"the last projection on this device was {n0} x s={s0}, not {n} x s={s}")
+    return ws, n0, s0, stream
+
+
+def overflow_counts(n: int = None, s: int = None):
+    """(voxels rescanned exhaustively in fp64, voxels with many tcgen05 candidate chunks that
+    were rescored warp-cooperatively) of the last ``project_device`` call on the current device
+    -- for the pipelined numpy path, its last chunk (diagnostic; read on that call's stream)."""
+    lib = _lib.load()
+    ws, n0, s0, stream = _last_workspace(n, s)
     out = (ctypes.c_int32 * 2)()
-    _lib.check(lib.cbb_project_overflow_counts(ws.data_ptr(), n, s, out, _lib.stream_ptr()),
+    _lib.check(lib.cbb_project_overflow_counts(ws.data_ptr(), n0, s0, out, stream.cuda_stream),
                "overflow_counts")
     return int(out[0]), int(out[1])
 
 
-def overflow_count(n: int, s: int) -> int:
-    """Voxels the last projection rescanned exhaustively in fp64 (diagnostic)."""
-    lib = _lib.load()
-    dev = require_cuda()
-    wsb = lib.cbb_project_workspace_bytes(n, s)
-    ws = workspace(wsb, dev, "project")
-    out = ctypes.c_int(0)
-    _lib.check(lib.cbb_project_overflow_count(ws.data_ptr(), n, s, ctypes.byref(out),
-                                              _lib.stream_ptr()), "overflow_count")
-    return int(out.value)
+def overflow_count(n: int = None, s: int = None) -> int:
+    """Voxels the last ``project_device`` call rescanned exhaustively in fp64 (diagnostic)."""
+    return overflow_counts(n, s)[0]

@@ -152,8 +152,8 @@ def test_ipg_lockstep_against_oracle():
     # trajectory vs the real reference (golden): same step sizes / shrink counts
     np.testing.assert_array_equal([r["shrinks"] for r in trace.records], g["shrinks"])
     np.testing.assert_allclose([r["mu"] for r in trace.records], g["mu"], rtol=1e-4)
-    np.testing.assert_allclose(trace.fidelities(), g["fidelity"], rtol=1e-3)
-    assert rel(X, g["X"]) <= 1e-2
+    np.testing.assert_allclose(trace.fidelities(), g["fidelity"], rtol=1e-5)
+    assert rel(X, g["X"]) <= 1e-4
 
 
 def test_cfg0_end_to_end_vs_reference_trace():
@@ -174,8 +174,12 @@ def test_cfg0_end_to_end_vs_reference_trace():
     same_idx = np.mean(maps.t1 == cfg.dictionary.lookup_table[g["indices"], 0])
     print("final nmse gpu/ref:", trace.records[-1]["nmse"], g["nmse"][-1], "T1 agreement",
           same_idx, agree)
-    assert np.all(np.abs(f_gpu[:k] - f_ref[:k]) / f_ref[:k] < 1e-2)
-    assert abs(trace.records[-1]["nmse"] - g["nmse"][-1]) < 0.1 * g["nmse"][-1]
+    # DESIGN 5: same iteration count, fidelity trajectory to fp32 rounding, the same maps
+    assert len(f_gpu) == len(f_ref)
+    assert np.all(np.abs(f_gpu - f_ref) / f_ref < 1e-5)
+    np.testing.assert_array_equal([r["shrinks"] for r in trace.records], g["shrinks"])
+    assert same_idx >= 0.999
+    assert abs(trace.records[-1]["nmse"] - g["nmse"][-1]) < 1e-4 * g["nmse"][-1]
 
 
 def test_reference_solver_kats():
