@@ -17,6 +17,7 @@
  *   cbb_project_cone_exact  <- projection.py:45-67  project_cone_exact(Z, dictionary)
  *                              (+ projection.py:38-42 _gammas_for, :64 write-back)
  *   cbb_project_step        <- solver.py:128-130   proj = project_fn(X - mu*G); dX; ||dX||^2
+ *   cbb_graph_*, cbb_trial_* <- solver.py:116-144 step_shrinkage decided on the device
  *   cbb_dict_prepare        <- projection.py:26-29 _atoms_of (device copy of .atoms /
  *                              .atoms_compressed, done once per dictionary)
  *   cbb_op_*                <- forward_model.py:123-167 ForwardOperator.apply/adjoint
@@ -117,6 +118,36 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
                      const cbb_dict_view* dict, const int32_t* idx_hint, int32_t* idx_out,
                      double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
                      void* workspace, size_t workspace_bytes, int32_t algo, void* stream);
+/* cbb_project_step with mu read from device memory (float, the same float(mu) the host loop
+ * passes): the graph-captured trials of cbb_graph_* below. */
+int cbb_project_step_dmu(const void* x, const void* g, const float* mu_dev, void* z_out,
+                         int64_t n, const cbb_dict_view* dict, const int32_t* idx_hint,
+                         int32_t* idx_out, double* gamma_out, void* xnext_out, void* dx_out,
+                         double* nd_out, void* workspace, size_t workspace_bytes, int32_t algo,
+                         void* stream);
+
+/* ---- device-decided IPG iteration (solver.py:116-144, 155-257) ----
+ * A CUDA graph of one iteration: the gradient, a while-conditional node repeating the trial
+ * (cbb_project_step_dmu + ||A dX||^2 + cbb_trial_decide) until the device accepts mu, reaches the
+ * fixed point or collapses, then the apply of the new iterate and the residual.  Capture:
+ * cbb_graph_capture_begin(stream) -> calls on stream -> cbb_graph_while_begin(g, body_stream) ->
+ * the trial's calls on body_stream -> cbb_trial_decide -> cbb_graph_while_end -> calls on stream
+ * -> cbb_graph_capture_end; replay with cbb_graph_launch.  The trial state (device memory of
+ * cbb_trial_state_bytes(): fp64 mu, mu_base, fp32 mu, shrinks, fixed, status, trials) is
+ * reset from mu_base by cbb_trial_init; cbb_trial_carry sets mu_base = mu (carry_over). */
+typedef struct cbb_graph cbb_graph;
+size_t cbb_trial_state_bytes(void);
+int cbb_trial_init(void* trial_state, void* stream);
+int cbb_trial_carry(void* trial_state, void* stream);
+int cbb_graph_capture_begin(void* stream, cbb_graph** out);
+int cbb_graph_while_begin(cbb_graph* g, void* body_stream);
+int cbb_trial_decide(cbb_graph* g, void* trial_state, const double* nd, const double* den,
+                     double zeta, int32_t max_shrink);
+int cbb_graph_while_end(cbb_graph* g);
+int cbb_graph_capture_end(cbb_graph* g);
+int cbb_graph_launch(cbb_graph* g, void* stream);
+int cbb_graph_destroy(cbb_graph* g);
+
 /* Atom-sharded building block (multi-GPU): per voxel the shard-local exact argmax
  * reported as a GLOBAL atom index (local + atom_offset, int64) and its raw fp64 score
  * Re<z, d_j*> (not clipped at 0), for the cross-rank combine (cbb_argmax_select). */

@@ -51,6 +51,19 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_step": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, ctypes.POINTER(DictView), c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32, c_vp]),
+    "cbb_project_step_dmu": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(DictView),
+                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32,
+                                     c_vp]),
+    "cbb_trial_state_bytes": (c_size, []),
+    "cbb_trial_init": (c_int, [c_vp, c_vp]),
+    "cbb_trial_carry": (c_int, [c_vp, c_vp]),
+    "cbb_graph_capture_begin": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "cbb_graph_while_begin": (c_int, [c_vp, c_vp]),
+    "cbb_trial_decide": (c_int, [c_vp, c_vp, c_vp, c_vp, c_dbl, c_i32]),
+    "cbb_graph_while_end": (c_int, [c_vp]),
+    "cbb_graph_capture_end": (c_int, [c_vp]),
+    "cbb_graph_launch": (c_int, [c_vp, c_vp]),
+    "cbb_graph_destroy": (c_int, [c_vp]),
     "cbb_project_best": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_i64, c_vp, c_vp,
                                  c_vp, c_size, c_i32, c_vp]),
     "cbb_scaled_rows": (c_int, [ctypes.POINTER(DictView), c_i64, c_vp, c_vp, c_i64, c_vp, c_i32,

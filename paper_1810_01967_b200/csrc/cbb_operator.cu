@@ -831,10 +831,11 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   else if (Ymeas != nullptr) mode = 2;
   double* pp = (mode != 0 || norm_out) ? part : nullptr;
   int launches = 2;
-  if (op->rows_sorted && int64_t(op->L) * op->m >= 4 * op->n) {
-    // location-tiled gather straight from the channel-planar FFT output
-    const int W = tile_width(op, s);
-    const int nb = int((op->n + W - 1) / W);
+  const int W = tile_width(op, s);
+  const int nb = int((op->n + W - 1) / W);
+  // location-tiled gather straight from the channel-planar FFT output, when there are enough
+  // tiles to fill the GPU (cfg0's 4096 locations are 8 tiles: sample-major below)
+  if (op->rows_sorted && int64_t(op->L) * op->m >= 4 * op->n && nb >= 2 * 148) {
     const int* seg = nullptr;
     if ((rc = seg_table(op, W, st, &seg))) return rc;
     int sms = 148;

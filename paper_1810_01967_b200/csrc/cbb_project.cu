@@ -587,6 +587,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 float2* __restrict__ lbz) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
+  const float mu = zs.mu_ptr ? *zs.mu_ptr : zs.mu;
   // tile pruning: (exact hint score rounded down, ||z|| rounded up); zero and non-finite voxels
   // are decided without the screen (+inf: they need no atom tile)
   if (lbz && v < n) lbz[v] = make_float2(INFINITY, 0.f);
@@ -604,7 +605,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     double re, im;
     if (zs.x != nullptr) {
       const float2 xk = zs.x[v * s + k], gk = zs.g[v * s + k];
-      const float zr = __fmaf_rn(-zs.mu, gk.x, xk.x), zi = __fmaf_rn(-zs.mu, gk.y, xk.y);
+      const float zr = __fmaf_rn(-mu, gk.x, xk.x), zi = __fmaf_rn(-mu, gk.y, xk.y);
       zs.z_out[v * s + k] = make_float2(zr, zi);
       re = zr; im = zi;
     } else if (zs.z128) {
@@ -664,8 +665,8 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     double re, im;
     if (zs.x != nullptr) {
       const float2 xk = zs.x[v * s + k], gk = zs.g[v * s + k];
-      re = __fmaf_rn(-zs.mu, gk.x, xk.x);
-      im = __fmaf_rn(-zs.mu, gk.y, xk.y);
+      re = __fmaf_rn(-mu, gk.x, xk.x);
+      im = __fmaf_rn(-mu, gk.y, xk.y);
     } else if (zs.z128) {
       double2 a = reinterpret_cast<const double2*>(zs.z)[v * s + k];
       re = a.x; im = a.y;

@@ -76,6 +76,7 @@ struct ZSource {
   float2* z_out;
   const int32_t* hint; // optional per-voxel atom index (e.g. the previous IPG winner): its exact
                        // score seeds the screen's running max (warm start); may be null
+  const float* mu_ptr; // IPG mode: mu read from device memory (graph-captured trials), else mu
 };
 
 // Outputs.  Any pointer may be null (not produced).

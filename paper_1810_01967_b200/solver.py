@@ -26,6 +26,7 @@ from __future__ import annotations
 import csv
 import ctypes
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -34,7 +35,7 @@ import torch
 
 from . import _lib
 from .device import workspace
-from .dictionary import device_dictionary, lookup_table_of
+from .dictionary import atoms_of, device_dictionary, lookup_table_of
 from .forward_model import as_device_operator
 from .projection import project_cone_exact  # noqa: F401  (re-exported drop-in)
 
@@ -156,20 +157,9 @@ class IpgState:
         self.dim = self.dd.s
         self.V = (None if basis is None else
                   torch.from_numpy(np.ascontiguousarray(basis, dtype=np.complex64)).to(device))
-        # upload in the caller's layout and precision; ||Y|| (fp64) and the frame-major complex64
-        # copy are formed on the device (no host transpose / cast of the measurements)
-        Yh = np.asarray(Y)
-        if Yh.shape != (self.cm, self.L):
-            raise ValueError(f"measurements are {Yh.shape}, the operator expects "
-                             f"{(self.cm, self.L)}")
-        if not np.iscomplexobj(Yh):
-            Yh = Yh.astype(np.complex128)
-        Yd = torch.from_numpy(np.ascontiguousarray(Yh)).to(device)     # (c*m, L)
-        self.y_norm = float(torch.linalg.vector_norm(torch.view_as_real(Yd), dtype=torch.float64))
-        self.Y = Yd.transpose(0, 1).to(torch.complex64).contiguous()   # (L, c*m)
-        del Yd
-        self.w = (None if weights is None else torch.from_numpy(np.ascontiguousarray(
-            np.broadcast_to(weights, np.asarray(Y).shape).T, dtype=np.float32)).to(device))
+        self.Y = torch.empty((self.L, self.cm), dtype=torch.complex64, device=device)
+        self.w = None
+        self.load_measurements(Y, weights)
         c64 = dict(dtype=torch.complex64, device=device)
         n, dim = self.n, self.dim
         self.X = torch.zeros((n, dim), **c64)
@@ -189,9 +179,38 @@ class IpgState:
         self.pws_bytes = lib.cbb_project_workspace_bytes_dict(n, ctypes.byref(self.dd.view))
         self.rws_bytes = lib.cbb_reduce_workspace_bytes()
         self.algo = 0
+        self._graphs = {}          # device-decided iteration graphs, per buffer parity
 
     def _rws(self):
         return workspace(self.rws_bytes, self.dev, "reduce")
+
+    def load_measurements(self, Y, weights):
+        """Upload Y in the caller's layout and precision into the frame-major complex64 buffer
+        (||Y|| in fp64 and the transpose / cast happen on the device) and the loss weights."""
+        Yh = np.asarray(Y)
+        if Yh.shape != (self.cm, self.L):
+            raise ValueError(f"measurements are {Yh.shape}, the operator expects "
+                             f"{(self.cm, self.L)}")
+        if not np.iscomplexobj(Yh):
+            Yh = Yh.astype(np.complex128)
+        Yd = torch.from_numpy(np.ascontiguousarray(Yh)).to(self.dev)     # (c*m, L)
+        self.y_norm = float(torch.linalg.vector_norm(torch.view_as_real(Yd), dtype=torch.float64))
+        self.Y.copy_(Yd.transpose(0, 1))                                  # (L, c*m) complex64
+        del Yd
+        w = (None if weights is None else torch.from_numpy(np.ascontiguousarray(
+            np.broadcast_to(weights, Yh.shape).T, dtype=np.float32)).to(self.dev))
+        if w is None or self.w is None:
+            self.w = w
+        else:
+            self.w.copy_(w)                   # keep the buffer a captured graph points to
+
+    def reset_iterates(self):
+        """X = 0 (solver.py:199): the state a solve starts from."""
+        self.X.zero_()
+        self.AX.zero_()
+        self.idx.zero_()
+        self.gam.zero_()
+        self.scal.zero_()
 
     def read(self, *slots):
         """Device fp64 scalars -> host floats (one small synchronous copy)."""
@@ -266,6 +285,110 @@ class IpgState:
     def decompress(self, Xs):
         return Xs if self.V is None else Xs @ self.V.conj().transpose(0, 1)
 
+    # -- device-decided iterations: one CUDA graph per iteration (include/coverblip_b200.h
+    #    cbb_graph_*): gradient, a while-conditional node repeating the trial until the device
+    #    accepts mu (solver.py:116-144), the apply of the new iterate and the residual; the host
+    #    synchronises once per iteration instead of once per trial.
+    _TS_DTYPE = np.dtype([("mu", "<f8"), ("mu_base", "<f8"), ("mu32", "<f4"), ("shrinks", "<i4"),
+                          ("fixed", "<i4"), ("status", "<i4"), ("trials", "<i4")])
+
+    def graph_capable(self, config) -> bool:
+        """The captured iteration needs allocation-free calls: the s-channel Cartesian
+        operator, the adaptive step rule and one GPU (the sharded state all-reduces on read)."""
+        return (self.V is not None and getattr(self.A, "kind", "") == "cartesian_dft"
+                and int(self.V.shape[1]) <= 32 and config.fixed_step is None
+                and type(self) is IpgState)
+
+    def _graph_setup(self):
+        if "ts" in self.__dict__:
+            return
+        nb = int(self.lib.cbb_trial_state_bytes())
+        assert nb >= self._TS_DTYPE.itemsize
+        self.ts = torch.zeros(nb, dtype=torch.uint8, device=self.dev)
+        self.ts_host = torch.zeros(nb, dtype=torch.uint8, pin_memory=True)
+        self.ts_mu_base = None
+        self.g_main = torch.cuda.Stream(device=self.dev)
+        self.g_body = torch.cuda.Stream(device=self.dev)
+
+    def project_step_dev(self, slot):
+        """project_step with mu from the trial state (fp32 image of the fp64 mu)."""
+        ws = workspace(self.pws_bytes, self.dev, "project")
+        o = self.scal[slot:slot + 1]
+        _lib.check(self.lib.cbb_project_step_dmu(
+            self.X.data_ptr(), self.G.data_ptr(), self.ts.data_ptr() + 16, self.Z.data_ptr(),
+            self.n, ctypes.byref(self.dd.view), self.idx.data_ptr(), self.idx_n.data_ptr(),
+            self.gam_n.data_ptr(), self.Xn.data_ptr(), self.dX.data_ptr(), o.data_ptr(),
+            ws.data_ptr(), self.pws_bytes, self.algo, _lib.stream_ptr()), "cbb_project_step_dmu")
+
+    def _capture_iteration(self, config, carry):
+        lib = self.lib
+        g = ctypes.c_void_p()
+        main, body = self.g_main, self.g_body
+        main.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(main):
+            _lib.check(lib.cbb_graph_capture_begin(main.cuda_stream, ctypes.byref(g)),
+                       "cbb_graph_capture_begin")
+            try:
+                self.gradient()
+                _lib.check(lib.cbb_trial_init(self.ts.data_ptr(), main.cuda_stream),
+                           "cbb_trial_init")
+                _lib.check(lib.cbb_graph_while_begin(g, body.cuda_stream), "while_begin")
+                with torch.cuda.stream(body):
+                    self.project_step_dev(1)
+                    self.apply_norm2(self.dX, 2)
+                    _lib.check(lib.cbb_trial_decide(g, self.ts.data_ptr(),
+                                                    self.scal[1:2].data_ptr(),
+                                                    self.scal[2:3].data_ptr(),
+                                                    float(config.zeta),
+                                                    int(config.max_shrink_per_iter)),
+                               "cbb_trial_decide")
+                _lib.check(lib.cbb_graph_while_end(g), "while_end")
+                self.apply(self.Xn, self.AX)       # the accepted trial's iterate
+                self.residual(0)
+                if carry:
+                    _lib.check(lib.cbb_trial_carry(self.ts.data_ptr(), main.cuda_stream),
+                               "cbb_trial_carry")
+                _lib.check(lib.cbb_graph_capture_end(g), "cbb_graph_capture_end")
+            except Exception:
+                lib.cbb_graph_destroy(g)
+                raise
+        torch.cuda.current_stream(self.dev).wait_stream(main)
+        return g
+
+    def graph_iteration(self, config, mu_base, carry):
+        """Run one device-decided iteration.  Returns (new objective, mu, shrinks, fixed,
+        collapsed)."""
+        self._graph_setup()
+        if mu_base != self.ts_mu_base:           # host mu_base (kappa, first use)
+            hv = np.zeros(1, self._TS_DTYPE)
+            hv["mu_base"] = mu_base
+            raw = torch.from_numpy(hv.view(np.uint8).copy())
+            self.ts[8:16].copy_(raw[8:16], non_blocking=False)
+            self.ts_mu_base = mu_base
+        key = (self.X.data_ptr(), carry)
+        g = self._graphs.get(key)
+        if g is None:
+            g = self._graphs[key] = self._capture_iteration(config, carry)
+        stream = torch.cuda.current_stream(self.dev)
+        _lib.check(self.lib.cbb_graph_launch(g, stream.cuda_stream), "cbb_graph_launch")
+        self.host[:1].copy_(self.scal[:1], non_blocking=True)
+        self.ts_host.copy_(self.ts, non_blocking=True)
+        stream.synchronize()
+        t = self.ts_host.numpy()[:self._TS_DTYPE.itemsize].view(self._TS_DTYPE)[0]
+        if carry:
+            self.ts_mu_base = float(t["mu"])
+        return (float(self.host[0]), float(t["mu"]), int(t["shrinks"]), bool(t["fixed"]),
+                bool(t["status"]))
+
+    def __del__(self):
+        graphs = self.__dict__.get("_graphs") or {}
+        for g in graphs.values():
+            try:
+                self.lib.cbb_graph_destroy(g)
+            except Exception:
+                pass
+        graphs.clear()
+
 
 _STAGE_BYTES = 256 << 20
 _copy_pool = None
@@ -325,8 +448,41 @@ def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
     start = time.perf_counter()
     trace.start = start
     have_proj = False
+    graphs = hasattr(st, "graph_capable") and st.graph_capable(config)
+    carry = config.step_policy == "carry_over"
     for k in range(1, max_iters + 1):
         t0 = time.perf_counter()
+        if graphs and k >= 2:
+            # device-decided iteration (gradient, trials, apply, residual in one graph)
+            new_obj, mu, shrinks, fixed_pt, collapsed = st.graph_iteration(config, mu_base, carry)
+            if collapsed:
+                raise SolverError(
+                    "step-size collapse: shrinkage exceeded "
+                    f"{config.max_shrink_per_iter} sub-iterations")
+            if on_iter is not None:
+                on_iter(k, st, mu, shrinks, fixed_pt)
+            if fixed_pt:
+                break
+            st.X, st.Xn = st.Xn, st.X
+            st.idx, st.idx_n = st.idx_n, st.idx
+            st.gam, st.gam_n = st.gam_n, st.gam
+            have_proj = True
+            if carry:
+                mu_base = mu
+            if not math.isfinite(new_obj):
+                raise SolverError(f"non-finite fidelity at iteration {k}: {new_obj}")
+            nmse = None
+            if gt_t is not None:
+                nmse = float(torch.linalg.vector_norm(st.decompress(st.X) - gt_t)) / gt_norm
+            trace.add(iter=k, fidelity=math.sqrt(new_obj), mu=mu, shrinks=shrinks,
+                      cost=n * d, nmse=nmse, seconds=time.perf_counter() - t0)
+            if obj > 0.0 and (obj - new_obj) / obj < config.rel_tol:
+                obj = new_obj
+                break
+            obj = new_obj
+            if obj == 0.0:
+                break
+            continue
         st.gradient()
         mu = mu_base
         shrinks = 0
@@ -394,6 +550,38 @@ def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
     return trace, have_proj
 
 
+_state_lock = threading.Lock()
+_state_cache: dict = {}
+
+
+def _state_for(Y, A, dictionary, basis, weights, dev):
+    """The IPG state of a solve.  The most recent state is kept (with its captured iteration
+    graphs) and reused by the next solve with the same operator, dictionary and basis objects:
+    repeated solves (the reference's harness runs many) skip the buffer allocation and the graph
+    capture.  The cache holds strong references, so the keyed ids cannot be recycled."""
+    key = (dev.index, id(A), id(atoms_of(dictionary)), id(basis),
+           None if basis is None else np.asarray(basis).shape, weights is None)
+    with _state_lock:
+        hit = _state_cache.get(key)
+        if hit is not None and not hit[0].busy:
+            st = hit[0]
+            st.busy = True                # concurrent solves (harness threads) get their own
+        else:
+            st = None
+            if hit is None:
+                _state_cache.clear()      # one cached state: free the previous buffers
+    if st is not None:
+        st.load_measurements(Y, weights)
+        st.reset_iterates()
+        return st
+    st = IpgState(Y, A, dictionary, basis, weights, dev)
+    st.busy = True
+    with _state_lock:
+        if key not in _state_cache:
+            _state_cache[key] = (st, A, atoms_of(dictionary), basis)
+    return st
+
+
 def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_device=False):
     """Device IPG loop following solver.py:155-257."""
     Ynp = np.asarray(Y)
@@ -407,7 +595,7 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
     if config.mode == "coverblip" and tree is None:
         raise SolverError("coverblip mode needs a tree")
     with torch.cuda.device(dev):
-        st = IpgState(Ynp, Ad, dictionary, basis, weights, dev)
+        st = _state_for(Ynp, Ad, dictionary, basis, weights, dev)
         n, d = st.n, st.dd.d
         if config.fixed_step is not None:
             mu_base = config.fixed_step
@@ -421,17 +609,24 @@ def _solve_core(Y, A, dictionary, tree, config, gt, basis, on_iter=None, return_
             gt_data = gt.data if hasattr(gt, "data") and not isinstance(gt, np.ndarray) else gt
             gt_t = torch.from_numpy(np.ascontiguousarray(gt_data, dtype=np.complex64)).to(dev)
             gt_norm = float(np.linalg.norm(gt_data))
-        trace, have_proj = _ipg_loop(st, config, mu_base, y_norm, gt_t,
-                                     gt_norm if gt_t is not None else None, n, d, on_iter)
-        torch.cuda.current_stream(dev).synchronize()
-        trace.total_time = time.perf_counter() - trace.start
-        if return_device:
-            return st, trace
-        idx = st.idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
-        gam = st.gam.cpu().numpy() if have_proj else np.zeros(n)
-        maps = _maps_from(dictionary, idx, gam)
-        out = _image_to_host(st.X, st.V)
-        return out, maps, gam, trace
+        try:
+            trace, have_proj = _ipg_loop(st, config, mu_base, y_norm, gt_t,
+                                         gt_norm if gt_t is not None else None, n, d, on_iter)
+            torch.cuda.current_stream(dev).synchronize()
+            trace.total_time = time.perf_counter() - trace.start
+            if return_device:             # the caller owns the state now: never reused
+                with _state_lock:
+                    for k_, v_ in list(_state_cache.items()):
+                        if v_[0] is st:
+                            del _state_cache[k_]
+                return st, trace
+            idx = st.idx.cpu().numpy().astype(np.int64) if have_proj else np.zeros(n, np.int64)
+            gam = st.gam.cpu().numpy() if have_proj else np.zeros(n)
+            maps = _maps_from(dictionary, idx, gam)
+            out = _image_to_host(st.X, st.V)
+            return out, maps, gam, trace
+        finally:
+            st.busy = False
 
 
 def solve(Y, A, dictionary, tree, config: SolverConfig, gt=None, **kw):
