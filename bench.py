@@ -394,7 +394,6 @@ class _IterProbe:
         import ctypes
 
         from paper_1810_01967_b200 import _lib
-        from paper_1810_01967_b200.device import workspace
         torch = self.torch
         n_loc = st.n
         v0 = getattr(getattr(st, "comm", None), "v0", 0)
@@ -408,7 +407,7 @@ class _IterProbe:
         self.last = snap
         lib = _lib.load()
         listed, total = ctypes.c_int64(0), ctypes.c_int64(0)
-        ws = workspace(st.pws_bytes, st.dev, "project")
+        ws = st.project_workspace()
         lib.cbb_project_prune_stats(ws.data_ptr(), st.pws_bytes, st.n, ctypes.byref(st.dd.view),
                                     ctypes.byref(listed), ctypes.byref(total), _lib.stream_ptr())
         self.listed.append(listed.value / total.value if listed.value >= 0 and total.value else

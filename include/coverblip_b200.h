@@ -118,17 +118,19 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
                      const cbb_dict_view* dict, const int32_t* idx_hint, int32_t* idx_out,
                      double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
                      void* workspace, size_t workspace_bytes, int32_t algo, void* stream);
-/* cbb_project_step with mu read from device memory (float, the same float(mu) the host loop
- * passes): the graph-captured trials of cbb_graph_* below. */
-int cbb_project_step_dmu(const void* x, const void* g, const float* mu_dev, void* z_out,
-                         int64_t n, const cbb_dict_view* dict, const int32_t* idx_hint,
-                         int32_t* idx_out, double* gamma_out, void* xnext_out, void* dx_out,
-                         double* nd_out, void* workspace, size_t workspace_bytes, int32_t algo,
-                         void* stream);
+/* cbb_project_step extended: mu_dev (optional) reads mu from device memory (float, the same
+ * float(mu) the host loop passes: graph-captured trials), idx_hint2 (optional) a second
+ * warm-start atom per voxel (e.g. the previous trial's winners): the better-scoring hint seeds
+ * the screen and the tile-pruning bound.  Results are those of cbb_project_step. */
+int cbb_project_step_ex(const void* x, const void* g, double mu, const float* mu_dev,
+                        void* z_out, int64_t n, const cbb_dict_view* dict,
+                        const int32_t* idx_hint, const int32_t* idx_hint2, int32_t* idx_out,
+                        double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
+                        void* workspace, size_t workspace_bytes, int32_t algo, void* stream);
 
 /* ---- device-decided IPG iteration (solver.py:116-144, 155-257) ----
  * A CUDA graph of one iteration: the gradient, a while-conditional node repeating the trial
- * (cbb_project_step_dmu + ||A dX||^2 + cbb_trial_decide) until the device accepts mu, reaches the
+ * (cbb_project_step_ex + ||A dX||^2 + cbb_trial_decide) until the device accepts mu, reaches the
  * fixed point or collapses, then the apply of the new iterate and the residual.  Capture:
  * cbb_graph_capture_begin(stream) -> calls on stream -> cbb_graph_while_begin(g, body_stream) ->
  * the trial's calls on body_stream -> cbb_trial_decide -> cbb_graph_while_end -> calls on stream

@@ -51,9 +51,9 @@ SIGNATURES = {
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_i32, c_vp]),
     "cbb_project_step": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_i64, ctypes.POINTER(DictView), c_vp,
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32, c_vp]),
-    "cbb_project_step_dmu": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(DictView),
-                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_i32,
-                                     c_vp]),
+    "cbb_project_step_ex": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_vp, c_i64,
+                                    ctypes.POINTER(DictView), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp, c_vp, c_size, c_i32, c_vp]),
     "cbb_trial_state_bytes": (c_size, []),
     "cbb_trial_init": (c_int, [c_vp, c_vp]),
     "cbb_trial_carry": (c_int, [c_vp, c_vp]),

@@ -207,18 +207,18 @@ int cbb_project_step(const void* x, const void* g, double mu, void* z_out, int64
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));
 }
 
-int cbb_project_step_dmu(const void* x, const void* g, const float* mu_dev, void* z_out,
-                         int64_t n, const cbb_dict_view* dict, const int32_t* idx_hint,
-                         int32_t* idx_out, double* gamma_out, void* xnext_out, void* dx_out,
-                         double* nd_out, void* workspace, size_t workspace_bytes, int32_t algo,
-                         void* stream) {
+int cbb_project_step_ex(const void* x, const void* g, double mu, const float* mu_dev,
+                        void* z_out, int64_t n, const cbb_dict_view* dict,
+                        const int32_t* idx_hint, const int32_t* idx_hint2, int32_t* idx_out,
+                        double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
+                        void* workspace, size_t workspace_bytes, int32_t algo, void* stream) {
   if (int rc = check_view(dict)) return rc;
-  if (n > 0 && (!x || !g || !mu_dev || !z_out || !xnext_out || !dx_out)) {
-    set_last_error("cbb_project_step_dmu: null argument");
+  if (n > 0 && (!x || !g || !z_out || !xnext_out || !dx_out)) {
+    set_last_error("cbb_project_step_ex: null argument");
     return kErrArgument;
   }
-  ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), 0.f,
-             static_cast<float2*>(z_out), idx_hint, mu_dev};
+  ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), float(mu),
+             static_cast<float2*>(z_out), idx_hint, mu_dev, idx_hint2};
   ProjOut o{idx_out, 0, gamma_out, xnext_out, 0, static_cast<const float2*>(x),
             static_cast<float2*>(dx_out), nullptr, nullptr, 0};
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));

@@ -340,6 +340,27 @@ constexpr int kChunkShift = 20;
 __device__ __forceinline__ int pack_chunk(int64_t jb, uint32_t mask) {
   return int(uint32_t(jb >> 5) | (mask << kChunkShift));
 }
+// Single-atom record (split screen: usually one atom of a recorded chunk is inside the narrow
+// window): bit 31 set, the atom's offset inside the chunk in bits [26, 31), no group mask.
+constexpr uint32_t kSingleAtom = 1u << 31;
+__device__ __forceinline__ int pack_single(int64_t jb, int offset) {
+  return int(uint32_t(jb >> 5) | (uint32_t(offset) << 26) | kSingleAtom);
+}
+// (first atom of the record, 64-bit mask of the atoms to rescore relative to it)
+__device__ __forceinline__ void unpack_record(int x, int64_t& j0, uint32_t& atoms) {
+  const uint32_t u = uint32_t(x);
+  j0 = int64_t(u & ((1u << kChunkShift) - 1)) << 5;
+  if (u & kSingleAtom) {
+    atoms = 1u << ((u >> 26) & 31u);
+    return;
+  }
+  const uint32_t g = (u >> kChunkShift) & 0x3Fu;  // 6-atom groups (the last one: atoms 30, 31)
+  atoms = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b)
+    if (g & (1u << b)) atoms |= 0x3Fu << (6 * b);
+  if (g & (1u << 5)) atoms |= 3u << 30;
+}
 
 // FFMA screen entries (one atom each) that survive the final window.
 __device__ __forceinline__ void rescore_entries(const ZSource& zs, const DictView& dv, int64_t v,
@@ -584,13 +605,14 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
                                 float* __restrict__ win_tc, float* __restrict__ win32,
                                 int s_pad, const double2* __restrict__ atoms64,
                                 int64_t d_atoms, float* __restrict__ init_tc, int split,
-                                float2* __restrict__ lbz) {
+                                float2* __restrict__ lbz, int32_t* __restrict__ hbest) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
   const float mu = zs.mu_ptr ? *zs.mu_ptr : zs.mu;
   // tile pruning: (exact hint score rounded down, ||z|| rounded up); zero and non-finite voxels
   // are decided without the screen (+inf: they need no atom tile)
   if (lbz && v < n) lbz[v] = make_float2(INFINITY, 0.f);
+  if (hbest && v < n) hbest[v] = zs.hint ? zs.hint[v] : -1;
   // plain row-major fp16 rows (kpad elements): staged into TMEM lanes by the epilogue warps
   uint8_t* trow = ztiles ? ztiles + size_t(v) * kpad * 2 : nullptr;
   if (v >= n) {
@@ -735,15 +757,20 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     // warm start: any atom's exact score lower-bounds the approximate maximum once the
     // certified half-window is subtracted (s~_max >= s~_j >= s_j - eps), in scaled units
     float init = -INFINITY;
-    const int64_t jh = zs.hint ? int64_t(zs.hint[v]) : -1;
-    if (jh >= 0 && jh < d_atoms) {
-      const double2* a = atoms64 + jh * s;
-      double acc = 0.0;
-      for (int k = 0; k < s; ++k) {
-        const double2 z = load_z(zs, v, s, k);
-        acc = fma(z.x, a[k].x, acc);
-        acc = fma(z.y, a[k].y, acc);
+    int64_t jh = zs.hint ? int64_t(zs.hint[v]) : -1;
+    if (!(jh >= 0 && jh < d_atoms)) jh = -1;
+    double acc = -INFINITY;
+    if (jh >= 0) acc = exact_score_g(zs, v, s, atoms64 + jh * s);
+    const int64_t j2 = zs.hint2 ? int64_t(zs.hint2[v]) : -1;
+    if (j2 >= 0 && j2 < d_atoms && j2 != jh) {  // any atom's exact score is a lower bound
+      const double a2 = exact_score_g(zs, v, s, atoms64 + j2 * s);
+      if (jh < 0 || a2 > acc) {
+        acc = a2;
+        jh = j2;
       }
+    }
+    if (hbest) hbest[v] = int32_t(jh);
+    if (jh >= 0) {
       init = __double2float_rd(acc * sv * sd - eb * 1.001);
       if (lbz) {  // scaled units of the tile-pruning bound pass (see prune_prepare)
         const double zn_s = sqrt(nz) * sv;
@@ -1198,6 +1225,13 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) { return fmax
 template <class CL>
 __device__ __forceinline__ void record_chunk_f32(const uint32_t* r, float cm, int64_t jb,
                                                  float thr, CL& cl) {
+  uint32_t in = 0;  // atoms of the chunk inside the window
+#pragma unroll
+  for (int i = 0; i < 32; ++i) in |= (__uint_as_float(r[i]) >= thr ? 1u : 0u) << i;
+  if (__popc(in) == 1) {  // the usual case with the split screen's 2^-18 window
+    cl.insert(pack_single(jb, __ffs(in) - 1), cm, thr);
+    return;
+  }
   uint32_t mask = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])) >= thr ? (1u << 5) : 0u;
 #pragma unroll
   for (int g = 0; g < 5; ++g) {
@@ -1855,23 +1889,18 @@ __device__ __forceinline__ void rescore_entry(int2 en, const double* zr, const d
                                               int s, const DictView& dv,
                                               const int32_t* __restrict__ amap, int64_t& best,
                                               double& bs) {
-  const int64_t j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
-  uint32_t mask = uint32_t(en.x) >> kChunkShift;
-  while (mask) {
-    const int b = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
-    for (int i = lo; i < hi; ++i) {
-      const int64_t j = amap ? int64_t(amap[j0 + i]) : j0 + i;
-      if (j >= dv.d) {
-        if (amap) continue;
-        break;
-      }
-      const double acc = dot_atom<S>(zr, zi, dv.atoms64 + j * s, s);
-      if (acc > bs || (acc == bs && j < best)) {
-        bs = acc;
-        best = j;
-      }
+  int64_t j0;
+  uint32_t atoms;
+  unpack_record(en.x, j0, atoms);
+  while (atoms) {
+    const int i = __ffs(atoms) - 1;
+    atoms &= atoms - 1;
+    const int64_t j = amap ? int64_t(amap[j0 + i]) : j0 + i;
+    if (j >= dv.d) continue;
+    const double acc = dot_atom<S>(zr, zi, dv.atoms64 + j * s, s);
+    if (acc > bs || (acc == bs && j < best)) {
+      bs = acc;
+      best = j;
     }
   }
 }
@@ -2036,18 +2065,14 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
     for (int e0 = 0; e0 < total; e0 += 32) {
       const int e = e0 + lane;
       int64_t j0 = 0;
-      uint32_t mask = 0;
+      uint32_t mask = 0;  // atoms of the record to rescore
       if (e < total) {
         int p, c;
         entry_part(e, cnt, p, c);
         const int2 en = cand[(int64_t(p) * kGCap + c) * n_pad + v];
-        if (__int_as_float(en.y) >= thr) {
-          j0 = int64_t(uint32_t(en.x) & ((1u << kChunkShift) - 1)) << 5;
-          mask = uint32_t(en.x) >> kChunkShift;
-        }
+        if (__int_as_float(en.y) >= thr) unpack_record(en.x, j0, mask);
       }
-      // groups 0..4: 6 atoms, group 5: 2 atoms
-      const int na = 6 * __popc(mask & 0x1Fu) + 2 * ((mask >> 5) & 1u);
+      const int na = __popc(mask);
       int off = na;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -2057,10 +2082,9 @@ __global__ void __launch_bounds__(32 * kRescoreWarps) rescore_warp_kernel(
       const int round_total = __shfl_sync(0xffffffffu, off, 31);
       off -= na;
       while (mask) {
-        const int b = __ffs(mask) - 1;
+        const int i = __ffs(mask) - 1;
         mask &= mask - 1;
-        const int lo = 6 * b, hi = b < 5 ? lo + 6 : 32;
-        for (int i = lo; i < hi; ++i) alist[off++] = amap ? amap[j0 + i] : int(j0 + i);
+        alist[off++] = amap ? amap[j0 + i] : int(j0 + i);
       }
       __syncwarp();
       for (int a = lane; a < round_total; a += 32) {
@@ -2595,6 +2619,7 @@ struct ProjWs {
   // the dictionary, project_ws_bytes(..., prune_tiles > 0))
   bool prune;
   float2* lbz;          // [n] (hint score rounded down, ||z|| rounded up)
+  int32_t* hbest;       // [n] the better-scoring warm-start atom (hint / hint2) per voxel
   int32_t* pkeys;       // [n] sort keys (hint atom's split-tile position) and values (voxel)
   int32_t* pkeys_out;
   int32_t* pvals;
@@ -2648,6 +2673,7 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr, int prune_
   w.prune = prune_tiles > 0 && n > 0 && n < (int64_t(1) << 31) && prune_tiles <= 65536;
   if (w.prune) {
     w.lbz = reinterpret_cast<float2*>(take(size_t(n) * 8));
+    w.hbest = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
     w.pkeys = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
     w.pkeys_out = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
     w.pvals = reinterpret_cast<int32_t*>(take(size_t(n) * 4));
@@ -2819,7 +2845,7 @@ static int prune_prepare(const ProjWs& w, int64_t n, const ZSource& zs, const Di
   const int threads = 256;
   const int32_t pos_range = int32_t(int64_t(dv.n_tiles2) * split_rows(split_kp(dv.s)) + 1);
   prune_keys_kernel<<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(
-      zs.hint, n, dv.d, dv.tc2_pos, w.lbz, dv.bounds, pos_range, w.pkeys, w.pvals);
+      w.hbest, n, dv.d, dv.tc2_pos, w.lbz, dv.bounds, pos_range, w.pkeys, w.pvals);
   CBB_CUDA_TRY(cudaGetLastError());
   int bits = 1;
   while ((int64_t(1) << bits) <= 4 * int64_t(pos_range)) ++bits;
@@ -2852,7 +2878,8 @@ static int launch_tc_as(const ProjWs& w, int64_t n, const ZSource& zs, const Dic
     const int kw = SPLIT ? KP : 8 * tc_nc(dv.s);  // row width (fp16 elements) as stored
     const int64_t chunks = int64_t(n_vt) * nh * C::BN * (kw / 8);
     hint_tiles_kernel<<<unsigned((chunks + 255) / 256), 256, 0, st>>>(
-        zs.hint, n, dv.d, n_vt, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, kw, SPLIT ? 1 : 0, C::BN,
+        PRUNE ? w.hbest : zs.hint, n, dv.d, n_vt, vox, SPLIT ? dv.atoms_tc2 : dv.atoms_tc, kw,
+        SPLIT ? 1 : 0, C::BN,
         nh, PRUNE ? w.vperm : nullptr, SPLIT ? dv.tc2_pos : nullptr, w.hint_tiles);
     CBB_CUDA_TRY(cudaGetLastError());
     count_launches(1);
@@ -3101,7 +3128,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
         zs, n, n_pad, dv.s, split ? split_kp(dv.s) : dv.kpad, dv.bounds,
         algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
-        algo == 1 ? w.init_tc : nullptr, split ? 1 : 0, prune ? w.lbz : nullptr);
+        algo == 1 ? w.init_tc : nullptr, split ? 1 : 0, prune ? w.lbz : nullptr,
+        prune ? w.hbest : nullptr);
     CBB_CUDA_TRY(cudaGetLastError());
     ZSource zr = zs;  // IPG mode: later kernels read Z from z_out
     if (zr.x != nullptr) {
@@ -3140,7 +3168,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
       prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                                dv.bounds, nullptr, nullptr,
                                                                nullptr, dv.s_pad, dv.atoms64,
-                                                               dv.d, nullptr, 0, nullptr);
+                                                               dv.d, nullptr, 0, nullptr,
+                                                               nullptr);
       CBB_CUDA_TRY(cudaGetLastError());
     }
     int rc = launch_exhaustive(n, zr, dv, nullptr, nullptr, o, st);
@@ -3239,7 +3268,7 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
   prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
                                                              w.win32, dv.s_pad, dv.atoms64, dv.d,
-                                                             w.init_tc, 0, nullptr);
+                                                             w.init_tc, 0, nullptr, nullptr);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

@@ -77,6 +77,8 @@ struct ZSource {
   const int32_t* hint; // optional per-voxel atom index (e.g. the previous IPG winner): its exact
                        // score seeds the screen's running max (warm start); may be null
   const float* mu_ptr; // IPG mode: mu read from device memory (graph-captured trials), else mu
+  const int32_t* hint2; // optional second warm-start atom per voxel (e.g. the previous trial's
+                        // winner): the better-scoring of the two hints seeds the screen
 };
 
 // Outputs.  Any pointer may be null (not produced).

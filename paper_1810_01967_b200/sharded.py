@@ -127,7 +127,7 @@ class ShardedIpgState(IpgState):
         self.AX = torch.zeros((L_r, self.cm), **c64)
         self.R = torch.empty((L_r, self.cm), **c64)
         self.idx = torch.zeros(nl, dtype=torch.int32, device=device)
-        self.idx_n = torch.empty(nl, dtype=torch.int32, device=device)
+        self.idx_n = torch.zeros(nl, dtype=torch.int32, device=device)
         self.gam = torch.zeros(nl, dtype=torch.float64, device=device)
         self.gam_n = torch.empty(nl, dtype=torch.float64, device=device)
         self.scal = torch.zeros(8, dtype=torch.float64, device=device)

@@ -170,7 +170,7 @@ class IpgState:
         self.AX = torch.zeros((self.L, self.cm), **c64)
         self.R = torch.empty((self.L, self.cm), **c64)
         self.idx = torch.zeros(n, dtype=torch.int32, device=device)
-        self.idx_n = torch.empty(n, dtype=torch.int32, device=device)
+        self.idx_n = torch.zeros(n, dtype=torch.int32, device=device)
         self.gam = torch.zeros(n, dtype=torch.float64, device=device)
         self.gam_n = torch.empty(n, dtype=torch.float64, device=device)
         self.scal = torch.zeros(8, dtype=torch.float64, device=device)  # device scalars
@@ -182,7 +182,21 @@ class IpgState:
         self._graphs = {}          # device-decided iteration graphs, per buffer parity
 
     def _rws(self):
-        return workspace(self.rws_bytes, self.dev, "reduce")
+        """The state's own reduction workspace (allocated once: the captured iteration graphs
+        point at it, and one solve drives a state at a time)."""
+        buf = self.__dict__.get("_rws_buf")
+        if buf is None:
+            buf = self._rws_buf = torch.empty(max(int(self.rws_bytes), 256), dtype=torch.uint8,
+                                              device=self.dev)
+        return buf
+
+    def project_workspace(self):
+        """The state's own projection workspace (sized for the dictionary's tile pruning)."""
+        buf = self.__dict__.get("_pws_buf")
+        if buf is None:
+            buf = self._pws_buf = torch.empty(max(int(self.pws_bytes), 256), dtype=torch.uint8,
+                                              device=self.dev)
+        return buf
 
     def load_measurements(self, Y, weights):
         """Upload Y in the caller's layout and precision into the frame-major complex64 buffer
@@ -271,16 +285,18 @@ class IpgState:
         _lib.check(self.lib.cbb_scale_c64(t.data_ptr(), float(alpha), t.numel(),
                                           _lib.stream_ptr()), "scale")
 
-    def project_step(self, mu, slot):
-        """Xn = P(X - mu G), dX = Xn - X, scal[slot] = ||dX||^2 (solver.py:128-130)."""
-        ws = workspace(self.pws_bytes, self.dev, "project")
+    def project_step(self, mu, slot, mu_dev=None):
+        """Xn = P(X - mu G), dX = Xn - X, scal[slot] = ||dX||^2 (solver.py:128-130).  Warm
+        start: the current atoms (idx) and the previous trial's winners (idx_n, still in place
+        until this projection overwrites them) -- any atom's exact score bounds the maximum."""
+        ws = self.project_workspace()
         o = self.scal[slot:slot + 1]
-        _lib.check(self.lib.cbb_project_step(
-            self.X.data_ptr(), self.G.data_ptr(), float(mu), self.Z.data_ptr(), self.n,
-            ctypes.byref(self.dd.view), self.idx.data_ptr(),   # warm start: current atoms
-            self.idx_n.data_ptr(), self.gam_n.data_ptr(),
-            self.Xn.data_ptr(), self.dX.data_ptr(), o.data_ptr(), ws.data_ptr(), self.pws_bytes,
-            self.algo, _lib.stream_ptr()), "cbb_project_step")
+        _lib.check(self.lib.cbb_project_step_ex(
+            self.X.data_ptr(), self.G.data_ptr(), float(mu), mu_dev, self.Z.data_ptr(), self.n,
+            ctypes.byref(self.dd.view), self.idx.data_ptr(), self.idx_n.data_ptr(),
+            self.idx_n.data_ptr(), self.gam_n.data_ptr(), self.Xn.data_ptr(), self.dX.data_ptr(),
+            o.data_ptr(), ws.data_ptr(), self.pws_bytes, self.algo, _lib.stream_ptr()),
+            "cbb_project_step_ex")
 
     def decompress(self, Xs):
         return Xs if self.V is None else Xs @ self.V.conj().transpose(0, 1)
@@ -312,13 +328,7 @@ class IpgState:
 
     def project_step_dev(self, slot):
         """project_step with mu from the trial state (fp32 image of the fp64 mu)."""
-        ws = workspace(self.pws_bytes, self.dev, "project")
-        o = self.scal[slot:slot + 1]
-        _lib.check(self.lib.cbb_project_step_dmu(
-            self.X.data_ptr(), self.G.data_ptr(), self.ts.data_ptr() + 16, self.Z.data_ptr(),
-            self.n, ctypes.byref(self.dd.view), self.idx.data_ptr(), self.idx_n.data_ptr(),
-            self.gam_n.data_ptr(), self.Xn.data_ptr(), self.dX.data_ptr(), o.data_ptr(),
-            ws.data_ptr(), self.pws_bytes, self.algo, _lib.stream_ptr()), "cbb_project_step_dmu")
+        self.project_step(0.0, slot, mu_dev=self.ts.data_ptr() + 16)
 
     def _capture_iteration(self, config, carry):
         lib = self.lib

@@ -10,12 +10,15 @@ import time
 import torch
 
 from paper_1810_01967_b200 import _lib, workloads
-from paper_1810_01967_b200.device import workspace
 from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
 from paper_1810_01967_b200.solver import SolverConfig, solve_compressed
 
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+if "nograph" in sys.argv[3:]:
+    # development: the host-driven iteration (every kernel visible to ncu's launch list)
+    from paper_1810_01967_b200.solver import IpgState
+    IpgState.graph_capable = lambda self, config: False
 dev = torch.device("cuda:0")
 cfg = getattr(workloads, f"make_{which}")(device=dev)
 s = cfg.cdict.s
@@ -26,7 +29,7 @@ stats = []
 
 def hook(k, st, mu, shrinks, fixed):
     listed, total = ctypes.c_int64(0), ctypes.c_int64(0)
-    ws = workspace(st.pws_bytes, st.dev, "project")
+    ws = st.project_workspace()
     lib.cbb_project_prune_stats(ws.data_ptr(), st.pws_bytes, st.n, ctypes.byref(st.dd.view),
                                 ctypes.byref(listed), ctypes.byref(total), _lib.stream_ptr())
     stats.append((k, shrinks, listed.value / max(1, total.value) if listed.value >= 0 else None))
