@@ -340,18 +340,24 @@ constexpr int kChunkShift = 20;
 __device__ __forceinline__ int pack_chunk(int64_t jb, uint32_t mask) {
   return int(uint32_t(jb >> 5) | (mask << kChunkShift));
 }
-// Single-atom record (split screen: usually one atom of a recorded chunk is inside the narrow
-// window): bit 31 set, the atom's offset inside the chunk in bits [26, 31), no group mask.
-constexpr uint32_t kSingleAtom = 1u << 31;
-__device__ __forceinline__ int pack_single(int64_t jb, int offset) {
-  return int(uint32_t(jb >> 5) | (uint32_t(offset) << 26) | kSingleAtom);
+// Explicit-atom record (split screen: usually one or two atoms of a recorded chunk are inside
+// the narrow window): bit 31 set, the first atom's offset inside the chunk in bits [20, 25), a
+// second one in bits [25, 30) when bit 30 is set; no group mask.
+constexpr uint32_t kExplicitAtoms = 1u << 31;
+__device__ __forceinline__ int pack_atoms(int64_t jb, uint32_t in) {  // popc(in) in {1, 2}
+  const uint32_t a = uint32_t(__ffs(in) - 1);
+  const uint32_t rest = in & (in - 1);
+  uint32_t x = uint32_t(jb >> 5) | (a << 20) | kExplicitAtoms;
+  if (rest) x |= (uint32_t(__ffs(rest) - 1) << 25) | (1u << 30);
+  return int(x);
 }
-// (first atom of the record, 64-bit mask of the atoms to rescore relative to it)
+// (first atom of the record, 32-bit mask of the atoms to rescore relative to it)
 __device__ __forceinline__ void unpack_record(int x, int64_t& j0, uint32_t& atoms) {
   const uint32_t u = uint32_t(x);
   j0 = int64_t(u & ((1u << kChunkShift) - 1)) << 5;
-  if (u & kSingleAtom) {
-    atoms = 1u << ((u >> 26) & 31u);
+  if (u & kExplicitAtoms) {
+    atoms = 1u << ((u >> 20) & 31u);
+    if (u & (1u << 30)) atoms |= 1u << ((u >> 25) & 31u);
     return;
   }
   const uint32_t g = (u >> kChunkShift) & 0x3Fu;  // 6-atom groups (the last one: atoms 30, 31)
@@ -1228,8 +1234,8 @@ __device__ __forceinline__ void record_chunk_f32(const uint32_t* r, float cm, in
   uint32_t in = 0;  // atoms of the chunk inside the window
 #pragma unroll
   for (int i = 0; i < 32; ++i) in |= (__uint_as_float(r[i]) >= thr ? 1u : 0u) << i;
-  if (__popc(in) == 1) {  // the usual case with the split screen's 2^-18 window
-    cl.insert(pack_single(jb, __ffs(in) - 1), cm, thr);
+  if (__popc(in) <= 2) {  // the usual case with the split screen's 2^-18 window
+    cl.insert(pack_atoms(jb, in), cm, thr);
     return;
   }
   uint32_t mask = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])) >= thr ? (1u << 5) : 0u;
@@ -1483,7 +1489,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
           // list entry loaded before the ring wait (its latency overlaps the wait)
           int ba;
           if constexpr (PRUNE) {
-            ba = b >= n_hint ? int(lst[b - n_hint]) : 0;
+            // per-CTA rotation of the list (neighbouring voxel tiles have similar lists:
+            // without it all CTAs stream the same atom tiles at the same time)
+            int q = b - n_hint + (int(blockIdx.x) * un.len) / int(gridDim.x);
+            if (q >= un.len) q -= un.len;
+            ba = b >= n_hint ? int(lst[q]) : 0;
           } else {
             ba = rot + b - n_hint;
             if (ba >= nBh) ba -= nBh;
@@ -1792,7 +1802,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
           const int qt = int(kk - kb) - n_hint;  // < 0: warm-start hint tile
           int ba;
           if constexpr (PRUNE) {
-            ba = qt >= 0 ? int(lst[qt]) : 0;       // loaded before the wait
+            const int len = T - n_hint;
+            int q = qt + (int(blockIdx.x) * len) / int(gridDim.x);  // the producer's rotation
+            if (q >= len) q -= len;
+            ba = qt >= 0 ? int(lst[q]) : 0;       // loaded before the wait
           } else {
             ba = rot + qt;                         // range tile (rot + qt) % nBh
             if (ba >= nBh) ba -= nBh;
@@ -1954,11 +1967,16 @@ __global__ void __launch_bounds__(256) rescore_fast_kernel(
     return;
   }
   const int s = dv.s;
-  double zr[32], zi[32];
-  for (int k = 0; k < s; ++k) {
-    const double2 z = load_z(zs, v, s, k);
-    zr[k] = z.x;
-    zi[k] = z.y;
+  // the voxel in registers (compile-time width S; S == 0: runtime s <= 32 in local memory)
+  constexpr int SA = S > 0 ? S : 32;
+  double zr[SA], zi[SA];
+#pragma unroll
+  for (int k = 0; k < SA; ++k) {
+    if (k < s) {
+      const double2 z = load_z(zs, v, s, k);
+      zr[k] = z.x;
+      zi[k] = z.y;
+    }
   }
   int64_t best = INT64_MAX;
   double bs = -INFINITY;

@@ -229,6 +229,36 @@ class DeviceDictionary:
         atoms have near-duplicates inside the fp16 screen's window (``coherence`` bound)."""
         return bool(self.view.prefer_split)
 
+    def representatives(self):
+        """For a prune-capable (coherent, bisection-ordered) dictionary: the atom nearest to
+        each split tile's centroid, as (atom indices int32 on the device, their prepared
+        ``DeviceDictionary``); None otherwise.  A projection onto these few atoms gives every
+        voxel a good warm-start atom when it has none (the IPG's first iteration, X = 0)."""
+        if not self.view.tile_c:
+            return None
+        rep = self.__dict__.get("_reps")
+        if rep is None:
+            d, s = self.d, self.s
+            nt = int(self.view.n_tiles2)
+            rows = 128 if s <= 10 else 64                              # split_rows(split_kp(s))
+            base = self.storage.data_ptr()
+            perm = self.storage[int(self.view.tc2_atom) - base:][:4 * d].view(torch.int32)
+            perm = perm.to(torch.int64)
+            a = self.atoms64()[perm]                                   # bisection order
+            idx = torch.arange(nt * rows, device=self.device).clamp_max(d - 1)
+            tiles = a[idx].view(nt, rows, s)
+            valid = (torch.arange(nt * rows, device=self.device) < d).view(nt, rows)
+            cnt = valid.sum(1, keepdim=True)
+            cen = (tiles * valid[..., None]).sum(1) / cnt
+            dist = torch.linalg.vector_norm(tiles - cen[:, None, :], dim=2)
+            dist = torch.where(valid, dist, torch.full_like(dist, float("inf")))
+            best = dist.argmin(1)                                      # row inside the tile
+            pos = torch.arange(nt, device=self.device) * rows + best
+            atoms_idx = perm[pos].to(torch.int32)
+            rep = self._reps = (atoms_idx, DeviceDictionary(self.atoms64()[atoms_idx.long()],
+                                                             self.device))
+        return rep
+
     def bounds(self) -> dict:
         """Certified rounding bounds of the prepared copies (``cbb_project.cuh`` kB* slots)."""
         off = int(self.view.bounds) - self.storage.data_ptr()

@@ -254,6 +254,19 @@ class IpgState:
                                               self._rws().data_ptr(), _lib.stream_ptr()),
                        "norm2")
 
+    def cold_hint(self):
+        """Warm-start atoms for an iterate without any (X = 0, the first iteration): the
+        argmax over the dictionary's tile representatives of Z = -mu G (mu > 0 does not change
+        the argmax), mapped to atom indices, in place of the all-zero idx.  Only a hint: the
+        projection's result does not depend on it."""
+        reps = self.dd.representatives()
+        if reps is None:
+            return
+        from .projection import project_device
+        atoms_idx, rdd = reps
+        ridx, _, _ = project_device(-self.G, rdd, idx_int64=True, proj_c128=False)
+        self.idx.copy_(atoms_idx[ridx])
+
     def gradient(self):
         """G = compress(A^H R) with R = w (A X - Y) from the last fidelity evaluation."""
         if self.V is not None:
@@ -494,6 +507,8 @@ def _ipg_loop(st, config, mu_base, y_norm, gt_t, gt_norm, n, d, on_iter=None):
                 break
             continue
         st.gradient()
+        if k == 1 and hasattr(st, "cold_hint"):
+            st.cold_hint()                       # X = 0: warm-start atoms from the tile reps
         mu = mu_base
         shrinks = 0
         fixed_pt = False
