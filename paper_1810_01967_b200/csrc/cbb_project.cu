@@ -1379,7 +1379,10 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
   uint64_t* acc_free2 = t_full2 + C::kTBars;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a lane-0 shuffle: provably warp-uniform, so per-warp addresses (TMEM
+  // stages, barriers, descriptors) stay in uniform registers instead of R2UR moves before every
+  // tcgen05 instruction
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int64_t d = dv.d;
   const int nB = int((d + BN - 1) / BN);
   // work unit u (the CTA's units are u = blockIdx.x + it * gridDim.x): voxel tile u / nsplit,
@@ -1512,6 +1515,69 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         }
         b -= T;
       }
+    }
+  } else if (!SPLIT && !PRUNE && !BOUND && warp >= 1 && warp <= kParts) {
+    // ------------------------------------------------ fp16 screen: lean MMA issuers
+    // Issuer `me` owns accumulator stage me, completion barrier me and the ring stages me,
+    // me + kParts, me + 2 kParts (kStages == 3 kParts): its tiles kk = me (mod kParts) of the
+    // fixed-length units (T tiles each) run through a 3-way unrolled loop whose descriptors are
+    // loop constants, so the release -> MMA hop is two barrier tests, a fence and the MMAs.
+    static_assert(C::kStages == 3 * kParts && C::kAcc == kParts && C::kTBars == kParts,
+                  "lean issuer: ring of 3 kParts stages, one accumulator stage per issuer");
+    const uint32_t me = uint32_t(warp - 1);
+    const int nks = mma_ksteps(dv.s);
+    const uint32_t tb0 = __shfl_sync(0xffffffffu, tbase, 0);
+    const uint32_t d_tm = tb0 + me * uint32_t(C::kAccCols);
+    const uint32_t a_tm0 = tb0 + uint32_t(C::kAColOff);
+    const uint32_t b_base = smem_u32(smem + C::kOffB);
+    uint64_t bd[3][KP / 16];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int kq = 0; kq < KP / 16; ++kq)
+        bd[j][kq] = umma_desc_interleave(
+            b_base + (me + uint32_t(j * kParts)) * uint32_t(C::kBBytes) + kq * 256, 128,
+            nc * 128);
+    const uint32_t T = uint32_t(n_hint + nBh);
+    const uint32_t total = uint32_t(my_vts) * T;
+    uint64_t* const accf = acc_free + me;
+    uint64_t* const tfull = t_full + me;
+    uint32_t kk = me, uend = T, acc_par = 1u, ph = 0u;
+    int it = 0;
+    if (my_vts > 0) mbar_wait(a_full, 0);
+    while (kk < total) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (kk < total) {
+          if (kk >= uend) {  // first tile of the next unit: its A buffer
+            ++it;
+            uend += T;
+            mbar_wait(a_full + (it & 1), (it >> 1) & 1);
+          }
+          const bool last = kk + kParts >= uend;
+          const uint32_t a_tm = a_tm0 + uint32_t((it & 1) * C::kACols);
+          uint64_t* const bfull = b_full + me + j * kParts;
+          mbar_wait(bfull, ph);
+          mbar_wait(accf, acc_par);
+          if (lane == 0) CBB_STAMP(4, kk);
+          acc_par ^= 1u;
+          tc_fence_after();
+          if (lane == 0) CBB_STAMP(0, kk);
+          if (elect_one()) {
+            tc_mma_f16_ts(d_tm, a_tm, bd[j][0], C::kIdesc, 0u);
+#pragma unroll
+            for (int kq = 1; kq < KP / 16; ++kq)
+              if (kq < nks) tc_mma_f16_ts(d_tm, a_tm + uint32_t(kq * 8), bd[j][kq], C::kIdesc, 1u);
+            CBB_STAMP(1, kk);
+            tc_commit(b_empty + me + j * kParts);
+            tc_commit(tfull);
+            if (last) tc_commit(a_empty + (it & 1));
+          }
+          __syncwarp();
+          kk += kParts;
+        }
+      }
+      ph ^= 1u;
     }
   } else if (warp >= 1 && warp <= kParts) {
     // ------------------------------------------------ MMA issuers (warp-uniform, elected lane)
