@@ -1183,10 +1183,27 @@ __device__ __forceinline__ void record_chunk(const uint32_t* r, __half cm, int64
   cl.insert(pack_chunk(jb, mask), __half2float(cm), thr_f);
 }
 
+// Highest of the parts' published thresholds (shared words tag | fp16 bits) whose tag is this
+// voxel tile's; -inf if none.  Words of an older voxel tile (or the -inf init) are ignored.
+__device__ __forceinline__ __half pub_thr(uint32_t w, uint32_t tag) {
+  return __ushort_as_half((w & 0xffff0000u) == tag ? uint16_t(w) : uint16_t(0xFC00));
+}
+__device__ __forceinline__ uint4 lds_v4_volatile(const uint32_t* p) {
+  uint4 w;
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "r"(smem_u32(p)));
+  return w;
+}
+__device__ __forceinline__ __half shared_thr(uint4 w, uint32_t tag) {
+  return __hmax(__hmax(pub_thr(w.x, tag), pub_thr(w.y, tag)), pub_thr(w.z, tag));
+}
+
 template <int NC, class CL>
 __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_t jb, float win,
                                             __half& runmax, __half& thr, bool& active,
-                                            CL& cl, uint32_t* pub, uint32_t tag) {
+                                            CL& cl, uint32_t* pub, uint32_t tag,
+                                            const uint32_t* pthr_row) {
   // NC independent 3-input chains, one per 32-atom chunk (8 VHMNMX/HMNMX2 each)
   __half2 c[NC];
 #pragma unroll
@@ -1201,8 +1218,12 @@ __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_
 #pragma unroll
   for (int k = 1; k < NC; ++k) m = __hmax2(m, c[k]);
   const __half cm = hmax_halves(m);
-  // warp-uniform test: the fast path carries no divergent branch / reconvergence
+  // warp-uniform test against the part's own threshold: the fast path carries no divergent
+  // branch, no shared-memory read and no reconvergence
   if (__any_sync(0xffffffffu, __hge(cm, thr))) {
+    // the other parts' published thresholds (any of them bounds the window edge from below)
+    // are read only here, where they can still turn the tile back into a fast one
+    thr = __hmax(thr, shared_thr(lds_v4_volatile(pthr_row), tag));
     if (__hge(cm, thr)) {
       runmax = __hmax(runmax, cm);
       if (active) {
@@ -1301,22 +1322,6 @@ __device__ __forceinline__ __half tile_max_f16(const uint32_t (&r)[16 * NC]) {
 #pragma unroll
   for (int i = 1; i + 1 < 16 * NC; i += 2) a = hmax3(a, as_h2(r[i]), as_h2(r[i + 1]));
   return hmax_halves(__hmax2(a, as_h2(r[16 * NC - 1])));
-}
-
-// Highest of the parts' published thresholds (shared words tag | fp16 bits) whose tag is this
-// voxel tile's; -inf if none.  Words of an older voxel tile (or the -inf init) are ignored.
-__device__ __forceinline__ __half pub_thr(uint32_t w, uint32_t tag) {
-  return __ushort_as_half((w & 0xffff0000u) == tag ? uint16_t(w) : uint16_t(0xFC00));
-}
-__device__ __forceinline__ uint4 lds_v4_volatile(const uint32_t* p) {
-  uint4 w;
-  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-               : "r"(smem_u32(p)));
-  return w;
-}
-__device__ __forceinline__ __half shared_thr(uint4 w, uint32_t tag) {
-  return __hmax(__hmax(pub_thr(w.x, tag), pub_thr(w.y, tag)), pub_thr(w.z, tag));
 }
 
 template <int KP>
@@ -1853,10 +1858,9 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         ba += hr * nBh;
         const int bend = hr * nBh + nBh;
         for (; kk < kend; kk += kParts) {
-          const uint4 w = lds_v4_volatile(pthr_row);
           consume();
-          thr = __hmax(thr, shared_thr(w, tag));
-          screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl, my_pub, tag);
+          screen_tile<C::kChunks>(r, int64_t(ba) * BN, win, runmax, thr, active, cl, my_pub, tag,
+                                  pthr_row);
           if (q == 0 && lane == 0) CBB_STAMP(6, kk);
           ba += kParts;
           if (ba >= bend) ba -= nBh;
