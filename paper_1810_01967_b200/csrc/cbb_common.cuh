@@ -125,18 +125,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// polling form: test_wait never suspends the thread (lower wake-up latency, costs issue slots)
-__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "SPIN_%=:\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra SPIN_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-
 // shared-window address forms (precomputed addresses: fewer instructions in single-lane loops)
 __device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
   asm volatile(

@@ -371,6 +371,96 @@ __global__ void __launch_bounds__(256) gather_tile_kernel(
   }
 }
 
+// Single-coil form of the location-tiled gather with compile-time channel count S (rows s..S-1
+// of the staged tile and of V are zero, so the padded products add exact zeros), tile width W and
+// mode: the channel reads are LDS with immediate offsets, the pattern / measurement values of a
+// frame's segment are fetched before its FMAs (up to 4 samples per lane in flight), one index
+// e = t m + i addresses pattern, y and the measurements (L m < 2^31), and |y|^2 is summed in fp32
+// per segment before it joins the fp64 partial.  Same FMA order per sample as the other gathers.
+template <int S, int W, int MODE>
+__global__ void __launch_bounds__(512) gather_tile1_kernel(
+    const float2* __restrict__ C, const int* __restrict__ pat, const int* __restrict__ seg,
+    int nb, int64_t n, int L, int m, int s, const float2* __restrict__ V, float scale,
+    const float2* __restrict__ Ymeas, const float* __restrict__ w, float2* __restrict__ Y,
+    double* __restrict__ partial) {
+  extern __shared__ float2 kt[];  // [S][W], swizzled columns
+  __shared__ double sh[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t w0 = int64_t(b) * W;
+    const int wn = int(n - w0 < W ? n - w0 : W);
+    __syncthreads();  // previous tile fully consumed
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      for (int j = threadIdx.x; j < W; j += 512)
+        kt[q * W + tile_swz(j)] =
+            (q < s && j < wn) ? C[int64_t(q) * n + w0 + j] : make_float2(0.f, 0.f);
+    __syncthreads();
+    const int* sb = seg + int64_t(b) * L;  // row b: first sample >= b W; row b + 1: the end
+    for (int t0 = 32 * warp; t0 < L; t0 += 32 * 16) {
+      const int tl = t0 + lane;
+      const int my_lo = tl < L ? sb[tl] : 0, my_hi = tl < L ? sb[L + tl] : 0;
+      uint32_t busy = __ballot_sync(0xffffffffu, my_hi > my_lo);
+      while (busy) {
+        const int j = __ffs(busy) - 1;
+        busy &= busy - 1;
+        const int t = t0 + j;
+        const int lo = __shfl_sync(0xffffffffu, my_lo, j), hi = __shfl_sync(0xffffffffu, my_hi, j);
+        float2 vr[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k)
+          vr[k] = k < s ? __ldg(V + int64_t(t) * s + k) : make_float2(0.f, 0.f);
+        const int e0 = t * m;
+        float psum = 0.f;
+        for (int i0 = lo + lane; i0 < hi; i0 += 128) {
+          int pw[4];
+          float2 ym[4];
+          float ww[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u;
+            pw[u] = i < hi ? __ldg(pat + e0 + i) - int(w0) : -1;
+            if (MODE == 2) {
+              ym[u] = i < hi ? __ldg(Ymeas + e0 + i) : make_float2(0.f, 0.f);
+              ww[u] = (w && i < hi) ? __ldg(w + e0 + i) : 1.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (pw[u] >= 0) {
+              const float2* kc = kt + tile_swz(pw[u]);
+              float yr = 0.f, yi = 0.f;
+#pragma unroll
+              for (int k = 0; k < S; ++k) {
+                const float2 a = kc[k * W], bv = vr[k];
+                yr = fmaf(a.x, bv.x, fmaf(a.y, bv.y, yr));   // a * conj(b)
+                yi = fmaf(a.y, bv.x, fmaf(-a.x, bv.y, yi));
+              }
+              const int e = e0 + i0 + 32 * u;
+              float2 y = make_float2(yr * scale, yi * scale);
+              if (MODE == 2) {
+                y.x -= ym[u].x;
+                y.y -= ym[u].y;
+                psum = fmaf(ww[u], fmaf(y.x, y.x, y.y * y.y), psum);
+                Y[e] = make_float2(ww[u] * y.x, ww[u] * y.y);
+              } else {
+                if (MODE == 0) Y[e] = y;
+                psum = fmaf(y.x, y.x, fmaf(y.y, y.y, psum));
+              }
+            }
+          }
+        }
+        acc += double(psum);
+      }
+    }
+  }
+  if (partial) {
+    double r = block_sum<512>(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = r;
+  }
+}
+
 // seg[b][t] = first sample of frame t at a location >= b W (rows sorted ascending), b = 0..nb
 // (row nb = m): tile b's segments are rows b and b + 1, each L contiguous entries
 __global__ void seg_table_kernel(const int* __restrict__ pat, int L, int m, int nb, int W,
@@ -403,39 +493,72 @@ __global__ void rows_sorted_kernel(const int* __restrict__ pat, int L, int m, in
 // R is read once and feeds all s channel accumulators (registers, S >= s); unsampled locations
 // get 0 (the zero-fill of forward_model.py:160-162).  Consecutive threads write consecutive
 // locations of each channel.
+// V rows are staged once per CTA in shared memory ([L][S] float2, rows zero-padded to S) when they
+// fit: the lanes of a warp read rows of different frames, which costs one L1 pass per distinct
+// line as a global load but only bank-conflict replays as a 16-byte shared load.  The grid is
+// persistent (each CTA walks location blocks) so the staging is amortised.  v_smem == 0: rows
+// from global memory (L s too large).
 template <int S>
-__global__ void __launch_bounds__(256) kspace_s_kernel(const float2* __restrict__ R,
+__global__ void __launch_bounds__(512, (S <= 20 ? 2 : 1)) kspace_s_kernel(const float2* __restrict__ R,
                                                        const int* __restrict__ csr_off,
                                                        const int* __restrict__ csr_e,
-                                                       int64_t n, DivM dm, int c, int s,
+                                                       int64_t n, DivM dm, int c, int s, int L,
                                                        const float2* __restrict__ V,
-                                                       float2* __restrict__ K) {
-  const int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (wloc >= n) return;
-  const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
+                                                       float2* __restrict__ K, int v_smem) {
+  static_assert(S % 2 == 0, "16-byte row reads");
+  extern __shared__ float4 vs4[];  // [L][S / 2]
+  if (v_smem) {
+    float2* vs = reinterpret_cast<float2*>(vs4);
+    for (int idx = threadIdx.x; idx < L * S; idx += blockDim.x) {
+      const int t = idx / S, k = idx - t * S;
+      vs[idx] = k < s ? V[int64_t(t) * s + k] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+  }
   const int m = dm.m;
   const int64_t cm = int64_t(c) * m;
-  for (int ci = 0; ci < c; ++ci) {
-    float2 acc[S];
+  for (int64_t wloc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; wloc < n;
+       wloc += int64_t(gridDim.x) * blockDim.x) {
+    const int b = csr_off[wloc], e_end = csr_off[wloc + 1];
+    for (int ci = 0; ci < c; ++ci) {
+      float2 acc[S];
 #pragma unroll
-    for (int k = 0; k < S; ++k) acc[k] = make_float2(0.f, 0.f);
-    for (int j = b; j < e_end; ++j) {
-      const uint32_t e = uint32_t(csr_e[j]);
-      const uint32_t t = dm.div(e), i = e - t * uint32_t(m);
-      const float2 r = R[int64_t(t) * cm + int64_t(ci) * m + i];
-      const float2* vt = V + int64_t(t) * s;
+      for (int k = 0; k < S; ++k) acc[k] = make_float2(0.f, 0.f);
+      if (v_smem) {
+        for (int j = b; j < e_end; ++j) {
+          const uint32_t e = uint32_t(__ldg(csr_e + j));
+          const uint32_t t = dm.div(e), i = e - t * uint32_t(m);
+          const float2 r = __ldg(R + int64_t(t) * cm + int64_t(ci) * m + i);
+          const float4* vt = vs4 + t * (S / 2);
 #pragma unroll
-      for (int k = 0; k < S; ++k) {
-        if (k < s) {
-          const float2 v = vt[k];
-          acc[k].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[k].x));
-          acc[k].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[k].y));
+          for (int k2 = 0; k2 < S / 2; ++k2) {
+            const float4 v = vt[k2];
+            acc[2 * k2].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[2 * k2].x));
+            acc[2 * k2].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[2 * k2].y));
+            acc[2 * k2 + 1].x = fmaf(r.x, v.z, fmaf(-r.y, v.w, acc[2 * k2 + 1].x));
+            acc[2 * k2 + 1].y = fmaf(r.x, v.w, fmaf(r.y, v.z, acc[2 * k2 + 1].y));
+          }
+        }
+      } else {
+        for (int j = b; j < e_end; ++j) {
+          const uint32_t e = uint32_t(csr_e[j]);
+          const uint32_t t = dm.div(e), i = e - t * uint32_t(m);
+          const float2 r = R[int64_t(t) * cm + int64_t(ci) * m + i];
+          const float2* vt = V + int64_t(t) * s;
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            if (k < s) {
+              const float2 v = vt[k];
+              acc[k].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[k].x));
+              acc[k].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[k].y));
+            }
+          }
         }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < S; ++k)
-      if (k < s) K[(int64_t(ci) * s + k) * n + wloc] = acc[k];
+      for (int k = 0; k < S; ++k)
+        if (k < s) K[(int64_t(ci) * s + k) * n + wloc] = acc[k];
+    }
   }
 }
 
@@ -702,12 +825,47 @@ int op_destroy(Op* op) {
   return kOk;
 }
 
-// Tile width of the location-tiled gather: the largest power of two (<= 2048, and not far past
-// n) whose c*s planes fit 40 KB of shared memory (several CTAs per SM hide the pattern loads).
+// Tile width of the location-tiled gather.  Single coil: 1024 locations for s <= 12 when that
+// leaves >= 2 tiles per SM, else 256 (gather_tile1_kernel).  With coil maps: the largest power of
+// two (<= 2048, and not far past n) whose c*s planes fit 40 KB of shared memory.
+static int padded_s(int s) {
+  const int p[8] = {4, 8, 10, 12, 16, 20, 24, 32};
+  for (int i = 0; i < 8; ++i)
+    if (s <= p[i]) return p[i];
+  return -1;
+}
 static int tile_width(const Op* op, int s) {
+  if (op->c == 1) return (s <= 12 && op->n >= int64_t(1024) * 2 * 148) ? 1024 : 256;
   int W = 2048;
   while (W > 32 && (size_t(op->c) * s * W * sizeof(float2) > 40 * 1024 || W / 2 >= op->n)) W >>= 1;
   return W;
+}
+
+template <int S, int W>
+static int launch_tile1(Op* op, const float2* C, const int* seg, int nb, int grid, int s,
+                        const float2* V, int mode, const float2* Ymeas, const float* w, float2* Y,
+                        double* pp, cudaStream_t st) {
+  const size_t smem = size_t(S) * W * sizeof(float2);
+  int dev = 0;
+  cudaGetDevice(&dev);
+#define CBB_T1(MODE)                                                                           \
+  do {                                                                                         \
+    static uint64_t attr_done = 0; /* per-device shared-memory opt-in */                       \
+    if (!((attr_done >> (dev & 63)) & 1)) {                                                    \
+      CBB_CUDA_TRY(cudaFuncSetAttribute(gather_tile1_kernel<S, W, MODE>,                       \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+      attr_done |= uint64_t(1) << (dev & 63);                                                  \
+    }                                                                                          \
+    gather_tile1_kernel<S, W, MODE><<<grid, 512, smem, st>>>(C, op->pattern, seg, nb, op->n,   \
+                                                             op->L, op->m, s, V, op->scale,    \
+                                                             Ymeas, w, Y, pp);                 \
+  } while (0)
+  if (mode == 0) CBB_T1(0);
+  else if (mode == 1) CBB_T1(1);
+  else CBB_T1(2);
+#undef CBB_T1
+  CBB_CUDA_TRY(cudaGetLastError());
+  return kOk;
 }
 
 // Segment table of the tiled gather for width W (built once per W, stream-ordered).
@@ -835,7 +993,8 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   const int nb = int((op->n + W - 1) / W);
   // location-tiled gather straight from the channel-planar FFT output, when there are enough
   // tiles to fill the GPU (cfg0's 4096 locations are 8 tiles: sample-major below)
-  if (op->rows_sorted && int64_t(op->L) * op->m >= 4 * op->n && nb >= 2 * 148) {
+  if (op->rows_sorted && int64_t(op->L) * op->m >= 4 * op->n &&
+      nb >= (op->c == 1 ? 148 : 2 * 148)) {
     const int* seg = nullptr;
     if ((rc = seg_table(op, W, st, &seg))) return rc;
     int sms = 148;
@@ -847,6 +1006,28 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
     int grid = 8 * sms;
     if (grid > kTileBlocks) grid = kTileBlocks;
     if (grid > nb) grid = nb;
+    if (op->c == 1) {
+      // single coil: compile-time (S, W) kernel, 512 threads; CTAs per SM by shared memory
+      const int S = padded_s(s);
+      const int per_sm = int((200 * 1024) / (size_t(S) * W * sizeof(float2)));
+      grid = sms * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
+      if (grid > nb) grid = nb;
+#define CBB_GT1(SP)                                                                            \
+  rc = (W == 1024) ? launch_tile1<SP, 1024>(op, C, seg, nb, grid, s, V, mode, Ymeas, w, Y, pp, st) \
+                   : launch_tile1<SP, 256>(op, C, seg, nb, grid, s, V, mode, Ymeas, w, Y, pp, st)
+#define CBB_GT1S(SP) rc = launch_tile1<SP, 256>(op, C, seg, nb, grid, s, V, mode, Ymeas, w, Y, pp, st)
+      if (S == 4) CBB_GT1(4);
+      else if (S == 8) CBB_GT1(8);
+      else if (S == 10) CBB_GT1(10);
+      else if (S == 12) CBB_GT1(12);
+      else if (S == 16) CBB_GT1S(16);
+      else if (S == 20) CBB_GT1S(20);
+      else if (S == 24) CBB_GT1S(24);
+      else CBB_GT1S(32);
+#undef CBB_GT1
+#undef CBB_GT1S
+      if (rc) return rc;
+    } else {
     const size_t smem = size_t(op->c) * s * W * sizeof(float2);
 #define CBB_GTILE(SP)                                                                        \
   do {                                                                                       \
@@ -863,6 +1044,7 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
     else CBB_GTILE(32);
 #undef CBB_GTILE
     CBB_CUDA_TRY(cudaGetLastError());
+    }
     if (norm_out) {
       count_launches(launches + 1);
       return finish(part, grid, norm_out, st);
@@ -906,16 +1088,40 @@ int op_adjoint_compressed(Op* op, const float2* R, const float2* V, int s, float
   if (s < 1 || s > 32) return kErrUnsupported;
   float2* K = ws_frames(ws);
   {
-    const unsigned grid = unsigned((op->n + 255) / 256);
-#define CBB_KSPACE(SP)                                                                    \
-  kspace_s_kernel<SP><<<grid, 256, 0, st>>>(R, op->csr_off, op->csr_e, op->n, op->dm, op->c, s, \
-                                            V, K)
-    if (s <= 4) CBB_KSPACE(4);
-    else if (s <= 8) CBB_KSPACE(8);
-    else if (s <= 12) CBB_KSPACE(12);
-    else if (s <= 16) CBB_KSPACE(16);
-    else if (s <= 20) CBB_KSPACE(20);
-    else if (s <= 24) CBB_KSPACE(24);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int S = padded_s(s);
+    // V rows in shared memory when [L][S] float2 fits beside >= 1 CTA per SM
+    const size_t vbytes = size_t(op->L) * S * sizeof(float2);
+    const int v_smem = vbytes <= 200 * 1024 ? 1 : 0;
+    const size_t smem = v_smem ? vbytes : 0;
+    int per_sm = v_smem ? int((220 * 1024) / (vbytes + 1024)) : 4;
+    if (per_sm > 4) per_sm = 4;
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid64 = (op->n + 511) / 512;
+    if (grid64 > int64_t(sms) * per_sm) grid64 = int64_t(sms) * per_sm;
+    const unsigned grid = unsigned(grid64);
+#define CBB_KSPACE(SP)                                                                        \
+  do {                                                                                        \
+    static uint64_t attr_done = 0; /* per-device shared-memory opt-in (largest request) */    \
+    static size_t attr_bytes[64] = {0};                                                       \
+    if (smem > 48 * 1024 && (!((attr_done >> (dev & 63)) & 1) || attr_bytes[dev & 63] < smem)) { \
+      CBB_CUDA_TRY(cudaFuncSetAttribute(kspace_s_kernel<SP>,                                  \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+      attr_done |= uint64_t(1) << (dev & 63);                                                 \
+      attr_bytes[dev & 63] = smem;                                                            \
+    }                                                                                         \
+    kspace_s_kernel<SP><<<grid, 512, smem, st>>>(R, op->csr_off, op->csr_e, op->n, op->dm,    \
+                                                 op->c, s, op->L, V, K, v_smem);              \
+  } while (0)
+    if (S == 4) CBB_KSPACE(4);
+    else if (S == 8) CBB_KSPACE(8);
+    else if (S == 10) CBB_KSPACE(10);
+    else if (S == 12) CBB_KSPACE(12);
+    else if (S == 16) CBB_KSPACE(16);
+    else if (S == 20) CBB_KSPACE(20);
+    else if (S == 24) CBB_KSPACE(24);
     else CBB_KSPACE(32);
 #undef CBB_KSPACE
   }

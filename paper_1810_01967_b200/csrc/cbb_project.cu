@@ -1220,11 +1220,7 @@ __device__ __forceinline__ void screen_tile(const uint32_t (&r)[16 * NC], int64_
   const __half cm = hmax_halves(m);
   // warp-uniform test against the part's own threshold: the fast path carries no divergent
   // branch, no shared-memory read and no reconvergence
-#ifdef CBB_EXP_NOSLOW
-  if (__any_sync(0xffffffffu, __hge(cm, __ushort_as_half(0x7C00)))) {
-#else
   if (__any_sync(0xffffffffu, __hge(cm, thr))) {
-#endif
     // the other parts' published thresholds (any of them bounds the window edge from below)
     // are read only here, where they can still turn the tile back into a fast one
     thr = __hmax(thr, shared_thr(lds_v4_volatile(pthr_row), tag));
@@ -1567,11 +1563,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
           const uint32_t a_tm = a_tm0 + uint32_t((it & 1) * C::kACols);
           uint64_t* const bfull = b_full + me + j * kParts;
           mbar_wait(bfull, ph);
-#ifdef CBB_EXP_ISSSPIN
-          mbar_wait_spin(accf, acc_par);
-#else
           mbar_wait(accf, acc_par);
-#endif
           if (lane == 0) CBB_STAMP(4, kk);
           acc_par ^= 1u;
           tc_fence_after();
@@ -1832,11 +1824,7 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         uint32_t r[16 * C::kChunks];
         auto consume = [&]() {
           if (q == 0 && lane == 0) CBB_STAMP(5, kk);
-#ifdef CBB_EXP_EPISPIN
-          mbar_wait_spin(t_full + part, ph);
-#else
           mbar_wait(t_full + part, ph);
-#endif
           tc_fence_after();
           if (q == 0 && lane == 0) CBB_STAMP(2, kk);
           __syncwarp();

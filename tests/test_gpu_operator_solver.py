@@ -331,6 +331,42 @@ def test_location_major_gather_matches_oracle():
     assert abs(float(out) - nref) <= 1e-5 * nref
 
 
+@pytest.mark.parametrize("shape,L,s", [((96, 64, 64), 12, 10), ((64, 64, 64), 24, 20),
+                                       ((256, 256), 64, 20)])
+def test_location_tiled_gather_matches_oracle(shape, L, s):
+    """Single coil, every frame's pattern row sorted, >= 148 location tiles: the s-channel forward
+    map runs the location-tiled gather (gather_tile1_kernel: 1024-location tiles at s = 10 on
+    393,216 locations, 256-location tiles otherwise; the 2-D case is an EPI-like pattern whose
+    segments are whole k-space lines).  Stored values and the norm-only mode against the oracle
+    chain A(X~ V^H); the adjoint of the same operator for completeness."""
+    from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
+    rng = np.random.default_rng(33)
+    n = int(np.prod(shape))
+    if len(shape) == 2:
+        lines = shape[0] // 4
+        pat = np.stack([(np.sort(rng.choice(shape[0], size=lines, replace=False))[:, None]
+                         * shape[1] + np.arange(shape[1])[None, :]).ravel() for _ in range(L)])
+    else:
+        m = n // 2
+        pat = np.stack([np.sort(rng.choice(n, size=m, replace=False)) for _ in range(L)])
+    A = make_cartesian_operator(SamplingPattern(pat, shape))
+    V, _ = np.linalg.qr(rng.standard_normal((L, s)) + 1j * rng.standard_normal((L, s)))
+    Xc = rng.standard_normal((n, s)) + 1j * rng.standard_normal((n, s))
+    R = oop.CartesianOperator(pat, shape)
+    dev = A.device
+    Xt = torch.from_numpy(Xc.astype(np.complex64)).to(dev)
+    Vt = torch.from_numpy(V.astype(np.complex64)).to(dev)
+    Y = A.fm_apply_compressed(Xt, Vt)
+    ref = R.apply(Xc @ V.conj().T)
+    assert rel(Y.cpu().numpy().T, ref) <= 1e-5
+    out = torch.zeros((), dtype=torch.float64, device=dev)
+    A.fm_apply_norm2_compressed(Xt, Vt, out)
+    nref = np.linalg.norm(ref) ** 2
+    assert abs(float(out) - nref) <= 1e-5 * nref
+    G = A.fm_adjoint_compressed(Y, Vt)
+    assert rel(G.cpu().numpy(), R.adjoint(ref) @ V) <= 1e-5
+
+
 def test_large_projection_unsplit_matches_oracle():
     """More than 2^17 voxels: the screen runs without atom ranges (one range per voxel tile)
     and with a ragged last voxel tile; indices are the oracle's exact argmax."""
