@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
     int nb, int64_t n, int L, int m, int s, const float2* __restrict__ V, float scale,
     const float2* __restrict__ Ymeas, const float* __restrict__ w, float2* __restrict__ Y,
     double* __restrict__ partial) {
-  extern __shared__ float2 kt[];  // [S][W], swizzled columns
+  static_assert(S % 2 == 0, "channel pairs");
+  extern __shared__ float4 kt4[];  // [S / 2][W]: channels 2q, 2q + 1 of a location in one 16-byte slot
   __shared__ double sh[512];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc = 0.0;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
 #pragma unroll
     for (int q = 0; q < S; ++q)
       for (int j = threadIdx.x; j < W; j += 512)
-        kt[q * W + tile_swz(j)] =
+        reinterpret_cast<float2*>(kt4 + (q >> 1) * W + j)[q & 1] =
             (q < s && j < wn) ? C[int64_t(q) * n + w0 + j] : make_float2(0.f, 0.f);
     __syncthreads();
     const int* sb = seg + int64_t(b) * L;  // row b: first sample >= b W; row b + 1: the end
@@ -402,11 +403,27 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
       const int tl = t0 + lane;
       const int my_lo = tl < L ? sb[tl] : 0, my_hi = tl < L ? sb[L + tl] : 0;
       uint32_t busy = __ballot_sync(0xffffffffu, my_hi > my_lo);
-      while (busy) {
+      // software pipeline over the group's non-empty segments: the pattern values of the next
+      // segment's first 128 samples are in flight (DRAM latency) while the current one is computed
+      int t = 0, lo = 0, hi = 0, pw[4];
+      auto take = [&](int& tt, int& l, int& h, int (&p)[4]) -> bool {
+        if (!busy) return false;
         const int j = __ffs(busy) - 1;
         busy &= busy - 1;
-        const int t = t0 + j;
-        const int lo = __shfl_sync(0xffffffffu, my_lo, j), hi = __shfl_sync(0xffffffffu, my_hi, j);
+        tt = t0 + j;
+        l = __shfl_sync(0xffffffffu, my_lo, j);
+        h = __shfl_sync(0xffffffffu, my_hi, j);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = l + lane + 32 * u;
+          p[u] = i < h ? __ldg(pat + tt * m + i) - int(w0) : -1;
+        }
+        return true;
+      };
+      bool have = take(t, lo, hi, pw);
+      while (have) {
+        int tn = 0, lon = 0, hin = 0, pwn[4];
+        const bool have_n = take(tn, lon, hin, pwn);
         float2 vr[S];
 #pragma unroll
         for (int k = 0; k < S; ++k)
@@ -414,14 +431,19 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
         const int e0 = t * m;
         float psum = 0.f;
         for (int i0 = lo + lane; i0 < hi; i0 += 128) {
-          int pw[4];
           float2 ym[4];
           float ww[4];
+          if (i0 != lo + lane) {  // segments longer than 128 samples: later chunks on demand
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = i0 + 32 * u;
-            pw[u] = i < hi ? __ldg(pat + e0 + i) - int(w0) : -1;
-            if (MODE == 2) {
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + 32 * u;
+              pw[u] = i < hi ? __ldg(pat + e0 + i) - int(w0) : -1;
+            }
+          }
+          if (MODE == 2) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + 32 * u;
               ym[u] = i < hi ? __ldg(Ymeas + e0 + i) : make_float2(0.f, 0.f);
               ww[u] = (w && i < hi) ? __ldg(w + e0 + i) : 1.f;
             }
@@ -429,13 +451,16 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (pw[u] >= 0) {
-              const float2* kc = kt + tile_swz(pw[u]);
+              const float4* kc = kt4 + pw[u];
               float yr = 0.f, yi = 0.f;
 #pragma unroll
-              for (int k = 0; k < S; ++k) {
-                const float2 a = kc[k * W], bv = vr[k];
-                yr = fmaf(a.x, bv.x, fmaf(a.y, bv.y, yr));   // a * conj(b)
-                yi = fmaf(a.y, bv.x, fmaf(-a.x, bv.y, yi));
+              for (int k2 = 0; k2 < S / 2; ++k2) {
+                const float4 a = kc[k2 * W];
+                const float2 b0 = vr[2 * k2], b1 = vr[2 * k2 + 1];
+                yr = fmaf(a.x, b0.x, fmaf(a.y, b0.y, yr));   // a * conj(b)
+                yi = fmaf(a.y, b0.x, fmaf(-a.x, b0.y, yi));
+                yr = fmaf(a.z, b1.x, fmaf(a.w, b1.y, yr));
+                yi = fmaf(a.w, b1.x, fmaf(-a.z, b1.y, yi));
               }
               const int e = e0 + i0 + 32 * u;
               float2 y = make_float2(yr * scale, yi * scale);
@@ -452,6 +477,12 @@ __global__ void __launch_bounds__(512) gather_tile1_kernel(
           }
         }
         acc += double(psum);
+        t = tn;
+        lo = lon;
+        hi = hin;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pw[u] = pwn[u];
+        have = have_n;
       }
     }
   }
@@ -525,18 +556,36 @@ __global__ void __launch_bounds__(512, (S <= 20 ? 2 : 1)) kspace_s_kernel(const 
 #pragma unroll
       for (int k = 0; k < S; ++k) acc[k] = make_float2(0.f, 0.f);
       if (v_smem) {
-        for (int j = b; j < e_end; ++j) {
-          const uint32_t e = uint32_t(__ldg(csr_e + j));
-          const uint32_t t = dm.div(e), i = e - t * uint32_t(m);
-          const float2 r = __ldg(R + int64_t(t) * cm + int64_t(ci) * m + i);
-          const float4* vt = vs4 + t * (S / 2);
+        // batches of 4 entries: the 4 CSR loads, then the 4 dependent residual loads, are in
+        // flight together (the accumulation order stays ascending e)
+        for (int j0 = b; j0 < e_end; j0 += 4) {
+          uint32_t tt[4];
+          float2 rr[4];
+          uint32_t ee[4];
 #pragma unroll
-          for (int k2 = 0; k2 < S / 2; ++k2) {
-            const float4 v = vt[k2];
-            acc[2 * k2].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[2 * k2].x));
-            acc[2 * k2].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[2 * k2].y));
-            acc[2 * k2 + 1].x = fmaf(r.x, v.z, fmaf(-r.y, v.w, acc[2 * k2 + 1].x));
-            acc[2 * k2 + 1].y = fmaf(r.x, v.w, fmaf(r.y, v.z, acc[2 * k2 + 1].y));
+          for (int u = 0; u < 4; ++u)
+            ee[u] = j0 + u < e_end ? uint32_t(__ldg(csr_e + j0 + u)) : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            tt[u] = dm.div(ee[u]);
+            const uint32_t i = ee[u] - tt[u] * uint32_t(m);
+            rr[u] = j0 + u < e_end ? __ldg(R + int64_t(tt[u]) * cm + int64_t(ci) * m + i)
+                                   : make_float2(0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (j0 + u < e_end) {
+              const float2 r = rr[u];
+              const float4* vt = vs4 + tt[u] * (S / 2);
+#pragma unroll
+              for (int k2 = 0; k2 < S / 2; ++k2) {
+                const float4 v = vt[k2];
+                acc[2 * k2].x = fmaf(r.x, v.x, fmaf(-r.y, v.y, acc[2 * k2].x));
+                acc[2 * k2].y = fmaf(r.x, v.y, fmaf(r.y, v.x, acc[2 * k2].y));
+                acc[2 * k2 + 1].x = fmaf(r.x, v.z, fmaf(-r.y, v.w, acc[2 * k2 + 1].x));
+                acc[2 * k2 + 1].y = fmaf(r.x, v.w, fmaf(r.y, v.z, acc[2 * k2 + 1].y));
+              }
+            }
           }
         }
       } else {
@@ -569,7 +618,7 @@ __global__ void __launch_bounds__(256) combine_s_kernel(const float2* __restrict
                                                         float2* __restrict__ G) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n) return;
-  for (int k = 0; k < s; ++k) {
+  auto one = [&](int k) {
     float gr = 0.f, gi = 0.f;
     for (int ci = 0; ci < c; ++ci) {
       const float2 a = K[(int64_t(ci) * s + k) * n + v];
@@ -577,7 +626,16 @@ __global__ void __launch_bounds__(256) combine_s_kernel(const float2* __restrict
       gr += sc.x * a.x + sc.y * a.y;   // conj(sc) * a
       gi += sc.x * a.y - sc.y * a.x;
     }
-    G[v * s + k] = make_float2(gr * scale, gi * scale);
+    return make_float2(gr * scale, gi * scale);
+  };
+  if ((s & 1) == 0) {  // rows of G are 16-byte aligned: two channels per store
+    float4* g4 = reinterpret_cast<float4*>(G + v * s);
+    for (int k = 0; k < s; k += 2) {
+      const float2 a = one(k), b = one(k + 1);
+      g4[k >> 1] = make_float4(a.x, a.y, b.x, b.y);
+    }
+  } else {
+    for (int k = 0; k < s; ++k) G[v * s + k] = one(k);
   }
 }
 
@@ -845,7 +903,7 @@ template <int S, int W>
 static int launch_tile1(Op* op, const float2* C, const int* seg, int nb, int grid, int s,
                         const float2* V, int mode, const float2* Ymeas, const float* w, float2* Y,
                         double* pp, cudaStream_t st) {
-  const size_t smem = size_t(S) * W * sizeof(float2);
+  const size_t smem = size_t(S / 2) * W * sizeof(float4);
   int dev = 0;
   cudaGetDevice(&dev);
 #define CBB_T1(MODE)                                                                           \

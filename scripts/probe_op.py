@@ -16,6 +16,9 @@ which = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 dev = torch.device("cuda:0")
 cfg = getattr(workloads, f"make_{which}")(device=dev)
 A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape), device=dev)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()   # ncu --profile-from-start off: only the operator launches
 res = bench.operator_block(A, cfg, dev, cfg.cdict.s)
+torch.cuda.profiler.stop()
 print(which, json.dumps({k: (round(v["ms"], 4), round(v["frac"], 3)) for k, v in res.items()
                          if isinstance(v, dict)}))
