@@ -128,6 +128,18 @@ int cbb_project_step_ex(const void* x, const void* g, double mu, const float* mu
                         double* gamma_out, void* xnext_out, void* dx_out, double* nd_out,
                         void* workspace, size_t workspace_bytes, int32_t algo, void* stream);
 
+/* Warm-start atoms for the first trial of an IPG iteration (solver.py:127-128, the first pass
+ * of the while loop): the exact projection of Z = X - mu*G (written to z_out, mu / mu_dev as in
+ * cbb_project_step_ex) onto the `reps` dictionary -- one representative atom per split tile of the
+ * full dictionary (the atom nearest to the tile's centroid) -- mapped through rep_atoms
+ * (representative -> atom index of the full dictionary) into hint_out (int32 per voxel).  The
+ * current iterate's atoms are a poor lower bound after a large step; the best representative
+ * is within one tile radius of the maximum, so the tile pruning of the following
+ * cbb_project_step_ex lists far fewer tiles.  Only a hint: results do not depend on it. */
+int cbb_project_hint(const void* x, const void* g, double mu, const float* mu_dev, void* z_out,
+                     int64_t n, const cbb_dict_view* reps, const int32_t* rep_atoms,
+                     int32_t* hint_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- device-decided IPG iteration (solver.py:116-144, 155-257) ----
  * A CUDA graph of one iteration: the gradient, a while-conditional node repeating the trial
  * (cbb_project_step_ex + ||A dX||^2 + cbb_trial_decide) until the device accepts mu, reaches the
@@ -175,6 +187,13 @@ int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* 
 int cbb_project_prune_stats(void* workspace, size_t workspace_bytes, int64_t n,
                             const cbb_dict_view* dict, int64_t* listed_host, int64_t* total_host,
                             void* stream);
+/* Per voxel tile of that projection, in screen order (ceil(n / 128) entries each): the length of
+ * its atom-tile list and the bound-tightness bucket of its first voxel (0: hint score >= 0.95
+ * ||z|| max||d||, 1: >= 0.8, 2: >= 0.5, 3: below).  counts_host[0] = -1 if nothing was pruned.
+ * Diagnostic (where the listed pairs come from); synchronises. */
+int cbb_project_prune_detail(void* workspace, size_t workspace_bytes, int64_t n,
+                             const cbb_dict_view* dict, int32_t* counts_host,
+                             int32_t* buckets_host, void* stream);
 /* Bring-up / test hook: prologue only (fp16 voxel rows + windows in the workspace). */
 int cbb_project_prologue(const void* z, int32_t z_c128, int64_t n, const cbb_dict_view* dict,
                          void* workspace, size_t workspace_bytes, void* stream);

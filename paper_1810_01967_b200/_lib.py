@@ -70,6 +70,9 @@ SIGNATURES = {
                                 c_vp]),
     "cbb_project_overflow_counts": (c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "cbb_project_overflow_count": (c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_int), c_vp]),
+    "cbb_project_hint": (c_int, [c_vp, c_vp, c_dbl, c_vp, c_vp, c_i64, ctypes.POINTER(DictView), c_vp, c_vp,
+                         c_vp, c_size, c_vp]),
+    "cbb_project_prune_detail": (c_int, [c_vp, c_size, c_i64, ctypes.POINTER(DictView), c_vp, c_vp, c_vp]),
     "cbb_project_prune_stats": (c_int, [c_vp, c_size, c_i64, ctypes.POINTER(DictView),
                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp]),
     "cbb_project_prologue": (c_int, [c_vp, c_i32, c_i64, ctypes.POINTER(DictView), c_vp, c_size,

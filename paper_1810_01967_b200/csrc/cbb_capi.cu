@@ -32,6 +32,9 @@ int prune_tiles_of(const DictView& dv);
 int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out, double* nd_sum,
             void* ws_ptr, size_t ws_bytes, int algo, int max_ctas, cudaStream_t st);
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st);
+int map_indices(int32_t* idx, const int32_t* table, int64_t n, int64_t table_len, cudaStream_t st);
+int project_prune_detail(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView& dv,
+                         int32_t* counts, int32_t* buckets, cudaStream_t st);
 int project_prune_stats(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView& dv,
                         int64_t* listed, int64_t* total, cudaStream_t st);
 int project_overflow_counts(void* ws_ptr, int64_t n, int s, int* host2, cudaStream_t st);
@@ -224,6 +227,23 @@ int cbb_project_step_ex(const void* x, const void* g, double mu, const float* mu
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));
 }
 
+int cbb_project_hint(const void* x, const void* g, double mu, const float* mu_dev, void* z_out,
+                     int64_t n, const cbb_dict_view* reps, const int32_t* rep_atoms,
+                     int32_t* hint_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_view(reps)) return rc;
+  if (n > 0 && (!x || !g || !z_out || !rep_atoms || !hint_out)) {
+    set_last_error("cbb_project_hint: null argument");
+    return kErrArgument;
+  }
+  ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), float(mu),
+             static_cast<float2*>(z_out), nullptr, mu_dev, nullptr};
+  ProjOut o{hint_out, 0, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0};
+  if (int rc = project(zs, n, to_view(reps), o, nullptr, workspace, workspace_bytes, 0, 0,
+                       S(stream)))
+    return rc;
+  return map_indices(hint_out, rep_atoms, n, reps->d, S(stream));
+}
+
 int cbb_project_overflow_count(void* workspace, int64_t n, int32_t s, int* count_host,
                                void* stream) {
   return project_overflow_count(workspace, n, s, count_host, S(stream));
@@ -236,6 +256,15 @@ int cbb_project_prune_stats(void* workspace, size_t workspace_bytes, int64_t n,
   if (!workspace || !listed_host || !total_host) return kErrArgument;
   return project_prune_stats(workspace, workspace_bytes, n, to_view(dict), listed_host,
                              total_host, S(stream));
+}
+
+int cbb_project_prune_detail(void* workspace, size_t workspace_bytes, int64_t n,
+                             const cbb_dict_view* dict, int32_t* counts_host,
+                             int32_t* buckets_host, void* stream) {
+  if (int rc = check_view(dict)) return rc;
+  if (!workspace || !counts_host || !buckets_host) return kErrArgument;
+  return project_prune_detail(workspace, workspace_bytes, n, to_view(dict), counts_host,
+                              buckets_host, S(stream));
 }
 
 int cbb_project_overflow_counts(void* workspace, int64_t n, int32_t s, int32_t* counts_host,

@@ -3296,6 +3296,44 @@ int project_prune_stats(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView
   return kOk;
 }
 
+// idx[v] = table[idx[v]] (representative -> atom index of the full dictionary)
+__global__ void map_indices_kernel(int32_t* __restrict__ idx, const int32_t* __restrict__ table,
+                                   int64_t n, int64_t table_len) {
+  const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t r = idx[v];
+  idx[v] = (r >= 0 && r < table_len) ? table[r] : -1;
+}
+int map_indices(int32_t* idx, const int32_t* table, int64_t n, int64_t table_len, cudaStream_t st) {
+  if (n <= 0) return kOk;
+  map_indices_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(idx, table, n, table_len);
+  CBB_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  return kOk;
+}
+
+// Per voxel tile (screen order) of the last pruned projection: the list length and the bound-
+// tightness bucket (0: lb / (||z|| dmax) >= 0.95, 1: >= 0.8, 2: >= 0.5, 3: below) of its first
+// voxel.  Diagnostic; synchronises.  counts[0] = -1 if that projection did not prune.
+int project_prune_detail(void* ws_ptr, size_t ws_bytes, int64_t n, const DictView& dv,
+                         int32_t* counts, int32_t* buckets, cudaStream_t st) {
+  const int pt = prune_tiles_of(dv);
+  if (n <= 0) return kOk;
+  counts[0] = -1;
+  if (pt <= 0 || ws_bytes < project_ws_bytes(n, dv.s, nullptr, nullptr, pt)) return kOk;
+  ProjWs w;
+  project_ws_bytes(n, dv.s, &w, ws_ptr, pt);
+  if (!w.prune) return kOk;
+  const int64_t n_vt = (n + 127) / 128;
+  CBB_CUDA_TRY(cudaMemcpyAsync(counts, w.pcnt, size_t(n_vt) * 4, cudaMemcpyDeviceToHost, st));
+  CBB_CUDA_TRY(cudaMemcpy2DAsync(buckets, 4, w.pkeys_out, 128 * 4, 4, size_t(n_vt),
+                                 cudaMemcpyDeviceToHost, st));
+  CBB_CUDA_TRY(cudaStreamSynchronize(st));
+  const int32_t pos_range = int32_t(int64_t(dv.n_tiles2) * split_rows(split_kp(dv.s)) + 1);
+  for (int64_t i = 0; i < n_vt; ++i) buckets[i] /= pos_range;
+  return kOk;
+}
+
 int project_overflow_count(void* ws_ptr, int64_t n, int s, int* host_count, cudaStream_t st) {
   ProjWs w;
   project_ws_bytes(n, s, &w, ws_ptr, 0);

@@ -19,6 +19,9 @@ if "nograph" in sys.argv[3:]:
     # development: the host-driven iteration (every kernel visible to ncu's launch list)
     from paper_1810_01967_b200.solver import IpgState
     IpgState.graph_capable = lambda self, config: False
+if "norephint" in sys.argv[3:]:
+    from paper_1810_01967_b200.solver import IpgState
+    IpgState.rep_hint_min_voxels = 1 << 62
 dev = torch.device("cuda:0")
 cfg = getattr(workloads, f"make_{which}")(device=dev)
 s = cfg.cdict.s
@@ -32,7 +35,18 @@ def hook(k, st, mu, shrinks, fixed):
     ws = st.project_workspace()
     lib.cbb_project_prune_stats(ws.data_ptr(), st.pws_bytes, st.n, ctypes.byref(st.dd.view),
                                 ctypes.byref(listed), ctypes.byref(total), _lib.stream_ptr())
-    stats.append((k, shrinks, listed.value / max(1, total.value) if listed.value >= 0 else None))
+    det = None
+    if "detail" in sys.argv[3:]:
+        import numpy as np
+        n_vt = (st.n + 127) // 128
+        cnt = np.zeros(n_vt, dtype=np.int32)
+        bkt = np.zeros(n_vt, dtype=np.int32)
+        lib.cbb_project_prune_detail(ws.data_ptr(), st.pws_bytes, st.n, ctypes.byref(st.dd.view),
+                                     cnt.ctypes.data, bkt.ctypes.data, _lib.stream_ptr())
+        if cnt[0] >= 0:
+            det = " ".join(f"b{b}: {int((bkt == b).sum())} vt x {cnt[bkt == b].mean() if (bkt == b).any() else 0:.0f}"
+                           for b in range(4))
+    stats.append((k, shrinks, listed.value / max(1, total.value) if listed.value >= 0 else None, det))
 
 
 solve_compressed(cfg.Y, A, cfg.cdict, None, SolverConfig(mode="blip_exact", max_iters=2,
@@ -47,5 +61,5 @@ torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print(f"{which}: {trace.iterations} iterations, loop {trace.total_time * 1e3 / trace.iterations:.2f} "
       f"ms/iter, fidelity {trace.fidelities()[-1]!r}")
-for k, sh, fr in stats:
-    print(f"  iter {k}: shrinks {sh}, listed tile fraction {fr}")
+for k, sh, fr, det in stats:
+    print(f"  iter {k}: shrinks {sh}, listed tile fraction {fr}" + (f"  [{det}]" if det else ""))
