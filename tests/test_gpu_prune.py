@@ -181,3 +181,71 @@ def test_prune_order_is_a_permutation(atoms10):
         c = blk.mean(0)
         assert np.linalg.norm(blk - c, axis=1).max() <= rad[t] * (1 + 1e-5) + 1e-6
     assert np.median(rad) < 0.5
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_representative_hint_leaves_the_trace_unchanged(graphs):
+    """cbb_project_hint: from the second iteration on, the first trial's second warm-start atom
+    is the best tile representative of X - mu G.  It is only a hint: with it (device-decided
+    graphs or the host loop) the solve returns the same iterates, atoms, step sizes and
+    fidelities as without, and in lockstep the atoms are the fp64 oracle's; the first-trial tile
+    lists get shorter."""
+    from paper_1810_01967_b200 import _lib, workloads
+    from paper_1810_01967_b200.forward_model import SamplingPattern, make_cartesian_operator
+    from paper_1810_01967_b200.solver import IpgState, SolverConfig, solve_compressed
+    cfg = workloads.make_cfg4(shape=(32, 32, 8), L=80, s=10, undersample=8, n_t1=40, n_t2=40,
+                              n_b0=6, device=torch.device("cuda"))
+    cd = cfg.cdict
+    A = make_cartesian_operator(SamplingPattern(cfg.pattern, cfg.spatial_shape))
+    conf = SolverConfig(mode="blip_exact", max_iters=6, zeta=2.0, compressed=10)
+    lib = _lib.load()
+    old_min, old_cap = IpgState.rep_hint_min_voxels, IpgState.graph_capable
+    runs = {}
+    try:
+        if not graphs:
+            IpgState.graph_capable = lambda self, config: False
+        for use in (False, True):
+            IpgState.rep_hint_min_voxels = 0 if use else 1 << 62
+            from paper_1810_01967_b200 import solver as _solver
+            _solver._state_cache.clear()              # a fresh state (the flag is cached on it)
+            snaps, listed = [], []
+
+            def on_iter(k, st, mu, shrinks, fixed):
+                assert st.rep_hint_ready() == use
+                snaps.append((k, mu, shrinks, st.idx_n.cpu().numpy().copy(),
+                              st.Z.cpu().numpy().copy()))
+                a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+                ws = st.project_workspace()
+                lib.cbb_project_prune_stats(ws.data_ptr(), st.pws_bytes, st.n,
+                                            ctypes.byref(st.dd.view), ctypes.byref(a),
+                                            ctypes.byref(b), _lib.stream_ptr())
+                listed.append((shrinks, a.value, b.value))
+
+            X, maps, gam, trace = solve_compressed(cfg.Y, A, cd, None, conf, on_iter=on_iter)
+            runs[use] = (X, gam, trace, snaps, listed)
+    finally:
+        IpgState.rep_hint_min_voxels, IpgState.graph_capable = old_min, old_cap
+    (X0, g0, t0, s0, l0), (X1, g1, t1, s1, l1) = runs[False], runs[True]
+    assert t0.iterations == t1.iterations >= 3
+    assert [r["shrinks"] for r in t0.records] == [r["shrinks"] for r in t1.records]
+    assert t0.fidelities() == t1.fidelities()
+    np.testing.assert_array_equal(X0, X1)
+    np.testing.assert_array_equal(g0, g1)
+    for (k, mu, sh, idx, Z), (k1, mu1, sh1, idx1, Z1) in zip(s0, s1):
+        assert (k, mu, sh) == (k1, mu1, sh1)
+        np.testing.assert_array_equal(idx, idx1)
+        np.testing.assert_array_equal(Z, Z1)
+    # lockstep against the oracle on the last accepted trial
+    k, mu, sh, idx, Z = s1[-1]
+    Zd = Z.astype(np.complex128)
+    ref = orc.project_cone_exact(Zd, cd.atoms_compressed)
+    i1, a1, a2 = orc.top2(Zd, cd.atoms_compressed)
+    bad = (idx != ref.indices) & ~orc.near_tie_mask(a1, a2)
+    assert not bad.any()
+    # pruning was active, and iterations accepted at their first trial list no more tiles with
+    # the representative hint than without
+    assert all(b > 0 and a >= 0 for _, a, b in l1)
+    first0 = [a for (sh, a, b) in l0[1:] if sh == 0]
+    first1 = [a for (sh, a, b) in l1[1:] if sh == 0]
+    if first0:
+        assert sum(first1) <= sum(first0)
