@@ -428,10 +428,14 @@ def _gather_rows(snap, world, group):
 
 def operator_block(A, cfg, device, s):
     """Achieved HBM GB/s of the s-channel operator calls of one IPG iteration (CUDA events, 5
-    repetitions each, after the solve), on modelled algorithmic bytes per call:
-      apply     X~ (8ns) + channel images written and FFT'd (c s n complex: 3 x 8csn incl. the
-                location-major copy) + gather (K 8csn, pattern CSR 12 Lm + 4n, y 8cLm)
-      adjoint   residual 8cLm + CSR 12 Lm + 4n + k-space images 8csn + FFT 16csn + combine 8csn + G 8ns
+    repetitions each, after the solve), on the ALGORITHMIC bytes of each call (every array read or
+    written once by the step that needs it; one read + one write for the in-place FFT, which
+    cuFFT performs in 2 (2-D) or 3 (3-D) passes):
+      apply     X~ read 8ns; channel images written 8csn; FFT 16csn; gather: channel images read
+                8csn, pattern 4Lm, y written 8cLm               = 8ns + 32csn + 4Lm + 8cLm
+      norm2     the same without the y write (||A dX||^2 only)   = 8ns + 32csn + 4Lm
+      adjoint   residual read 8cLm; CSR entries 4Lm + offsets 4n; k-space images written 8csn;
+                FFT 16csn; combine reads 8csn, G~ written 8ns    = 8cLm + 4Lm + 4n + 32csn + 8ns
       residual  AX and Y read, R written: 24 cLm
     """
     import torch
@@ -461,12 +465,13 @@ def operator_block(A, cfg, device, s):
         torch.cuda.synchronize()
         return ev[0].elapsed_time(ev[1]) / reps
 
-    csr = 12 * L * m + 4 * n
     calls = {
         "apply": (lambda: A.fm_apply_compressed(Xs, V, out=Y),
-                  8 * n * s + 3 * 8 * c * s * n + 8 * c * s * n + csr + 8 * c * L * m),
+                  8 * n * s + 32 * c * s * n + 4 * L * m + 8 * c * L * m),
+        "norm2": (lambda: A.fm_apply_norm2_compressed(Xs, V, o),
+                  8 * n * s + 32 * c * s * n + 4 * L * m),
         "adjoint": (lambda: A.fm_adjoint_compressed(Y, V, out=G),
-                    8 * c * L * m + csr + 8 * c * s * n + 16 * c * s * n + 8 * c * s * n + 8 * n * s),
+                    8 * c * L * m + 4 * L * m + 4 * n + 32 * c * s * n + 8 * n * s),
         "residual": (lambda: _lib.check(lib.cbb_residual(Y.data_ptr(), Y.data_ptr(), Y.numel(),
                                                          None, R.data_ptr(), o.data_ptr(),
                                                          rws.data_ptr(), _lib.stream_ptr()),

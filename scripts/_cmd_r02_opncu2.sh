@@ -3,7 +3,7 @@ export PYTHONPATH=.
 timeout 600 python scripts/probe_op.py cfg4 2>&1 | tail -1
 timeout 600 python scripts/probe_op.py cfg2 2>&1 | tail -1
 mkdir -p gpurun_out
-R=${R:-r02f}
+R=${R:-r02g}
 for cfg in cfg4 cfg2; do
 timeout 900 ncu --set full --clock-control none -k regex:"gather_tile1|gather_loc|gather_s_kernel|kspace_s|combine_s|channels_kernel|interleave|vec_kernel|regular_fft|vector_fft" --profile-from-start off --launch-count 60 -o /tmp/prof_op_${cfg}_$R -f python scripts/probe_op.py $cfg > gpurun_out/ncu_op_${cfg}_$R.log 2>&1
 echo "ncu op $cfg rc=$?"
