@@ -5,9 +5,9 @@ mkdir -p gpurun_out
 R=${R:-r02g}
 timeout 1200 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${R}_reference.json 2> gpurun_out/bench_${R}_reference.err; echo "ref rc=$?"
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"cbb|_fft" --csv --log-file gpurun_out/bench_launches_$R.csv python bench.py --steps 3 --warmup 3 --skip-cfg3 --skip-cpu-reference > gpurun_out/ncu_launch_$R.log 2>&1
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"mf_tc|mf_ffma|rescore|prologue|gather|kspace|combine_s|channels|interleave|vec_kernel|scale_kernel|hint_tiles|prune_|exhaustive|reduce_stage|finish_sum|trial_|map_indices|coil_transpose|scatter_kernel|coherence|seg_table|rows_sorted|prep_|argmax_select|scaled_rows|_fft|DeviceRadixSort" --csv --log-file gpurun_out/bench_launches_$R.csv python bench.py --steps 3 --warmup 3 --skip-cfg3 --skip-cpu-reference > gpurun_out/ncu_launch_$R.log 2>&1
 echo "ncu launches rc=$?"
-python scripts/summarize_ncu.py launches gpurun_out/bench_launches_$R.csv gpurun_out/bench_launches_${R}_summary.txt "ncu --metrics gpu__time_duration.sum -k regex:cbb|_fft python bench.py --steps 3 --warmup 3 --skip-cfg3 --skip-cpu-reference (the library's kernels and cuFFT; graph-replayed launches are not listed)" > /dev/null
+python scripts/summarize_ncu.py launches gpurun_out/bench_launches_$R.csv gpurun_out/bench_launches_${R}_summary.txt "ncu --metrics gpu__time_duration.sum -k regex:<the library's kernels, cuFFT, CUB sort> python bench.py --steps 3 --warmup 3 --skip-cfg3 --skip-cpu-reference (the library's kernels and cuFFT; graph-replayed launches are not listed)" > /dev/null
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mf_tc_kernel --launch-skip 3 --launch-count 1 -o /tmp/prof_bench_$R -f python bench.py --skip-cfg2 --skip-cfg3 --skip-cfg4 --skip-cpu-reference > gpurun_out/ncu_full_$R.log 2>&1
 echo "ncu full rc=$?"
 python scripts/summarize_ncu.py full /tmp/prof_bench_$R.ncu-rep gpurun_out/mf_tc_ncu_full_$R.txt gpurun_out/roofline_traffic_$R.json "ncu --set full -k regex:mf_tc_kernel --launch-skip 3 --launch-count 1 python bench.py (cfg1 screen)" > /dev/null
