@@ -892,8 +892,8 @@ static int padded_s(int s) {
     if (s <= p[i]) return p[i];
   return -1;
 }
-static int tile_width(const Op* op, int s) {
-  if (op->c == 1) return (s <= 12 && op->n >= int64_t(1024) * 2 * 148) ? 1024 : 256;
+static int tile_width(const Op* op, int s, int mode) {
+  if (op->c == 1 && mode != 2) return (s <= 12 && op->n >= int64_t(1024) * 2 * 148) ? 1024 : 256;
   int W = 2048;
   while (W > 32 && (size_t(op->c) * s * W * sizeof(float2) > 40 * 1024 || W / 2 >= op->n)) W >>= 1;
   return W;
@@ -919,8 +919,7 @@ static int launch_tile1(Op* op, const float2* C, const int* seg, int nb, int gri
                                                              Ymeas, w, Y, pp);                 \
   } while (0)
   if (mode == 0) CBB_T1(0);
-  else if (mode == 1) CBB_T1(1);
-  else CBB_T1(2);
+  else CBB_T1(1);
 #undef CBB_T1
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
@@ -1047,7 +1046,7 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
   else if (Ymeas != nullptr) mode = 2;
   double* pp = (mode != 0 || norm_out) ? part : nullptr;
   int launches = 2;
-  const int W = tile_width(op, s);
+  const int W = tile_width(op, s, mode);
   const int nb = int((op->n + W - 1) / W);
   // location-tiled gather straight from the channel-planar FFT output, when there are enough
   // tiles to fill the GPU (cfg0's 4096 locations are 8 tiles: sample-major below)
@@ -1064,8 +1063,9 @@ int op_apply_compressed(Op* op, const float2* Xc, const float2* V, int s, float2
     int grid = 8 * sms;
     if (grid > kTileBlocks) grid = kTileBlocks;
     if (grid > nb) grid = nb;
-    if (op->c == 1) {
-      // single coil: compile-time (S, W) kernel, 512 threads; CTAs per SM by shared memory
+    if (op->c == 1 && mode != 2) {
+      // single coil, store / norm-only (the fused-residual mode is not reachable through the C
+      // ABI and stays on the generic kernel): compile-time (S, W) kernel, 512 threads
       const int S = padded_s(s);
       const int per_sm = int((200 * 1024) / (size_t(S) * W * sizeof(float2)));
       grid = sms * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));

@@ -606,14 +606,22 @@ __global__ void __launch_bounds__(256) coherence_kernel(const float* __restrict_
 // value bounded by sum|products| (<= ||z~|| ||d~||), i.e. (KP/16) * 2^-11, plus slack for
 // internal alignment and fp16 subnormals.  window = 2 * bound: the true argmax j* satisfies
 // s~_j* >= max s~ - window.  The FFMA window (win32) is in unscaled fp32 units.
-__global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int kpad,
+// S > 0: compile-time signature length (the BASELINE ranks 10 and 20): the component loops unroll
+// and the fp16 row stays in registers; S == 0: runtime s.  Same arithmetic in the same order.
+// SP: the split flag at compile time too (with S > 0 the row width and every row index are
+// constants); -1: runtime.
+template <int S, int SP = -1>
+__global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s_arg, int kpad_arg,
                                 const float* __restrict__ bounds, uint8_t* __restrict__ ztiles,
                                 float* __restrict__ win_tc, float* __restrict__ win32,
                                 int s_pad, const double2* __restrict__ atoms64,
-                                int64_t d_atoms, float* __restrict__ init_tc, int split,
+                                int64_t d_atoms, float* __restrict__ init_tc, int split_arg,
                                 float2* __restrict__ lbz, int32_t* __restrict__ hbest) {
   const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= n_pad) return;
+  const int s = S > 0 ? S : s_arg;
+  const int split = SP >= 0 ? SP : split_arg;
+  const int kpad = (S > 0 && SP >= 0) ? (SP == 1 ? split_kp(S) : (2 * S < 32 ? 32 : 64)) : kpad_arg;
   const float mu = zs.mu_ptr ? *zs.mu_ptr : zs.mu;
   // tile pruning: (exact hint score rounded down, ||z|| rounded up); zero and non-finite voxels
   // are decided without the screen (+inf: they need no atom tile)
@@ -629,6 +637,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   }
   // pass 1: Z (IPG: X - mu G, written to z_out) and its largest component magnitude
   double amax = 0;
+#pragma unroll
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (zs.x != nullptr) {
@@ -670,6 +679,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
   }
   // pass 2: norms and the fp32 rounding error (no under- / overflow for |z| in 2^[-80, 80])
   double nz = 0, ez32 = 0, nz32 = 0;
+#pragma unroll
   for (int k = 0; k < s; ++k) {
     const double2 z = load_z(zs, v, s, k);
     const double re = z.x, im = z.y;
@@ -689,6 +699,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
 #pragma unroll
   for (int e = 0; e < 128; ++e) row[e] = 0;
   double eh = 0, nzh = 0, nlo = 0, nhi = 0;
+#pragma unroll
   for (int k = 0; k < s; ++k) {
     double re, im;
     if (zs.x != nullptr) {
@@ -726,6 +737,7 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     }
   }
   row[split == 1 ? 6 * s : 2 * s] = kF16One;  // sentinel column right after the data (< kpad)
+#pragma unroll
   for (int c = 0; c < kpad / 8; ++c) {
     uint4 pk;
     pk.x = uint32_t(row[c * 8 + 0]) | (uint32_t(row[c * 8 + 1]) << 16);
@@ -789,6 +801,23 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s, int
     init_tc[v] = init;
   }
 }
+
+
+// prologue launch: compile-time signature length for the BASELINE ranks
+#define CBB_PROLOGUE(GRID, THREADS, ST, SVAL, SPLITVAL, KPVAL, ...)                            \
+  do {                                                                                         \
+    const int sv_ = (SVAL), sp_ = (SPLITVAL), kp_ = (KPVAL);                                   \
+    if (sv_ == 10 && sp_ == 1 && kp_ == 64)                                                    \
+      prologue_kernel<10, 1><<<(GRID), (THREADS), 0, (ST)>>>(__VA_ARGS__);                     \
+    else if (sv_ == 10 && sp_ == 0 && kp_ == 32)                                               \
+      prologue_kernel<10, 0><<<(GRID), (THREADS), 0, (ST)>>>(__VA_ARGS__);                     \
+    else if (sv_ == 20 && sp_ == 1 && kp_ == 128)                                              \
+      prologue_kernel<20, 1><<<(GRID), (THREADS), 0, (ST)>>>(__VA_ARGS__);                     \
+    else if (sv_ == 20 && sp_ == 0 && kp_ == 64)                                               \
+      prologue_kernel<20, 0><<<(GRID), (THREADS), 0, (ST)>>>(__VA_ARGS__);                     \
+    else                                                                                       \
+      prologue_kernel<0><<<(GRID), (THREADS), 0, (ST)>>>(__VA_ARGS__);                         \
+  } while (0)
 
 // ============================================================== FFMA screening
 template <int S>
@@ -3213,7 +3242,8 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   if (algo == 1 || algo == 2) {
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
-    prologue_kernel<<<int((n_pad + threads - 1) / threads), threads, 0, st>>>(
+    CBB_PROLOGUE(int((n_pad + threads - 1) / threads), threads, st, dv.s, split ? 1 : 0,
+        split ? split_kp(dv.s) : dv.kpad,
         zs, n, n_pad, dv.s, split ? split_kp(dv.s) : dv.kpad, dv.bounds,
         algo == 1 ? w.ztiles : nullptr, w.win_tc, w.win32, dv.s_pad, dv.atoms64, dv.d,
         algo == 1 ? w.init_tc : nullptr, split ? 1 : 0, prune ? w.lbz : nullptr,
@@ -3253,7 +3283,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
     if (zs.x != nullptr) {
       // materialise Z = X - mu G (same fp32 rounding as the prologue)
       const int64_t n_pad = n;
-      prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
+      CBB_PROLOGUE(int((n_pad + 255) / 256), 256, st, dv.s, 0, dv.kpad, zs, n, n_pad, dv.s, dv.kpad,
                                                                dv.bounds, nullptr, nullptr,
                                                                nullptr, dv.s_pad, dv.atoms64,
                                                                dv.d, nullptr, 0, nullptr,
@@ -3391,7 +3421,7 @@ int prologue_only(const ZSource& zs, int64_t n, const DictView& dv, void* ws_ptr
   ProjWs w;
   project_ws_bytes(n, dv.s, &w, ws_ptr, 0);
   const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
-  prologue_kernel<<<int((n_pad + 255) / 256), 256, 0, st>>>(zs, n, n_pad, dv.s, dv.kpad,
+  CBB_PROLOGUE(int((n_pad + 255) / 256), 256, st, dv.s, 0, dv.kpad, zs, n, n_pad, dv.s, dv.kpad,
                                                              dv.bounds, w.ztiles, w.win_tc,
                                                              w.win32, dv.s_pad, dv.atoms64, dv.d,
                                                              w.init_tc, 0, nullptr, nullptr);
