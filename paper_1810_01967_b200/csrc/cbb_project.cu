@@ -523,6 +523,22 @@ __global__ void prep_tc2_kernel(const double2* __restrict__ atoms64, int64_t d, 
 // Centroid rows of the tile-pruning bound pass: row t = split-operand row of the fp32 centroid c_t
 // (same layout and scale_d as prep_tc2_kernel, no bound updates: the bound pass carries its own
 // margin), rs[t] = ru(scale_d r_t); rows >= nt are sentinel rows (score -65504).
+// Folded bound (tile pruning): when the split rows have three spare K columns after the sentinel
+// (6s + 4 <= kp: every s <= 20 except none; s = 21 has one), the bound pass's test
+//   fl(zn r_t + s~) >= lb'   becomes the sign of one accumulator: the voxel rows carry
+//   [ru16(zn), hi16(lb'), lo16(lb')] in those columns (hi + lo <= lb', lo rounded down) and the
+//   centroid rows [ru16(scale_d r_t), -1, -1], so the MMA returns s~ + zn r_t - lb' itself (the
+//   products are exact in the fp32 accumulator; ru / rd only loosen the bound, the truncation of
+//   the K = 16 step that holds them, <= 16 x 2^-24 x 2^13, is far inside lb's margin of >= 1).
+//   Atom rows are zero in these columns: the screens are unchanged.
+__host__ __device__ constexpr bool bound_folds(int s) { return 6 * s + 4 <= split_kp(s); }
+__device__ __forceinline__ unsigned short f16_bits_ru(float x) {
+  return __half_as_ushort(__float2half_ru(x));
+}
+__device__ __forceinline__ unsigned short f16_bits_rd(float x) {
+  return __half_as_ushort(__float2half_rd(x));
+}
+
 __global__ void prep_ctr_kernel(const float* __restrict__ cen, const float* __restrict__ rad,
                                 int nt, int rows_alloc, int s, int sp,
                                 const float* __restrict__ bounds, uint8_t* __restrict__ out,
@@ -542,6 +558,11 @@ __global__ void prep_ctr_kernel(const float* __restrict__ cen, const float* __re
   }
   const double sc = dict_scale(bounds);
   rs[t] = __double2float_ru(double(rad[t]) * sc);
+  if (bound_folds(s)) {
+    put(6 * s + 1, f16_bits_ru(rs[t]));
+    put(6 * s + 2, 0xBC00);  // -1.0
+    put(6 * s + 3, 0xBC00);
+  }
   for (int k = 0; k < s; ++k) {
     const double x[2] = {double(cen[size_t(t) * 2 * sp + k]) * sc,
                          double(cen[size_t(t) * 2 * sp + sp + k]) * sc};
@@ -788,15 +809,26 @@ __global__ void prologue_kernel(ZSource zs, int64_t n, int64_t n_pad, int s_arg,
       }
     }
     if (hbest) hbest[v] = int32_t(jh);
+    float2 lz = make_float2(-INFINITY, __double2float_ru(sqrt(nz) * sv));
     if (jh >= 0) {
       init = __double2float_rd(acc * sv * sd - eb * 1.001);
-      if (lbz) {  // scaled units of the tile-pruning bound pass (see prune_prepare)
-        const double zn_s = sqrt(nz) * sv;
-        lbz[v] = make_float2(__double2float_rd(acc * sv * sd - 0x1p-11 * zn_s * sd * dmax),
-                             __double2float_ru(zn_s));
+      // scaled units of the tile-pruning bound pass (see prune_prepare)
+      lz.x = __double2float_rd(acc * sv * sd - 0x1p-11 * double(lz.y) * sd * dmax);
+    }
+    if (lbz) {
+      lbz[v] = lz;
+      if (split == 1 && bound_folds(s)) {  // folded bound columns (see bound_folds)
+        // no hint (lb = -inf): -65504 keeps every tile (|s~| <= 2^13); infinities never enter
+        // the rows (inf x 0 against the atom rows' zero columns would poison the screen)
+        const bool fin = fabsf(lz.x) <= 60000.f;
+        const unsigned short hi = fin ? __half_as_ushort(__float2half_rn(lz.x))
+                                      : (lz.x > 0.f ? 0x7BFF : 0xFBFF);
+        const float rem = fin ? lz.x - __half2float(__ushort_as_half(hi)) : 0.f;
+        unsigned short* fold = reinterpret_cast<unsigned short*>(trow) + 6 * s + 1;
+        fold[0] = f16_bits_ru(lz.y);
+        fold[1] = hi;
+        fold[2] = f16_bits_rd(rem);
       }
-    } else if (lbz) {
-      lbz[v] = make_float2(-INFINITY, __double2float_ru(sqrt(nz) * sv));
     }
     init_tc[v] = init;
   }
@@ -1783,6 +1815,11 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
         // (the tile's 32-centroid words) into the voxel tile's global need mask
         const float2 lz = live ? lbz[v] : make_float2(INFINITY, 0.f);
         uint32_t* vbits = bnd_bits + size_t(vt) * bnd_words;
+        // folded form (bnd_rs == nullptr, see bound_folds): the accumulator holds
+        // s~ + zn r - lb' itself, need = its sign bit clear; voxels that need nothing (zero /
+        // non-finite / padding rows: lb = +inf) are masked here
+        const bool fold = bnd_rs == nullptr;
+        const uint32_t want = lz.x < INFINITY ? 0xffffffffu : 0u;
         for (; kk < kend; kk += kParts) {
           const int ba = int(kk - kb);  // centroid tile
           mbar_wait(t_full + tb, ph);
@@ -1810,6 +1847,18 @@ __global__ void __launch_bounds__(TcCfg<KP, SPLIT>::kThreads, 1)
                 mbar_arrive(C::kHalves && h == 1 ? acc_free2 + part : acc_free + part);
             }
             const int col0 = ba * BN + 32 * kRegChunks * h;
+            if (fold) {
+#pragma unroll
+              for (int c = 0; c < kRegChunks; ++c) {
+                uint32_t neg = 0;  // bit 31 - i = sign of centroid i (one funnel shift each)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) neg = __funnelshift_l(r[32 * c + i], neg, 1);
+                uint32_t wbits = ~__brev(neg) & want;
+                wbits = __reduce_or_sync(0xffffffffu, wbits);
+                if (lane == 0 && wbits) atomicOr(vbits + (col0 >> 5) + c, wbits);
+              }
+              continue;
+            }
             const float4* rs4 = reinterpret_cast<const float4*>(bnd_rs + col0);
 #pragma unroll
             for (int c = 0; c < kRegChunks; ++c) {
@@ -3028,7 +3077,7 @@ static int launch_bound(const ProjWs& w, int64_t n, const DictView& dv, cudaStre
   mf_tc_kernel<KP, true, false, false, true><<<grid, C::kThreads, C::kSmem, st>>>(
       w.ztiles, n, n_vt, (const float*)w.win_tc, (const float*)w.init_tc, cv, w.n_pad, w.cand,
       w.meta, (const uint8_t*)w.hint_tiles, 0, 1, w.vperm, nullptr, nullptr, 0, w.lbz,
-      dv.tile_rs, w.pbits, (dv.n_tiles2 + 31) / 32 + 4);
+      bound_folds(dv.s) ? nullptr : dv.tile_rs, w.pbits, (dv.n_tiles2 + 31) / 32 + 4);
   CBB_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
