@@ -2,7 +2,7 @@
 # bench, ncu --set full of the cfg1 screen and of a pruned split screen inside the cfg4 IPG.
 export PYTHONPATH=.
 mkdir -p gpurun_out
-R=${R:-r02g}
+R=${R:-r02h}
 timeout 1200 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${R}_reference.json 2> gpurun_out/bench_${R}_reference.err; echo "ref rc=$?"
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"mf_tc|mf_ffma|rescore|prologue|gather|kspace|combine_s|channels|interleave|vec_kernel|scale_kernel|hint_tiles|prune_|exhaustive|reduce_stage|finish_sum|trial_|map_indices|coil_transpose|scatter_kernel|coherence|seg_table|rows_sorted|prep_|argmax_select|scaled_rows|_fft|DeviceRadixSort" --csv --log-file gpurun_out/bench_launches_$R.csv python bench.py --steps 3 --warmup 3 --skip-cfg3 --skip-cpu-reference > gpurun_out/ncu_launch_$R.log 2>&1
