@@ -300,6 +300,38 @@ def cpu_reference_legs():
     return out
 
 
+def cpu_ipg_model(which, res, cpu_macs_per_s):
+    """Modelled CPU time of one reference IPG iteration at BASELINE configs[2] / configs[4]
+    (solver.py:208-252: per iteration r projections, 2 + r applies and 1 adjoint, each operator
+    call L per-frame FFTs, forward_model.py:123-167): the exact projection at this run's measured
+    CPU rate (complex128 zgemm + argmax, all host cores) plus L numpy FFTs per operator call at
+    the time of one frame's complex128 FFT measured here.  An estimate, not a run."""
+    spec = LARGE_IPG[which]
+    shape = {"cfg2": (256, 256), "cfg4": (256, 256, 64)}[which]
+    L = {"cfg2": 1000, "cfg4": 500}[which]
+    D = int(res["parity"]["first"]["D"]) if "parity" in res else None
+    if D is None:
+        return {"note": "dictionary size unavailable"}
+    n, s = int(np.prod(shape)), spec["s"]
+    r = res["projection_trials"] / max(1, res["iterations"])
+    rng = np.random.default_rng(0)
+    frame = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    np.fft.fftn(frame, norm="ortho")
+    t0 = time.perf_counter()
+    reps = 3 if n <= 1 << 16 else 1
+    for _ in range(reps):
+        np.fft.fftn(frame, norm="ortho")
+    t_fft = (time.perf_counter() - t0) / reps
+    t_proj = r * n * D * 2.0 * s / cpu_macs_per_s
+    t_op = (3.0 + r) * L * t_fft
+    return {"kind": "model", "ms_per_iter": 1e3 * (t_proj + t_op),
+            "projection_ms": 1e3 * t_proj, "operator_ms": 1e3 * t_op,
+            "frame_fft_ms": 1e3 * t_fft, "trials_per_iter": r,
+            "basis": "r n D 2s MACs at the measured CPU exact-projection rate + (3 + r) L "
+                     "per-frame complex128 numpy FFTs (one frame timed here); not run",
+            "speedup_vs_model": (t_proj + t_op) / (1e-3 * res["ms_per_iter"])}
+
+
 class _OracleOp:
     """cfg0 Cartesian operator of the oracle restatement (fallback CPU IPG leg)."""
 
@@ -806,6 +838,14 @@ def run_ours(args, rank, world, local_rank, group):
             line["ipg"] = ipg_rate(dev)
         except Exception as exc:  # report, never hide
             line["ipg"] = {"error": repr(exc)}
+        # CPU denominators of the large IPG legs: not run (one cfg2 iteration of the reference
+        # takes minutes on the host), modelled from rates measured in this run
+        try:
+            for which, res in ipg_large.items():
+                if "error" not in res:
+                    res["cpu_model"] = cpu_ipg_model(which, res, line["cpu_baseline"]["value"])
+        except Exception as exc:
+            line["cpu_baseline"]["ipg_model_error"] = repr(exc)
     if cfg3 is not None and "parity" in cfg3:
         parity["cfg3"] = cfg3["parity"]
     for which, res in ipg_large.items():
