@@ -2820,9 +2820,10 @@ size_t project_ws_bytes(int64_t n, int s, ProjWs* ws, void* base_ptr, int prune_
   w.win_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.init_tc = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
   w.win32 = reinterpret_cast<float*>(take(size_t(n_vt) * kVoxPad * 4));
-  w.ovf_count = reinterpret_cast<int*>(take(16));
+  w.ovf_count = reinterpret_cast<int*>(take(16));   // both counters in one 16-byte block:
+  w.heavy_count = w.ovf_count ? w.ovf_count + 2 : nullptr;  // one memset node per projection
   w.ovf_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
-  w.heavy_count = reinterpret_cast<int*>(take(16));
+  take(16);  // (layout kept)
   w.heavy_list = reinterpret_cast<int64_t*>(take(size_t(n) * 8));
   w.exh_partial = reinterpret_cast<double2*>(take(size_t(n) * kExhSplits * sizeof(double2)));
   {  // hint tiles: the largest per-voxel-tile block of the screens this s can use
@@ -3286,8 +3287,7 @@ int project(const ZSource& zs, int64_t n, const DictView& dv, const ProjOut& out
   }
   // records of the split screen hold split-tile positions: the rescoring maps them to atoms
   const int32_t* amap = split ? dv.tc2_atom : nullptr;
-  CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, sizeof(int), st));
-  CBB_CUDA_TRY(cudaMemsetAsync(w.heavy_count, 0, sizeof(int), st));
+  CBB_CUDA_TRY(cudaMemsetAsync(w.ovf_count, 0, 16, st));  // ovf_count and heavy_count
   if (algo == 1 || algo == 2) {
     const int64_t n_pad = ((n + kVoxPad - 1) / kVoxPad) * kVoxPad;
     const int threads = 256;
