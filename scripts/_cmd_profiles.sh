@@ -16,6 +16,6 @@ echo "ncu split rc=$?"
 python scripts/summarize_ncu.py full /tmp/prof_split_pruned_$R.ncu-rep gpurun_out/mf_tc_split_pruned_cfg4_ncu_full_$R.txt gpurun_out/split_traffic_$R.json "ncu --set full, launch 15 of mf_tc_kernel in probe_ipg cfg4 8 nograph (a pruned split screen, iteration ~7)" > /dev/null
 rm -f gpurun_out/*.ncu-rep
 du -sh gpurun_out; ls gpurun_out/*$R*
-R=$R bash scripts/_cmd_r02_opncu2.sh > gpurun_out/opncu_$R.log 2>&1; echo "op ncu rc=$?"
-R=$R bash scripts/_cmd_r02_ipglist.sh > gpurun_out/ipglist_$R.log 2>&1; echo "ipg list rc=$?"
+R=$R bash scripts/_cmd_opncu.sh > gpurun_out/opncu_$R.log 2>&1; echo "op ncu rc=$?"
+R=$R bash scripts/_cmd_ipglist.sh > gpurun_out/ipglist_$R.log 2>&1; echo "ipg list rc=$?"
 ls gpurun_out/*$R*

@@ -28,3 +28,19 @@ def test_pipeline_bounds_cover_and_align(n):
         assert sizes[:3] == [1, 2, 4]
         assert max(sizes) <= 8 and (total < 22 or max(sizes) == 8)
         assert sizes[-3:-1] == [4, 2] and b[-1][1] - b[-1][0] <= unit
+
+
+def test_bench_cpu_ipg_model_fields():
+    """bench.cpu_ipg_model: the modelled CPU denominators of the large IPG legs (projection at
+    the measured CPU rate + per-frame FFTs) are finite, positive and consistent."""
+    import bench
+    res = {"parity": {"first": {"D": 120624}}, "projection_trials": 52, "iterations": 22,
+           "ms_per_iter": 2.3}
+    m = bench.cpu_ipg_model("cfg2", res, 5.0e9)
+    assert m["kind"] == "model"
+    assert m["projection_ms"] > 0 and m["operator_ms"] > 0
+    assert abs(m["ms_per_iter"] - (m["projection_ms"] + m["operator_ms"])) < 1e-6 * m["ms_per_iter"]
+    # r n D 2s / rate
+    r = 52 / 22
+    assert abs(m["projection_ms"] - 1e3 * r * 65536 * 120624 * 40 / 5.0e9) < 1e-6 * m["projection_ms"]
+    assert abs(m["speedup_vs_model"] - m["ms_per_iter"] / 2.3) < 1e-6 * m["speedup_vs_model"]
