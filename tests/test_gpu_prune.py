@@ -100,10 +100,21 @@ def _assert_same(a, b):
     assert a["nd"] == b["nd"]
 
 
-@pytest.mark.parametrize("s", [10, 20])
-@pytest.mark.parametrize("noise", [0.01, 0.1, 0.5])
+_atoms_cache = {}
+
+
+def _atoms_for(s):
+    if s not in _atoms_cache:
+        _atoms_cache[s] = _coherent(s=s)
+    return _atoms_cache[s]
+
+
+@pytest.mark.parametrize("s,noise", [(10, 0.01), (10, 0.1), (10, 0.5), (20, 0.01), (20, 0.1),
+                                     (20, 0.5), (8, 0.1), (21, 0.1)])
 def test_pruned_step_equals_exhaustive(atoms10, atoms20, s, noise):
-    atoms = atoms10 if s == 10 else atoms20
+    """s = 8, 10, 20: the bound pass folded into the MMA (three spare K columns); s = 21: no
+    spare columns, the epilogue evaluates the bound itself."""
+    atoms = atoms10 if s == 10 else atoms20 if s == 20 else _atoms_for(s)
     rng = np.random.default_rng(int(noise * 1000) + s)
     n = 20000
     X, G, j = _state(rng, atoms, n, noise)
