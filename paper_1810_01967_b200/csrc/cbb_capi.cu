@@ -227,6 +227,12 @@ int cbb_project_step_ex(const void* x, const void* g, double mu, const float* mu
   return project(zs, n, to_view(dict), o, nd_out, workspace, workspace_bytes, algo, 0, S(stream));
 }
 
+// The representatives sit about one tile radius apart: far outside the fp16 screen's window, so
+// the cheaper fp16 screen (algo 1) serves them even though the dictionary they come from is
+// coherent (auto mode would pick the split screen for them too).  Small representative sets fall
+// back to auto (the tcgen05 screens need d > 320).
+static int rep_algo(const cbb_dict_view* reps) { return (reps->d > 320 && 2 * reps->s < 64) ? 1 : 0; }
+
 int cbb_project_hint(const void* x, const void* g, double mu, const float* mu_dev, void* z_out,
                      int64_t n, const cbb_dict_view* reps, const int32_t* rep_atoms,
                      int32_t* hint_out, void* workspace, size_t workspace_bytes, void* stream) {
@@ -238,7 +244,7 @@ int cbb_project_hint(const void* x, const void* g, double mu, const float* mu_de
   ZSource zs{nullptr, 0, static_cast<const float2*>(x), static_cast<const float2*>(g), float(mu),
              static_cast<float2*>(z_out), nullptr, mu_dev, nullptr};
   ProjOut o{hint_out, 0, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0};
-  if (int rc = project(zs, n, to_view(reps), o, nullptr, workspace, workspace_bytes, 0, 0,
+  if (int rc = project(zs, n, to_view(reps), o, nullptr, workspace, workspace_bytes, rep_algo(reps), 0,
                        S(stream)))
     return rc;
   return map_indices(hint_out, rep_atoms, n, reps->d, S(stream));
